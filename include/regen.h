@@ -1,0 +1,206 @@
+/*
+ * regen.h — C-ABI of the B200 (sm_100a) region-aware enhancement hot path of RegenHance
+ * (arXiv 2407.16990). Implemented by paper_2407_16990_b200/libregen.so.
+ *
+ * Citations: P:<line> = PAPER.md line, readings D1..D12 = DESIGN.md §3.
+ *
+ * Conventions (all calls):
+ *  - Pointers prefixed d_ are DEVICE pointers (cudaMalloc / torch CUDA tensors) on the current
+ *    device; h_ are host pointers. The caller owns every buffer, including the workspace d_ws
+ *    (size from regen_workspace_size). The library owns only the SR handle.
+ *  - Every call is stream-ordered on `stream` (a cudaStream_t passed as void*), never
+ *    synchronises the host, and is capturable in a CUDA graph.
+ *  - Synchronous argument errors (null pointer, bad size/mode, too small workspace) return
+ *    REGEN_E_INVALID (or REGEN_E_UNSUPPORTED) before any launch; regen_last_error() gives a
+ *    thread-local message. Launch failures return REGEN_E_CUDA.
+ *  - Data-dependent overflow (more regions/boxes than the caller's capacity, packer free-list
+ *    full) is reported asynchronously by OR-ing REGEN_ST_* bits into *d_status (int32, device);
+ *    outputs are then truncated deterministically. Unplaced boxes are NOT an error: their
+ *    MBs keep the bilinear value.
+ *  - Determinism: identical inputs give bit-identical integer outputs (selection, labels, boxes,
+ *    densities, order, placements, owners), independent of launch configuration; they equal the
+ *    CPU oracle (oracle/) bit for bit.
+ *  - A "call" processes one selection group: S streams x F frames of frame_w x frame_h pixels.
+ */
+#ifndef REGEN_H_
+#define REGEN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define REGEN_API __attribute__((visibility("default")))
+#else
+#define REGEN_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  REGEN_OK = 0,
+  REGEN_E_INVALID = 1,
+  REGEN_E_CAPACITY = 2,
+  REGEN_E_CUDA = 3,
+  REGEN_E_UNSUPPORTED = 4
+} regen_status;
+
+enum { REGEN_MODE_TOPK = 0, REGEN_MODE_THRESHOLD = 1 };
+enum { REGEN_SCOPE_GLOBAL = 0, REGEN_SCOPE_PER_STREAM = 1, REGEN_SCOPE_PER_FRAME = 2 };
+enum { REGEN_ORDER_DENSITY = 0, REGEN_ORDER_AREA = 1 };
+enum { REGEN_DTYPE_BF16 = 0, REGEN_DTYPE_FP32 = 1 };
+enum { REGEN_CALL_SELECT = 0, REGEN_CALL_PACK = 1, REGEN_CALL_ENHANCE = 2, REGEN_CALL_SCATTER = 3 };
+
+/* asynchronous status bits (*d_status) */
+enum {
+  REGEN_ST_REGION_OVERFLOW = 1,   /* num_regions > max_regions */
+  REGEN_ST_BOX_OVERFLOW = 2,      /* num_boxes > max_boxes */
+  REGEN_ST_FREELIST_OVERFLOW = 4  /* packer free-area pool full: remaining boxes left unplaced */
+};
+
+/* Frame geometry. MB grid GW = ceil(frame_w/mb), GH = ceil(frame_h/mb) (D1); mb = 16. */
+typedef struct {
+  int32_t S, F;               /* streams, frames per stream in this call */
+  int32_t frame_w, frame_h;   /* LR frame size in pixels */
+  int32_t mb;                 /* macroblock size, 16 */
+} regen_geom;
+
+/* Cross-stream MB selection, §3.3.1 P:638-667 (D2). */
+typedef struct {
+  int32_t mode;          /* REGEN_MODE_TOPK: the k best MBs; REGEN_MODE_THRESHOLD: score >= tau */
+  int32_t scope;         /* GLOBAL: one queue over the call; PER_STREAM (Uniform); PER_FRAME */
+  int64_t k;             /* TOPK: count per scope segment (>= 0). THRESHOLD: cap (-1 = none) */
+  float tau;             /* THRESHOLD only; must not be NaN */
+  int32_t connectivity;  /* 8 (default, D3) or 4 */
+} regen_select_params;
+
+/* Region-aware bin packing, Alg. 1 P:677-719 (D4-D8, D12). */
+typedef struct {
+  int32_t bin_w, bin_h;    /* H x W of the bins; bin_w >= 4 */
+  int32_t max_bins;        /* B: bins available; boxes beyond stay bilinear */
+  int32_t expand;          /* pixels of expansion around a box, 3 */
+  int32_t partition_mb;    /* Partition preset size in MBs (D5): 4 for 128-px bins, 3 for 64-px */
+  int32_t gutter;          /* zero gutter right/below each box (D8), 1 */
+  int32_t order;           /* REGEN_ORDER_DENSITY (Alg. 1 l.6) or REGEN_ORDER_AREA (max-area-first) */
+} regen_pack_params;
+
+/* SR network (D11): EDSR-baseline, or the tiny 2-conv model when n_resblocks == 0. */
+typedef struct {
+  int32_t scale;        /* 2, 3 or 4 */
+  int32_t channels;     /* C: 8..64, multiple of 8 (tiny model: 8..64) */
+  int32_t n_resblocks;  /* 0 => tiny model: conv 3->C, ReLU, conv C->3s^2, PixelShuffle(s) */
+  int32_t dtype;        /* REGEN_DTYPE_BF16 (tcgen05, bf16 storage, fp32 accumulate) or REGEN_DTYPE_FP32 */
+  float res_scale;      /* residual scaling, 1.0 */
+} regen_sr_config;
+
+/* Region record (Alg. 1 l.3): id order = (stream, frame, smallest raster index) (D3). 32 bytes. */
+typedef struct {
+  int32_t stream, frame;
+  int32_t root;                 /* smallest raster index gy*GW+gx of the region in its frame */
+  int32_t mx0, my0, mx1, my1;   /* MB bounding span, half-open */
+  int32_t n_members;
+} regen_region;
+
+/* Box record (Alg. 1 l.4-6 + the packing plan, l.12). Index = creation order (region id, then
+ * partition pieces in raster order). 80 bytes. */
+typedef struct {
+  int32_t stream, frame;
+  int32_t mx0, my0, mx1, my1;   /* MB span after partition and re-bounding (D5), half-open */
+  int32_t x0, y0, w, h;         /* LR pixel box after 3-px expansion, clamped to the frame */
+  int32_t n_members;            /* member MBs (selected MBs of its region inside the span) */
+  int32_t region;               /* region id */
+  double density;               /* mean importance over the MB span, fp64 raster-order sum (D4) */
+  int32_t bin, bx, by;          /* placement: bin index and top-left in the bin; bin = -1: unplaced */
+  int32_t rotated;              /* 1: stored rotated 90 deg clockwise in the bin (D7) */
+  int32_t rank;                 /* position in the packing order */
+  int32_t reserved;
+} regen_box;
+
+/* ---------------------------------------------------------------------------------------------
+ * a1+a2. Select MBs and grow regions. §3.3.1; Alg. 1 l.3 P:688.
+ *   d_importance  [S][F][GH][GW] fp32 scores (in)
+ *   d_sel_bitmap  [S][F][GH][ceil(GW/32)] u32; bit gx%32 of word gx/32 = MB selected (out)
+ *   d_labels      [S][F][GH][GW] int32 region id of each selected MB, -1 otherwise (out)
+ *   d_regions     [max_regions] region records (out); d_num_regions: int64 count (out, may exceed
+ *                 max_regions => REGEN_ST_REGION_OVERFLOW and records truncated)
+ * ------------------------------------------------------------------------------------------- */
+REGEN_API regen_status regen_select_mbs(const regen_geom* geom, const regen_select_params* params,
+                              const float* d_importance, uint32_t* d_sel_bitmap, int32_t* d_labels,
+                              regen_region* d_regions, int64_t max_regions, int64_t* d_num_regions,
+                              int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * a3-a5. Bound + expand + partition + density, sort, pack. Alg. 1 l.4-21 P:689-717, Alg. 2.
+ *   in : d_importance, d_labels, d_regions, d_num_regions (from regen_select_mbs)
+ *   out: d_boxes [max_boxes] (creation order, placement filled in), d_num_boxes (int64),
+ *        d_order [max_boxes] int32 box indices in packing order, d_num_bins (int32, 1 + highest
+ *        bin used), d_mb_owner [S][F][GH][GW] int32: index of the placed box owning each selected
+ *        MB, -1 if unselected or its box is unplaced (D9).
+ * ------------------------------------------------------------------------------------------- */
+REGEN_API regen_status regen_pack_regions(const regen_geom* geom, const regen_pack_params* params,
+                                const float* d_importance, const int32_t* d_labels,
+                                const regen_region* d_regions, const int64_t* d_num_regions,
+                                regen_box* d_boxes, int64_t max_boxes, int64_t* d_num_boxes,
+                                int32_t* d_order, int32_t* d_num_bins, int32_t* d_mb_owner,
+                                int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * SR network handle. h_weights: host fp32, per conv W[Cout][Cin][3][3] then bias[Cout], in
+ * network order (D11): head, 2 per resblock, body, upsampler conv(s), tail; tiny: conv0, conv1.
+ * n_weights must equal the sum. Weights are repacked once (bf16 per-tap tensor-core layout for
+ * BF16) and copied to the device; the caller's buffer may be freed afterwards. Not stream-ordered.
+ * ------------------------------------------------------------------------------------------- */
+REGEN_API regen_status regen_sr_create(const regen_sr_config* cfg, const float* h_weights, size_t n_weights,
+                             void** out_handle);
+REGEN_API regen_status regen_sr_destroy(void* handle);
+
+/* ---------------------------------------------------------------------------------------------
+ * a6. Stitch regions into bins, the first stage of regen_enhance_packed, exposed alone.
+ *   d_frames  [S][F][frame_h][frame_w][3] u8 RGB (in)
+ *   d_lr_bins [max_bins][bin_h][bin_w][4] (dtype: bf16 or fp32): channels 0..2 = bf16(u8/255) or
+ *             fp32(u8/255) (D9) inside placed boxes (rotated per D7), 0 elsewhere; channel 3 = 0.
+ * Bins >= *d_num_bins are not written. max_boxes = capacity of d_boxes (as given to
+ * regen_pack_regions). Workspace: regen_workspace_size(REGEN_CALL_ENHANCE, ...) suffices.
+ * ------------------------------------------------------------------------------------------- */
+REGEN_API regen_status regen_stitch_bins(const regen_geom* geom, const regen_pack_params* params, int32_t dtype,
+                               const uint8_t* d_frames, const regen_box* d_boxes, int64_t max_boxes,
+                               const int64_t* d_num_boxes, const int32_t* d_num_bins, void* d_lr_bins,
+                               void* d_ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * a6+a7. Gather the placed boxes into packed bins and run the SR network over the packed batch.
+ *   d_hr_bins [max_bins][scale*bin_h][scale*bin_w][4] (bf16 for BF16, fp32 for FP32): channels
+ *             0..2 = SR output, each box equal to SR of the box alone with zero padding (D8);
+ *             0 outside boxes; channel 3 = 0. Bins >= *d_num_bins are not written.
+ * ------------------------------------------------------------------------------------------- */
+REGEN_API regen_status regen_enhance_packed(void* sr, const regen_geom* geom, const regen_pack_params* params,
+                                  const uint8_t* d_frames, const regen_box* d_boxes, int64_t max_boxes,
+                                  const int64_t* d_num_boxes, const int32_t* d_num_bins, void* d_hr_bins,
+                                  int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * a8. Scatter-and-blend (eq. P:461-464): d_out [S][F][scale*frame_h][scale*frame_w][3]
+ * (out_dtype bf16 or fp32) = bilinear x scale of u8/255 (D10), overwritten on the HR square of
+ * every MB with d_mb_owner >= 0 by that box's HR bin pixels (un-rotated).
+ * ------------------------------------------------------------------------------------------- */
+REGEN_API regen_status regen_scatter_blend(const regen_geom* geom, const regen_pack_params* params, int32_t scale,
+                                 const uint8_t* d_frames, const regen_box* d_boxes,
+                                 const int32_t* d_mb_owner, const void* d_hr_bins, int32_t hr_dtype,
+                                 void* d_out, int32_t out_dtype, void* stream);
+
+/* Workspace bytes for a call (which = REGEN_CALL_*; params = the call's params struct;
+ * sr = SR handle for ENHANCE, else NULL). */
+REGEN_API regen_status regen_workspace_size(int32_t which, const regen_geom* geom, const void* params, const void* sr,
+                                  size_t* bytes);
+
+/* Helpers. */
+REGEN_API int64_t regen_capacity_mbs(int32_t bin_w, int32_t bin_h, int32_t n_bins, int32_t mb);  /* floor(H*W*B/mb^2) */
+REGEN_API const char* regen_status_string(regen_status s);
+REGEN_API const char* regen_last_error(void);
+REGEN_API int32_t regen_abi_version(void);   /* 1 */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* REGEN_H_ */

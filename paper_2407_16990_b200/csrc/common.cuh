@@ -1,0 +1,123 @@
+// Internal helpers shared by the libregen CUDA sources (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/regen.h"
+
+namespace regen {
+
+void set_error(const char* fmt, ...);
+
+#define REGEN_REQUIRE(cond, ...)        \
+  do {                                  \
+    if (!(cond)) {                      \
+      ::regen::set_error(__VA_ARGS__);  \
+      return REGEN_E_INVALID;           \
+    }                                   \
+  } while (0)
+
+#define REGEN_CUDA(call)                                                              \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess) {                                                          \
+      ::regen::set_error("%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return REGEN_E_CUDA;                                                            \
+    }                                                                                 \
+  } while (0)
+
+#define REGEN_LAUNCH_CHECK()                                                          \
+  do {                                                                                \
+    cudaError_t e_ = cudaGetLastError();                                              \
+    if (e_ != cudaSuccess) {                                                          \
+      ::regen::set_error("launch: %s (%s:%d)", cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return REGEN_E_CUDA;                                                            \
+    }                                                                                 \
+  } while (0)
+
+inline int grid_w(const regen_geom& g) { return (g.frame_w + g.mb - 1) / g.mb; }
+inline int grid_h(const regen_geom& g) { return (g.frame_h + g.mb - 1) / g.mb; }
+inline int words_per_row(const regen_geom& g) { return (grid_w(g) + 31) / 32; }
+inline int64_t n_frames(const regen_geom& g) { return (int64_t)g.S * g.F; }
+inline int64_t n_mbs(const regen_geom& g) { return n_frames(g) * grid_h(g) * grid_w(g); }
+
+// Workspace carving: sequential 256-B aligned slices.
+struct Carver {
+  uint8_t* base;
+  size_t off = 0;
+  explicit Carver(void* b) : base((uint8_t*)b) {}
+  template <typename T>
+  T* take(size_t n) {
+    off = (off + 255) & ~(size_t)255;
+    T* p = base ? (T*)(base + off) : nullptr;
+    off += n * sizeof(T);
+    return p;
+  }
+};
+
+regen_status validate_geom(const regen_geom* g);
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ uint32_t score_ord(float s) {
+  uint32_t b = __float_as_uint(s);
+  if (s != s) return 0u;          // NaN lowest
+  if (s == 0.0f) b = 0u;          // -0 == +0
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+__device__ __forceinline__ uint64_t density_ord(double d) {
+  uint64_t b = (uint64_t)__double_as_longlong(d);
+  if (d != d) return 0ull;
+  if (d == 0.0) b = 0ull;
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+
+// Block-wide exclusive scan of one int per thread (blockDim.x <= 1024, multiple of 32).
+// `scratch` must hold 33 ints. Returns exclusive prefix; *total gets the block sum.
+__device__ __forceinline__ int block_exclusive_scan(int v, int* scratch, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) scratch[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < nw ? scratch[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) scratch[lane] = w;  // inclusive warp sums
+    if (lane == nw - 1) scratch[32] = w;
+  }
+  __syncthreads();
+  int res = x - v + (warp > 0 ? scratch[warp - 1] : 0);
+  *total = scratch[32];
+  __syncthreads();
+  return res;
+}
+
+}  // namespace regen

@@ -1,0 +1,453 @@
+// a6 + a7: stitch the placed boxes into packed bins (§3.3.3) and run the SR network
+// over the packed batch (reading D11), with the per-conv occupancy mask that makes every box
+// equal to SR of the box alone (reading D8).
+//
+// paint_kernel   one CTA per placed box writes its index over its bin footprint (the mask map).
+// gather_kernel  one thread per bin pixel: covering box -> source pixel (rotation D7) -> u8/255 ->
+//                bf16/fp32 chunk of 8 channels (3 real + 5 zero); zero outside boxes.
+// conv_simt      fp32 direct 3x3 conv (CUDA cores), the FP32 model path (C1) and the reference
+//                path for convs the tcgen05 kernel does not cover; same layout and epilogues.
+#include <math.h>
+
+#include <vector>
+
+#include "net.cuh"
+
+namespace regen {
+
+// ------------------------------------------------------------------------------------ handle
+
+static void build_convs(SRNet* net) {
+  const regen_sr_config& c = net->cfg;
+  const int C = c.channels, s = c.scale;
+  auto add = [&](int cin, int cout, int role, int ps, int res) {
+    ConvDesc d;
+    d.cin = cin;
+    d.cout = cout;
+    d.cin8 = (cin + 7) / 8;
+    d.role = role;
+    d.ps = ps;
+    d.res = res;
+    d.w_off = d.b_off = d.tc_off = 0;
+    d.tc_mode = 0;
+    net->convs.push_back(d);
+  };
+  if (c.n_resblocks == 0) {
+    add(3, C, ROLE_TINY0, 1, 1);
+    add(C, 3 * s * s, ROLE_TINY1, s, 1);
+    return;
+  }
+  add(3, C, ROLE_HEAD, 1, 1);
+  for (int i = 0; i < c.n_resblocks; ++i) {
+    add(C, C, ROLE_RES_A, 1, 1);
+    add(C, C, ROLE_RES_B, 1, 1);
+  }
+  add(C, C, ROLE_BODY, 1, 1);
+  if (s == 4) {
+    add(C, 4 * C, ROLE_UP, 2, 1);
+    add(C, 4 * C, ROLE_UP, 2, 2);
+  } else {
+    add(C, C * s * s, ROLE_UP, s, 1);
+  }
+  add(C, 3, ROLE_TAIL, 1, s);
+}
+
+static uint16_t f32_to_bf16_bits(float f) {
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+
+float round_bf16_host(float f) {
+  uint32_t u = (uint32_t)f32_to_bf16_bits(f) << 16;
+  float r;
+  memcpy(&r, &u, 4);
+  return r;
+}
+
+}  // namespace regen
+
+using namespace regen;
+
+extern "C" regen_status regen_sr_create(const regen_sr_config* cfg, const float* h_weights, size_t n_weights,
+                                        void** out_handle) {
+  REGEN_REQUIRE(cfg && h_weights && out_handle, "null argument");
+  REGEN_REQUIRE(cfg->scale == 2 || cfg->scale == 3 || cfg->scale == 4, "scale must be 2, 3 or 4");
+  REGEN_REQUIRE(cfg->channels >= 8 && cfg->channels <= 64 && cfg->channels % 8 == 0,
+                "channels must be a multiple of 8 in [8, 64]");
+  REGEN_REQUIRE(cfg->n_resblocks >= 0 && cfg->n_resblocks <= 64, "bad n_resblocks");
+  REGEN_REQUIRE(cfg->dtype == REGEN_DTYPE_BF16 || cfg->dtype == REGEN_DTYPE_FP32, "bad dtype");
+  REGEN_REQUIRE(!(cfg->res_scale != cfg->res_scale), "res_scale is NaN");
+  SRNet* net = new SRNet();
+  net->cfg = *cfg;
+  build_convs(net);
+  size_t need = 0;
+  for (auto& d : net->convs) need += (size_t)d.cout * d.cin * 9 + d.cout;
+  if (need != n_weights) {
+    set_error("n_weights %zu != %zu expected for this config", n_weights, need);
+    delete net;
+    return REGEN_E_INVALID;
+  }
+  // fp32 device weights: [cout][cin8*8][9] zero padded, biases after each conv
+  std::vector<float> w32;
+  size_t src = 0;
+  for (auto& d : net->convs) {
+    d.w_off = w32.size();
+    w32.resize(w32.size() + (size_t)d.cout * d.cin8 * 8 * 9, 0.0f);
+    for (int co = 0; co < d.cout; ++co)
+      for (int ci = 0; ci < d.cin; ++ci)
+        for (int t = 0; t < 9; ++t) {
+          float v = h_weights[src + ((size_t)co * d.cin + ci) * 9 + t];
+          if (cfg->dtype == REGEN_DTYPE_BF16) v = round_bf16_host(v);
+          w32[d.w_off + ((size_t)co * d.cin8 * 8 + ci) * 9 + t] = v;
+        }
+    src += (size_t)d.cout * d.cin * 9;
+    d.b_off = w32.size();
+    for (int co = 0; co < d.cout; ++co) w32.push_back(h_weights[src + co]);
+    src += d.cout;
+  }
+  cudaError_t e = cudaMalloc(&net->d_w32, w32.size() * sizeof(float));
+  if (e == cudaSuccess) e = cudaMemcpy(net->d_w32, w32.data(), w32.size() * sizeof(float), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    set_error("weights upload: %s", cudaGetErrorString(e));
+    cudaFree(net->d_w32);
+    delete net;
+    return REGEN_E_CUDA;
+  }
+  if (cfg->dtype == REGEN_DTYPE_BF16) {
+    regen_status st = conv_tc_prepare(net);
+    if (st != REGEN_OK) {
+      cudaFree(net->d_w32);
+      delete net;
+      return st;
+    }
+  }
+  *out_handle = net;
+  return REGEN_OK;
+}
+
+extern "C" regen_status regen_sr_destroy(void* handle) {
+  if (!handle) return REGEN_OK;
+  SRNet* net = (SRNet*)handle;
+  cudaFree(net->d_w32);
+  cudaFree(net->d_wtc);
+  delete net;
+  return REGEN_OK;
+}
+
+namespace regen {
+
+// ------------------------------------------------------------------------------------ stitch
+
+__global__ void paint_kernel(const regen_box* boxes, const int64_t* num_boxes, int64_t max_boxes, int32_t* map,
+                             int bin_w, int bin_h) {
+  const int64_t b = blockIdx.x;
+  if (b >= min(*num_boxes, max_boxes)) return;
+  const regen_box bx = boxes[b];
+  if (bx.bin < 0) return;
+  const int fw = bx.rotated ? bx.h : bx.w, fh = bx.rotated ? bx.w : bx.h;
+  int32_t* m = map + (int64_t)bx.bin * bin_w * bin_h;
+  for (int i = threadIdx.x; i < fw * fh; i += blockDim.x) {
+    const int q = i / fw, p = i - q * fw;
+    m[(bx.by + q) * bin_w + bx.bx + p] = (int32_t)b;
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T to_t(float v);
+template <>
+__device__ __forceinline__ float to_t<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 to_t<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+template <typename T>
+__device__ __forceinline__ float from_t(T v);
+template <>
+__device__ __forceinline__ float from_t<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ float from_t<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+// LAYOUT 0: activation layout chunk [bin][y][1][x][8]; LAYOUT 1: plain [bin][y][x][4]
+template <typename T, int LAYOUT>
+__global__ void gather_kernel(const uint8_t* frames, const regen_box* boxes, const int32_t* map,
+                              const int32_t* num_bins, int bin_w, int bin_h, int F, int W, int H, T* out) {
+  const int b = blockIdx.z;
+  if (b >= *num_bins) return;
+  const int y = blockIdx.y;
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= bin_w) return;
+  const int32_t id = map[((int64_t)b * bin_h + y) * bin_w + x];
+  float v[3] = {0.f, 0.f, 0.f};
+  if (id >= 0) {
+    const regen_box bx = boxes[id];
+    const int p = x - bx.bx, q = y - bx.by;
+    const int sx = bx.rotated ? bx.x0 + q : bx.x0 + p;
+    const int sy = bx.rotated ? bx.y0 + bx.h - 1 - p : bx.y0 + q;
+    const uint8_t* src = frames + ((((int64_t)bx.stream * F + bx.frame) * H + sy) * W + sx) * 3;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) v[c] = __fdiv_rn((float)src[c], 255.0f);
+  }
+  if (LAYOUT == 0) {
+    T* o = out + (((int64_t)b * bin_h + y) * bin_w + x) * 8;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) o[c] = to_t<T>(c < 3 ? v[c] : 0.0f);
+  } else {
+    T* o = out + (((int64_t)b * bin_h + y) * bin_w + x) * 4;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) o[c] = to_t<T>(c < 3 ? v[c] : 0.0f);
+  }
+}
+
+// ------------------------------------------------------------------------------------ SIMT conv
+
+struct SimtArgs {
+  const void* in;
+  void* out;
+  const void* skip;
+  const float* w;      // [cout][cin8*8][9]
+  const float* bias;
+  const int32_t* map;  // [bin][bin_h][bin_w] at LR
+  const int32_t* num_bins;
+  int cin8, cout, role, ps, res;
+  int Wr, Hr;          // grid of this conv (bin_w*res, bin_h*res)
+  int bin_w, bin_h;
+  int out_c8;          // chunks of the output activation (ROLE_UP: cout/ps^2/8)
+  float res_scale;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(128) conv_simt_kernel(SimtArgs a) {
+  const int b = blockIdx.z;
+  if (b >= *a.num_bins) return;
+  const int y = blockIdx.y;
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= a.Wr) return;
+  const T* in = (const T*)a.in;
+  const int64_t plane = (int64_t)a.Wr * 8;                    // elements per (row, chunk)
+  const int64_t rowstride = plane * a.cin8;
+  const T* inb = in + (int64_t)b * a.Hr * rowstride;
+  const bool occ = a.map[((int64_t)b * a.bin_h + y / a.res) * a.bin_w + x / a.res] >= 0;
+  const int K = a.cin8 * 8 * 9;
+  for (int co0 = 0; co0 < a.cout; co0 += 16) {
+    float acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = (co0 + j < a.cout) ? __ldg(a.bias + co0 + j) : 0.f;
+    for (int c8 = 0; c8 < a.cin8; ++c8)
+      for (int t = 0; t < 9; ++t) {
+        const int yy = y + t / 3 - 1, xx = x + t % 3 - 1;
+        if (yy < 0 || xx < 0 || yy >= a.Hr || xx >= a.Wr) continue;
+        float v[8];
+        const T* src = inb + yy * rowstride + c8 * plane + (int64_t)xx * 8;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = from_t<T>(src[i]);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if (co0 + j >= a.cout) break;
+          const float* wr = a.w + (int64_t)(co0 + j) * K + (c8 * 8) * 9 + t;
+          float s = acc[j];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) s = fmaf(__ldg(wr + i * 9), v[i], s);
+          acc[j] = s;
+        }
+      }
+    // epilogue
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int co = co0 + j;
+      if (co >= a.cout) break;
+      float v = acc[j];
+      if (a.role == ROLE_RES_A || a.role == ROLE_TINY0) v = fmaxf(v, 0.f);
+      if (!occ) v = 0.f;
+      if (a.role == ROLE_UP || a.role == ROLE_TINY1) {
+        const int p2 = a.ps * a.ps;
+        const int c = co / p2, i = (co % p2) / a.ps, jj = co % a.ps;
+        const int Y = y * a.ps + i, X = x * a.ps + jj;
+        const int Wo = a.Wr * a.ps, Ho = a.Hr * a.ps;
+        if (a.role == ROLE_UP) {
+          T* o = (T*)a.out + (int64_t)b * Ho * (int64_t)Wo * a.out_c8 * 8;
+          o[((int64_t)Y * a.out_c8 + c / 8) * Wo * 8 + (int64_t)X * 8 + (c & 7)] = to_t<T>(v);
+        } else {
+          T* o = (T*)a.out + (int64_t)b * Ho * (int64_t)Wo * 4;
+          o[((int64_t)Y * Wo + X) * 4 + c] = to_t<T>(v);
+          if (c == 2) o[((int64_t)Y * Wo + X) * 4 + 3] = to_t<T>(0.f);
+        }
+      } else if (a.role == ROLE_TAIL) {
+        T* o = (T*)a.out + ((int64_t)b * a.Hr + y) * (int64_t)a.Wr * 4 + (int64_t)x * 4;
+        o[co] = to_t<T>(v);
+        if (co == 2) o[3] = to_t<T>(0.f);
+      } else {
+        const int64_t idx = (int64_t)b * a.Hr * (int64_t)a.Wr * a.out_c8 * 8 +
+                            ((int64_t)y * a.out_c8 + co / 8) * a.Wr * 8 + (int64_t)x * 8 + (co & 7);
+        if (a.role == ROLE_RES_B) v = occ ? from_t<T>(((const T*)a.skip)[idx]) + a.res_scale * v : 0.f;
+        if (a.role == ROLE_BODY) v = occ ? v + from_t<T>(((const T*)a.skip)[idx]) : 0.f;
+        ((T*)a.out)[idx] = to_t<T>(v);
+      }
+    }
+  }
+}
+
+regen_status conv_simt_launch(const SRNet* net, const ConvDesc& cv, const void* in, void* out, const void* skip,
+                              const int32_t* map, int max_bins, const int32_t* d_num_bins, int bin_w, int bin_h,
+                              cudaStream_t s) {
+  SimtArgs a;
+  a.in = in;
+  a.out = out;
+  a.skip = skip;
+  a.w = net->d_w32 + cv.w_off;
+  a.bias = net->d_w32 + cv.b_off;
+  a.map = map;
+  a.num_bins = d_num_bins;
+  a.cin8 = cv.cin8;
+  a.cout = cv.cout;
+  a.role = cv.role;
+  a.ps = cv.ps;
+  a.res = cv.res;
+  a.Wr = bin_w * cv.res;
+  a.Hr = bin_h * cv.res;
+  a.bin_w = bin_w;
+  a.bin_h = bin_h;
+  a.out_c8 = cv.role == ROLE_UP ? (cv.cout / (cv.ps * cv.ps) + 7) / 8 : (cv.cout + 7) / 8;
+  a.res_scale = net->cfg.res_scale;
+  dim3 grid((a.Wr + 127) / 128, a.Hr, max_bins);
+  if (net->cfg.dtype == REGEN_DTYPE_BF16)
+    conv_simt_kernel<__nv_bfloat16><<<grid, 128, 0, s>>>(a);
+  else
+    conv_simt_kernel<float><<<grid, 128, 0, s>>>(a);
+  REGEN_LAUNCH_CHECK();
+  return REGEN_OK;
+}
+
+// ------------------------------------------------------------------------------------ buffers
+
+EnhanceBufs enhance_bufs(const SRNet* net, const regen_pack_params& p, void* base) {
+  Carver c(base);
+  const size_t es = net->cfg.dtype == REGEN_DTYPE_BF16 ? 2 : 4;
+  const int C8 = net->cfg.channels / 8, s = net->cfg.scale;
+  const size_t px = (size_t)p.max_bins * p.bin_w * p.bin_h;
+  EnhanceBufs e;
+  e.map = c.take<int32_t>(px);
+  e.x0 = c.take<uint8_t>(px * 8 * es);
+  e.a0 = c.take<uint8_t>(px * C8 * 8 * es);
+  if (net->cfg.n_resblocks > 0) {
+    e.a1 = c.take<uint8_t>(px * C8 * 8 * es);
+    e.a2 = c.take<uint8_t>(px * C8 * 8 * es);
+    e.u1 = s == 4 ? (void*)c.take<uint8_t>(px * 4 * C8 * 8 * es) : nullptr;
+    e.u = c.take<uint8_t>(px * s * s * C8 * 8 * es);
+  } else {
+    e.a1 = e.a2 = e.u1 = e.u = nullptr;
+  }
+  e.bytes = c.off + 256;
+  return e;
+}
+
+static regen_status run_conv(const SRNet* net, const ConvDesc& cv, const void* in, void* out, const void* skip,
+                             const int32_t* map, const regen_pack_params& p, const int32_t* d_num_bins,
+                             cudaStream_t s) {
+  if (net->use_tc && conv_tc_supported(net, cv))
+    return conv_tc_launch(net, cv, in, out, skip, map, p.max_bins, d_num_bins, p.bin_w, p.bin_h, s);
+  return conv_simt_launch(net, cv, in, out, skip, map, p.max_bins, d_num_bins, p.bin_w, p.bin_h, s);
+}
+
+static regen_status validate_pack(const regen_pack_params* p) {
+  REGEN_REQUIRE(p != nullptr, "pack params null");
+  REGEN_REQUIRE(p->bin_w >= 4 && p->bin_h >= 1 && p->bin_w <= 4096 && p->bin_h <= 4096 && p->max_bins >= 1,
+                "bad bin geometry");
+  return REGEN_OK;
+}
+
+}  // namespace regen
+
+namespace regen {
+
+regen_status stitch_into(const regen_geom& g, const regen_pack_params& p, int dtype, int layout,
+                         const uint8_t* d_frames, const regen_box* d_boxes, const int64_t* d_num_boxes,
+                         int64_t max_boxes, const int32_t* d_num_bins, int32_t* map, void* out, cudaStream_t s) {
+  REGEN_CUDA(cudaMemsetAsync(map, 0xFF, (size_t)p.max_bins * p.bin_w * p.bin_h * 4, s));
+  paint_kernel<<<(unsigned)max_boxes, 256, 0, s>>>(d_boxes, d_num_boxes, max_boxes, map, p.bin_w, p.bin_h);
+  REGEN_LAUNCH_CHECK();
+  dim3 grid((p.bin_w + 127) / 128, p.bin_h, p.max_bins);
+  if (dtype == REGEN_DTYPE_BF16) {
+    if (layout == 0)
+      gather_kernel<__nv_bfloat16, 0><<<grid, 128, 0, s>>>(d_frames, d_boxes, map, d_num_bins, p.bin_w, p.bin_h, g.F,
+                                                           g.frame_w, g.frame_h, (__nv_bfloat16*)out);
+    else
+      gather_kernel<__nv_bfloat16, 1><<<grid, 128, 0, s>>>(d_frames, d_boxes, map, d_num_bins, p.bin_w, p.bin_h, g.F,
+                                                           g.frame_w, g.frame_h, (__nv_bfloat16*)out);
+  } else {
+    if (layout == 0)
+      gather_kernel<float, 0><<<grid, 128, 0, s>>>(d_frames, d_boxes, map, d_num_bins, p.bin_w, p.bin_h, g.F,
+                                                   g.frame_w, g.frame_h, (float*)out);
+    else
+      gather_kernel<float, 1><<<grid, 128, 0, s>>>(d_frames, d_boxes, map, d_num_bins, p.bin_w, p.bin_h, g.F,
+                                                   g.frame_w, g.frame_h, (float*)out);
+  }
+  REGEN_LAUNCH_CHECK();
+  return REGEN_OK;
+}
+
+}  // namespace regen
+
+using namespace regen;
+
+extern "C" regen_status regen_stitch_bins(const regen_geom* geom, const regen_pack_params* p, int32_t dtype,
+                                          const uint8_t* d_frames, const regen_box* d_boxes, int64_t max_boxes,
+                                          const int64_t* d_num_boxes, const int32_t* d_num_bins, void* d_lr_bins,
+                                          void* d_ws, size_t ws_bytes, void* stream) {
+  regen_status st = validate_geom(geom);
+  if (st != REGEN_OK) return st;
+  st = validate_pack(p);
+  if (st != REGEN_OK) return st;
+  REGEN_REQUIRE(dtype == REGEN_DTYPE_BF16 || dtype == REGEN_DTYPE_FP32, "bad dtype");
+  REGEN_REQUIRE(d_frames && d_boxes && d_num_boxes && d_num_bins && d_lr_bins, "null device pointer");
+  REGEN_REQUIRE(max_boxes >= 1 && max_boxes < (1ll << 31), "bad max_boxes");
+  const size_t need = (size_t)p->max_bins * p->bin_w * p->bin_h * 4 + 256;
+  REGEN_REQUIRE(d_ws && ws_bytes >= need, "workspace too small");
+  return stitch_into(*geom, *p, dtype, 1, d_frames, d_boxes, d_num_boxes, max_boxes, d_num_bins, (int32_t*)d_ws,
+                     d_lr_bins, (cudaStream_t)stream);
+}
+
+extern "C" regen_status regen_enhance_packed(void* sr, const regen_geom* geom, const regen_pack_params* p,
+                                             const uint8_t* d_frames, const regen_box* d_boxes, int64_t max_boxes,
+                                             const int64_t* d_num_boxes, const int32_t* d_num_bins, void* d_hr_bins,
+                                             int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream) {
+  REGEN_REQUIRE(sr != nullptr, "null SR handle");
+  regen_status st = validate_geom(geom);
+  if (st != REGEN_OK) return st;
+  st = validate_pack(p);
+  if (st != REGEN_OK) return st;
+  REGEN_REQUIRE(d_frames && d_boxes && d_num_boxes && d_num_bins && d_hr_bins && d_status, "null device pointer");
+  REGEN_REQUIRE(max_boxes >= 1 && max_boxes < (1ll << 31), "bad max_boxes");
+  const SRNet* net = (const SRNet*)sr;
+  EnhanceBufs e = enhance_bufs(net, *p, nullptr);
+  REGEN_REQUIRE(d_ws && ws_bytes >= e.bytes, "workspace too small (%zu < %zu)", ws_bytes, e.bytes);
+  e = enhance_bufs(net, *p, d_ws);
+  cudaStream_t s = (cudaStream_t)stream;
+  st = stitch_into(*geom, *p, net->cfg.dtype, 0, d_frames, d_boxes, d_num_boxes, max_boxes, d_num_bins, e.map, e.x0, s);
+  if (st != REGEN_OK) return st;
+  const auto& cv = net->convs;
+  if (net->cfg.n_resblocks == 0) {
+    st = run_conv(net, cv[0], e.x0, e.a0, nullptr, e.map, *p, d_num_bins, s);
+    if (st == REGEN_OK) st = run_conv(net, cv[1], e.a0, d_hr_bins, nullptr, e.map, *p, d_num_bins, s);
+    return st;
+  }
+  size_t i = 0;
+  st = run_conv(net, cv[i++], e.x0, e.a0, nullptr, e.map, *p, d_num_bins, s);            // head -> h
+  const void* r = e.a0;
+  for (int k = 0; k < net->cfg.n_resblocks && st == REGEN_OK; ++k) {
+    st = run_conv(net, cv[i++], r, e.a2, nullptr, e.map, *p, d_num_bins, s);             // t = relu(conv(r))
+    if (st != REGEN_OK) break;
+    st = run_conv(net, cv[i++], e.a2, e.a1, r, e.map, *p, d_num_bins, s);                // r' = r + s*conv(t)
+    r = e.a1;
+  }
+  if (st == REGEN_OK) st = run_conv(net, cv[i++], r, e.a2, e.a0, e.map, *p, d_num_bins, s);  // body + h
+  if (st != REGEN_OK) return st;
+  if (net->cfg.scale == 4) {
+    st = run_conv(net, cv[i++], e.a2, e.u1, nullptr, e.map, *p, d_num_bins, s);
+    if (st == REGEN_OK) st = run_conv(net, cv[i++], e.u1, e.u, nullptr, e.map, *p, d_num_bins, s);
+  } else {
+    st = run_conv(net, cv[i++], e.a2, e.u, nullptr, e.map, *p, d_num_bins, s);
+  }
+  if (st == REGEN_OK) st = run_conv(net, cv[i++], e.u, d_hr_bins, nullptr, e.map, *p, d_num_bins, s);  // tail
+  return st;
+}

@@ -1,0 +1,70 @@
+// SR network handle and activation layout (internal).
+//
+// Activation layout (both dtypes): [bin][row][C/8][col][8] — per bin row, C/8 planes of 8-channel
+// 16-B (bf16) / 32-B (fp32) chunks, each plane `width` pixels long. One bin row of one plane is a
+// contiguous run, so a tcgen05 K-major no-swizzle operand tile (8 rows x 16 B core matrices, rows
+// contiguous) is a plain 16-B-aligned slice of it and every 3x3 tap is a start-address offset.
+#pragma once
+#include <vector>
+
+#include "common.cuh"
+
+namespace regen {
+
+enum ConvRole : int {
+  ROLE_HEAD = 0,     // x0 -> h (also the residual stream)
+  ROLE_RES_A = 1,    // r -> t = relu(conv)
+  ROLE_RES_B = 2,    // t -> r' = r + res_scale * conv
+  ROLE_BODY = 3,     // r -> conv + h
+  ROLE_UP = 4,       // -> conv, PixelShuffle(ps) into the next resolution
+  ROLE_TAIL = 5,     // -> HR output [bin][y][x][4]
+  ROLE_TINY0 = 6,    // x0 -> relu(conv)
+  ROLE_TINY1 = 7     // -> conv, PixelShuffle(scale) into the HR output
+};
+
+struct ConvDesc {
+  int cin, cout;       // real channel counts
+  int cin8;            // input chunks of 8 channels
+  int role;
+  int ps;              // pixel-shuffle factor for ROLE_UP / ROLE_TINY1
+  int res;             // resolution factor of the conv's input/output grid relative to LR (1, 2, 3, 4)
+  size_t w_off;        // offset (floats) into d_w32: [cout][cin8*8][9] zero padded
+  size_t b_off;        // offset (floats) of bias[cout]
+  size_t tc_off;       // offset (bytes) into d_wtc (tcgen05 packed bf16 B operand), see conv_tc.cu
+  int tc_mode;         // tcgen05 mapping (0 = none)
+};
+
+struct SRNet {
+  regen_sr_config cfg;
+  std::vector<ConvDesc> convs;
+  float* d_w32 = nullptr;      // fp32 weights (bf16-rounded for the BF16 model) + biases
+  uint8_t* d_wtc = nullptr;    // tcgen05 B-operand images
+  size_t wtc_bytes = 0;
+  bool use_tc = false;
+};
+
+// enhance workspace layout
+struct EnhanceBufs {
+  int32_t* map;      // [max_bins][bin_h][bin_w] box index covering the pixel, -1 outside boxes
+  void* x0;          // [max_bins][bin_h][1][bin_w][8]
+  void* a0;          // [max_bins][bin_h][C/8][bin_w][8]  (h)
+  void* a1;          // (r)
+  void* a2;          // (t)
+  void* u1;          // [max_bins][2 bin_h][C/8][2 bin_w][8] (x4 only: after the first x2 stage)
+  void* u;           // [max_bins][s bin_h][C/8][s bin_w][8] (input of the tail)
+  size_t bytes;
+};
+
+EnhanceBufs enhance_bufs(const SRNet* net, const regen_pack_params& p, void* base);
+
+// conv launchers
+regen_status conv_simt_launch(const SRNet* net, const ConvDesc& cv, const void* in, void* out, const void* skip,
+                              const int32_t* map, int max_bins, const int32_t* d_num_bins, int bin_w, int bin_h,
+                              cudaStream_t s);
+bool conv_tc_supported(const SRNet* net, const ConvDesc& cv);
+regen_status conv_tc_prepare(SRNet* net);
+regen_status conv_tc_launch(const SRNet* net, const ConvDesc& cv, const void* in, void* out, const void* skip,
+                            const int32_t* map, int max_bins, const int32_t* d_num_bins, int bin_w, int bin_h,
+                            cudaStream_t s);
+
+}  // namespace regen

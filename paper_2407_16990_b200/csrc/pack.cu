@@ -1,0 +1,427 @@
+// a3-a5: Bound + expand + Partition + density (Alg. 1 l.4-6), Sort (l.6), Packing (l.7-21, Alg. 2).
+//
+// box_count/box_write  one warp per region: enumerate the MB-aligned partition pieces (D5), keep
+//                      the region's members (warp ballot over the piece span), re-bound them with
+//                      warp min/max, drop empty pieces; a scan over regions gives creation-ordered
+//                      box indices. Density = fp64 raster-order sum over the span (one lane, D4).
+// sort_rank            rank of every box under (density desc, index asc) or (area desc, index asc):
+//                      unique keys => order is the exact inverse permutation (SMEM-tiled count).
+// pack_kernel          one CTA, free areas of the opened bins in an SMEM pool statically owned by
+//                      threads; per box one block-wide min-reduction finds the first fitting free area
+//                      in (bin, seq) order (D12); every thread replays the same decision and the slot
+//                      owners apply the guillotine remainders (D6). Unopened bins are implicit.
+#include "common.cuh"
+
+namespace regen {
+
+size_t select_workspace_bytes(const regen_geom& g);
+
+// ------------------------------------------------------------------------------------ boxes
+
+struct BoxArgs {
+  const float* imp;
+  const int32_t* labels;
+  const regen_region* regions;
+  const int64_t* num_regions;
+  int64_t max_regions;
+  int32_t* region_count;     // [max_regions] non-empty pieces per region
+  const int64_t* region_off; // [max_regions]
+  regen_box* boxes;
+  int64_t max_boxes;
+  int32_t* box_of_mb;        // [frames][GH][GW] (d_mb_owner, pre-filled with -1)
+  int32_t* status;
+  int GW, GH, W, H, F, mb, expand, P;
+};
+
+__device__ __forceinline__ int piece_start(int n, int pieces, int i) {
+  const int base = n / pieces, rem = n % pieces;
+  return i * base + (i < rem ? i : rem);
+}
+
+// Enumerates the non-empty pieces of region r with one warp. WRITE=false: count only.
+template <bool WRITE>
+__device__ int region_pieces(const BoxArgs& a, int64_t r, int64_t box_base) {
+  const int lane = threadIdx.x & 31;
+  const regen_region rg = a.regions[r];
+  const int64_t frame = (int64_t)rg.stream * a.F + rg.frame;
+  const int32_t* lab = a.labels + frame * a.GW * a.GH;
+  const int wm = rg.mx1 - rg.mx0, hm = rg.my1 - rg.my0;
+  const int nx = (wm + a.P - 1) / a.P, ny = (hm + a.P - 1) / a.P;
+  int produced = 0;
+  for (int py = 0; py < ny; ++py)
+    for (int px = 0; px < nx; ++px) {
+      const int sx0 = rg.mx0 + piece_start(wm, nx, px), sx1 = rg.mx0 + piece_start(wm, nx, px + 1);
+      const int sy0 = rg.my0 + piece_start(hm, ny, py), sy1 = rg.my0 + piece_start(hm, ny, py + 1);
+      const int pw = sx1 - sx0, ncell = pw * (sy1 - sy0);
+      int mx0 = 1 << 30, my0 = 1 << 30, mx1 = -1, my1 = -1, cnt = 0;
+      for (int c = lane; c < ncell; c += 32) {
+        const int x = sx0 + c % pw, y = sy0 + c / pw;
+        if (lab[y * a.GW + x] == (int32_t)r) {
+          ++cnt;
+          mx0 = min(mx0, x); my0 = min(my0, y); mx1 = max(mx1, x + 1); my1 = max(my1, y + 1);
+        }
+      }
+      cnt = warp_sum(cnt);
+      if (cnt == 0) continue;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        mx0 = min(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+        my0 = min(my0, __shfl_xor_sync(0xffffffffu, my0, o));
+        mx1 = max(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+        my1 = max(my1, __shfl_xor_sync(0xffffffffu, my1, o));
+      }
+      if (WRITE) {
+        const int64_t b = box_base + produced;
+        if (b < a.max_boxes) {
+          if (lane == 0) {
+            double sum = 0.0;
+            const float* sc = a.imp + frame * a.GW * a.GH;
+            for (int y = my0; y < my1; ++y)
+              for (int x = mx0; x < mx1; ++x) sum = __dadd_rn(sum, (double)sc[y * a.GW + x]);
+            regen_box bx;
+            bx.stream = rg.stream;
+            bx.frame = rg.frame;
+            bx.mx0 = mx0; bx.my0 = my0; bx.mx1 = mx1; bx.my1 = my1;
+            const int x0 = max(0, a.mb * mx0 - a.expand), y0 = max(0, a.mb * my0 - a.expand);
+            const int x1 = min(a.W, a.mb * mx1 + a.expand), y1 = min(a.H, a.mb * my1 + a.expand);
+            bx.x0 = x0; bx.y0 = y0; bx.w = x1 - x0; bx.h = y1 - y0;
+            bx.n_members = cnt;
+            bx.region = (int32_t)r;
+            bx.density = __ddiv_rn(sum, (double)((mx1 - mx0) * (my1 - my0)));
+            bx.bin = -1; bx.bx = 0; bx.by = 0; bx.rotated = 0; bx.rank = 0; bx.reserved = 0;
+            a.boxes[b] = bx;
+          }
+          int32_t* own = a.box_of_mb + frame * a.GW * a.GH;
+          const int bw = mx1 - mx0, bc = bw * (my1 - my0);
+          for (int c = lane; c < bc; c += 32) {
+            const int x = mx0 + c % bw, y = my0 + c / bw;
+            if (lab[y * a.GW + x] == (int32_t)r) own[y * a.GW + x] = (int32_t)b;
+          }
+        } else if (lane == 0) {
+          atomicOr(a.status, REGEN_ST_BOX_OVERFLOW);
+        }
+      }
+      ++produced;
+    }
+  return produced;
+}
+
+__global__ void box_count_kernel(BoxArgs a) {
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t nr = min(*a.num_regions, a.max_regions);
+  if (r >= nr) return;
+  const int n = region_pieces<false>(a, r, 0);
+  if ((threadIdx.x & 31) == 0) a.region_count[r] = n;
+}
+
+__global__ void box_write_kernel(BoxArgs a) {
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t nr = min(*a.num_regions, a.max_regions);
+  if (r >= nr) return;
+  region_pieces<true>(a, r, a.region_off[r]);
+}
+
+__global__ void clamp_count_kernel(const int64_t* num_regions, int64_t max_regions, int32_t* region_count,
+                                   int64_t* n_out) {
+  // regions beyond the (truncated) record count contribute nothing to the scan
+  (void)region_count;
+  *n_out = min(*num_regions, max_regions);
+}
+
+__global__ void scan_counts64_kernel(const int32_t* counts, const int64_t* n_ptr, int64_t* offsets, int64_t* total) {
+  __shared__ int scratch[33];
+  const int64_t n = *n_ptr;
+  int64_t carry = 0;
+  for (int64_t base = 0; base < n; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const int c = i < n ? counts[i] : 0;
+    int tot;
+    const int ex = block_exclusive_scan(c, scratch, &tot);
+    if (i < n) offsets[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+// ------------------------------------------------------------------------------------ sort
+
+__device__ __forceinline__ uint64_t box_key(const regen_box& b, int order) {
+  return order == REGEN_ORDER_AREA ? (uint64_t)((int64_t)b.w * b.h) : density_ord(b.density);
+}
+
+__global__ void __launch_bounds__(256) sort_rank_kernel(regen_box* boxes, const int64_t* num_boxes, int64_t max_boxes,
+                                                        int order, int32_t* out_order) {
+  __shared__ uint64_t tile[1024];
+  const int64_t n = min(*num_boxes, max_boxes);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if ((int64_t)blockIdx.x * blockDim.x >= n) return;
+  const uint64_t ki = i < n ? box_key(boxes[i], order) : 0;
+  int64_t rank = 0;
+  for (int64_t base = 0; base < n; base += 1024) {
+    for (int t = threadIdx.x; t < 1024; t += blockDim.x) {
+      const int64_t j = base + t;
+      tile[t] = j < n ? box_key(boxes[j], order) : 0;
+    }
+    __syncthreads();
+    const int lim = (int)min((int64_t)1024, n - base);
+    for (int t = 0; t < lim; ++t) {
+      const uint64_t kj = tile[t];
+      const int64_t j = base + t;
+      rank += (kj > ki) || (kj == ki && j < i);
+    }
+    __syncthreads();
+  }
+  if (i < n) {
+    out_order[rank] = (int32_t)i;
+    boxes[i].rank = (int32_t)rank;
+  }
+}
+
+// ------------------------------------------------------------------------------------ pack
+
+constexpr int PACK_THREADS = 512;
+constexpr int PACK_POOL = 12288;              // free-area slots (SMEM), statically owned: slot % PACK_THREADS
+
+struct PackArgs {
+  regen_box* boxes;
+  const int32_t* order;
+  const int64_t* num_boxes;
+  int64_t max_boxes;
+  int32_t* num_bins;
+  int32_t* status;
+  int bin_w, bin_h, max_bins, gutter;
+};
+
+// slot record: key = bin<<44 | seq<<18 | slot (unique; min = first in (bin, seq) order)
+__global__ void __launch_bounds__(PACK_THREADS, 1) pack_kernel(PackArgs a) {
+  extern __shared__ uint8_t psm[];
+  uint64_t* key = (uint64_t*)psm;                       // PACK_POOL; ~0 = empty
+  uint64_t* rect = key + PACK_POOL;                     // x | y<<16 | w<<32 | h<<48
+  __shared__ uint64_t wmin[2][PACK_THREADS / 32];
+  __shared__ uint64_t wrect[2][PACK_THREADS / 32];
+  __shared__ int s_minA, s_minB;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t n = min(*a.num_boxes, a.max_boxes);
+  for (int i = tid; i < PACK_POOL; i += PACK_THREADS) key[i] = ~0ull;
+  // placement-invariant pruning bounds: a free area narrower than every box can never be used
+  int mA = 1 << 30, mB = 1 << 30;
+  for (int64_t i = tid; i < n; i += PACK_THREADS) {
+    const int pw = a.boxes[i].w + a.gutter, ph = a.boxes[i].h + a.gutter;
+    mA = min(mA, min(pw, ph));
+    mB = min(mB, max(pw, ph));
+  }
+  if (tid == 0) { s_minA = 1 << 30; s_minB = 1 << 30; }
+  __syncthreads();
+  atomicMin(&s_minA, mA);
+  atomicMin(&s_minB, mB);
+  __syncthreads();
+  const int minA = s_minA, minB = s_minB;
+  const int FW = a.bin_w - 1, FH = a.bin_h + a.gutter;   // a fresh bin's free area (x=1, y=0)
+  int hw = 0;        // slots in use: [0, hw)
+  int opened = 0;    // bins opened (lazily, in index order)
+  uint32_t seq = 0;
+  int used = 0;
+  bool overflow = false;
+  for (int64_t oi = 0; oi < n; ++oi) {
+    const int b = a.order[oi];
+    const int pw = a.boxes[b].w + a.gutter, ph = a.boxes[b].h + a.gutter;
+    // phase A: first fitting free area among my slots (key, rect) pairs
+    uint64_t best = ~0ull, brect = 0;
+    for (int s = tid; s < hw; s += PACK_THREADS) {
+      const uint64_t k = key[s];
+      if (k == ~0ull) continue;
+      const uint64_t rr = rect[s];
+      const int fw = (int)((rr >> 32) & 0xFFFF), fh = (int)(rr >> 48);
+      if (((fw >= pw && fh >= ph) || (fw >= ph && fh >= pw)) && k < best) { best = k; brect = rr; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t k2 = __shfl_xor_sync(0xffffffffu, best, o);
+      const uint64_t r2 = __shfl_xor_sync(0xffffffffu, brect, o);
+      if (k2 < best) { best = k2; brect = r2; }
+    }
+    const int buf = (int)(oi & 1);
+    if (lane == 0) { wmin[buf][warp] = best; wrect[buf][warp] = brect; }
+    __syncthreads();
+    best = lane < PACK_THREADS / 32 ? wmin[buf][lane] : ~0ull;
+    brect = lane < PACK_THREADS / 32 ? wrect[buf][lane] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t k2 = __shfl_xor_sync(0xffffffffu, best, o);
+      const uint64_t r2 = __shfl_xor_sync(0xffffffffu, brect, o);
+      if (k2 < best) { best = k2; brect = r2; }
+    }
+    // replicated decision (every thread computes the same placement)
+    int fx = 0, fy = 0, fw = 0, fh = 0, bin = 0, slot = -1;
+    bool place = false;
+    if (best != ~0ull) {
+      slot = (int)(best & 0x3FFFF);
+      fx = (int)(brect & 0xFFFF); fy = (int)((brect >> 16) & 0xFFFF);
+      fw = (int)((brect >> 32) & 0xFFFF); fh = (int)(brect >> 48);
+      bin = (int)(best >> 44);
+      place = true;
+    } else if (opened < a.max_bins && ((FW >= pw && FH >= ph) || (FW >= ph && FH >= pw))) {
+      bin = opened++;
+      fx = 1; fy = 0; fw = FW; fh = FH;
+      place = true;
+    }
+    if (place) {
+      const bool rot = !(fw >= pw && fh >= ph);
+      const int uw = rot ? ph : pw, uh = rot ? pw : ph;
+      if (tid == 0) {
+        a.boxes[b].bin = bin;
+        a.boxes[b].bx = fx;
+        a.boxes[b].by = fy;
+        a.boxes[b].rotated = rot ? 1 : 0;
+      }
+      used = max(used, bin + 1);
+      // InnerFree (D6): guillotine remainders
+      const int64_t v_a = (int64_t)(fw - uw) * fh, v_b = (int64_t)uw * (fh - uh);
+      const int64_t h_a = (int64_t)fw * (fh - uh), h_b = (int64_t)(fw - uw) * uh;
+      const bool vert = max(v_a, v_b) >= max(h_a, h_b);
+      int rx[2], ry[2], rw[2], rh[2];
+      if (vert) {
+        rx[0] = fx + uw; ry[0] = fy; rw[0] = fw - uw; rh[0] = fh;
+        rx[1] = fx; ry[1] = fy + uh; rw[1] = uw; rh[1] = fh - uh;
+      } else {
+        rx[0] = fx; ry[0] = fy + uh; rw[0] = fw; rh[0] = fh - uh;
+        rx[1] = fx + uw; ry[1] = fy; rw[1] = fw - uw; rh[1] = uh;
+      }
+      int reuse = slot;  // the consumed slot is reused by the first kept remainder
+      if (slot >= 0 && tid == (slot % PACK_THREADS)) key[slot] = ~0ull;
+      for (int t = 0; t < 2; ++t) {
+        if (rw[t] <= 0 || rh[t] <= 0) continue;
+        const uint32_t sq = seq++;   // sequence numbers follow the oracle's creation order
+        // prune areas no box of this call can ever use (placement-invariant)
+        if (min(rw[t], rh[t]) < minA || max(rw[t], rh[t]) < minB) continue;
+        int dst;
+        if (reuse >= 0) { dst = reuse; reuse = -1; }
+        else {
+          if (hw >= PACK_POOL) { overflow = true; continue; }
+          dst = hw++;
+        }
+        if (tid == (dst % PACK_THREADS)) {
+          key[dst] = ((uint64_t)bin << 44) | ((uint64_t)sq << 18) | (uint64_t)dst;
+          rect[dst] = (uint64_t)rx[t] | ((uint64_t)ry[t] << 16) | ((uint64_t)rw[t] << 32) | ((uint64_t)rh[t] << 48);
+        }
+      }
+    }
+  }
+  if (tid == 0) {
+    *a.num_bins = used;
+    if (overflow) atomicOr(a.status, REGEN_ST_FREELIST_OVERFLOW);
+  }
+}
+
+__global__ void owner_fix_kernel(int32_t* owner, int64_t n_mbs, const regen_box* boxes, const int64_t* num_boxes,
+                                 int64_t max_boxes) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_mbs) return;
+  const int32_t o = owner[i];
+  if (o < 0) return;
+  const int64_t nb = min(*num_boxes, max_boxes);
+  if (o >= nb || boxes[o].bin < 0) owner[i] = -1;
+}
+
+static size_t pack_ws(const regen_geom& g, int64_t max_regions, void* base, int32_t** rcount, int64_t** roff,
+                      int64_t** nreg) {
+  Carver c(base);
+  int32_t* rc = c.take<int32_t>((size_t)max_regions + 1);
+  int64_t* ro = c.take<int64_t>((size_t)max_regions + 1);
+  int64_t* nr = c.take<int64_t>(4);
+  if (rcount) *rcount = rc;
+  if (roff) *roff = ro;
+  if (nreg) *nreg = nr;
+  (void)g;
+  return c.off + 256;
+}
+
+size_t pack_workspace_bytes(const regen_geom& g, int64_t max_regions) {
+  return pack_ws(g, max_regions, nullptr, nullptr, nullptr, nullptr);
+}
+
+}  // namespace regen
+
+using namespace regen;
+
+extern "C" regen_status regen_pack_regions(const regen_geom* geom, const regen_pack_params* p,
+                                           const float* d_importance, const int32_t* d_labels,
+                                           const regen_region* d_regions, const int64_t* d_num_regions,
+                                           regen_box* d_boxes, int64_t max_boxes, int64_t* d_num_boxes,
+                                           int32_t* d_order, int32_t* d_num_bins, int32_t* d_mb_owner,
+                                           int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream) {
+  regen_status st = validate_geom(geom);
+  if (st != REGEN_OK) return st;
+  REGEN_REQUIRE(p != nullptr, "params is null");
+  REGEN_REQUIRE(p->bin_w >= 4 && p->bin_h >= 1 && p->bin_w <= 4096 && p->bin_h <= 4096, "bad bin size");
+  REGEN_REQUIRE(p->max_bins >= 0 && p->max_bins < (1 << 19), "bad max_bins");
+  REGEN_REQUIRE(p->expand >= 0 && p->expand <= 64, "bad expand");
+  REGEN_REQUIRE(p->partition_mb >= 1 && p->partition_mb <= 64, "bad partition_mb");
+  REGEN_REQUIRE(p->gutter >= 0 && p->gutter <= 8, "bad gutter");
+  REGEN_REQUIRE(p->order == REGEN_ORDER_DENSITY || p->order == REGEN_ORDER_AREA, "bad order");
+  REGEN_REQUIRE(d_importance && d_labels && d_num_regions && d_num_boxes && d_num_bins && d_mb_owner && d_status,
+                "null device pointer");
+  REGEN_REQUIRE(max_boxes >= 1 && max_boxes < (1ll << 31) && d_boxes && d_order, "bad boxes buffer");
+  const regen_geom g = *geom;
+  // the region capacity is implied by the labels: at most one region per MB
+  const int64_t max_regions = n_mbs(g);
+  REGEN_REQUIRE(ws_bytes >= pack_workspace_bytes(g, max_regions) && d_ws, "workspace too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  int32_t* rcount;
+  int64_t *roff, *nreg;
+  pack_ws(g, max_regions, d_ws, &rcount, &roff, &nreg);
+  REGEN_CUDA(cudaMemsetAsync(d_mb_owner, 0xFF, sizeof(int32_t) * (size_t)n_mbs(g), s));
+
+  BoxArgs a;
+  a.imp = d_importance;
+  a.labels = d_labels;
+  a.regions = d_regions;
+  a.num_regions = d_num_regions;
+  a.max_regions = max_regions;
+  a.region_count = rcount;
+  a.region_off = roff;
+  a.boxes = d_boxes;
+  a.max_boxes = max_boxes;
+  a.box_of_mb = d_mb_owner;
+  a.status = d_status;
+  a.GW = grid_w(g);
+  a.GH = grid_h(g);
+  a.W = g.frame_w;
+  a.H = g.frame_h;
+  a.F = g.F;
+  a.mb = g.mb;
+  a.expand = p->expand;
+  a.P = p->partition_mb;
+  const int warps_per_block = 8;
+  const unsigned nblk = (unsigned)((max_regions + warps_per_block - 1) / warps_per_block);
+  clamp_count_kernel<<<1, 1, 0, s>>>(d_num_regions, max_regions, rcount, nreg);
+  REGEN_LAUNCH_CHECK();
+  box_count_kernel<<<nblk, 32 * warps_per_block, 0, s>>>(a);
+  REGEN_LAUNCH_CHECK();
+  scan_counts64_kernel<<<1, 1024, 0, s>>>(rcount, nreg, roff, d_num_boxes);
+  REGEN_LAUNCH_CHECK();
+  box_write_kernel<<<nblk, 32 * warps_per_block, 0, s>>>(a);
+  REGEN_LAUNCH_CHECK();
+  sort_rank_kernel<<<(unsigned)((max_boxes + 255) / 256), 256, 0, s>>>(d_boxes, d_num_boxes, max_boxes, p->order,
+                                                                       d_order);
+  REGEN_LAUNCH_CHECK();
+  PackArgs k;
+  k.boxes = d_boxes;
+  k.order = d_order;
+  k.num_boxes = d_num_boxes;
+  k.max_boxes = max_boxes;
+  k.num_bins = d_num_bins;
+  k.status = d_status;
+  k.bin_w = p->bin_w;
+  k.bin_h = p->bin_h;
+  k.max_bins = p->max_bins;
+  k.gutter = p->gutter;
+  const size_t smem = (size_t)PACK_POOL * 16;
+  REGEN_CUDA(cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  pack_kernel<<<1, PACK_THREADS, smem, s>>>(k);
+  REGEN_LAUNCH_CHECK();
+  owner_fix_kernel<<<(unsigned)((n_mbs(g) + 255) / 256), 256, 0, s>>>(d_mb_owner, n_mbs(g), d_boxes, d_num_boxes,
+                                                                       max_boxes);
+  REGEN_LAUNCH_CHECK();
+  return REGEN_OK;
+}

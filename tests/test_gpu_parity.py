@@ -1,0 +1,203 @@
+"""GPU parity: the CUDA path through the C-ABI (paper_2407_16990_b200) vs the CPU oracle, on the same
+seeded inputs. Integer outputs (selection, labels, regions, boxes incl. fp64 density bits, order,
+placements, bin count, MB owners) must be bit-exact; pixels within 1e-4 (fp32 model) or 2e-2 (bf16
+model) max-abs (BASELINE.json north_star)."""
+import dataclasses
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = {True: 2e-2, False: 1e-4}
+
+
+def _rg():
+    import paper_2407_16990_b200 as rg
+    return rg
+
+
+def _pipeline(wl, weights, **kw):
+    rg = _rg()
+    return rg.Pipeline(S=wl.S, F=wl.F, W=wl.W, H=wl.H, k=kw.pop("k", wl.k), bin_w=wl.bin_w, bin_h=wl.bin_h,
+                       max_bins=wl.max_bins, partition_mb=wl.partition_mb, scale=wl.sr.scale,
+                       channels=wl.sr.channels, n_resblocks=wl.sr.n_resblocks, weights=weights, bf16=wl.sr.bf16,
+                       res_scale=wl.sr.res_scale, **kw)
+
+
+def _oracle_index(wl, imp, **kw):
+    return oracle.index_path(imp, wl.W, wl.H, kw.pop("k", wl.k), partition_mb=wl.partition_mb, bin_w=wl.bin_w,
+                             bin_h=wl.bin_h, max_bins=wl.max_bins, **kw)
+
+
+def _assert_index_equal(g, o):
+    assert g["status"] == 0
+    np.testing.assert_array_equal(g["sel"], o["sel"])
+    np.testing.assert_array_equal(g["labels"], o["labels"])
+    assert g["num_regions"] == len(o["regions"])
+    gr = g["regions"]
+    np.testing.assert_array_equal(np.stack([gr[f] for f in gr.dtype.names], 1), o["regions"])
+    assert g["num_boxes"] == len(o["boxes"])
+    gb = g["boxes"]
+    cols = ["stream", "frame", "mx0", "my0", "mx1", "my1", "x0", "y0", "w", "h", "n_members", "region"]
+    np.testing.assert_array_equal(np.stack([gb[c] for c in cols], 1), o["boxes"])
+    np.testing.assert_array_equal(gb["density"].view(np.uint64), o["density"].view(np.uint64))
+    np.testing.assert_array_equal(g["order"], o["order"])
+    np.testing.assert_array_equal(np.stack([gb["bin"], gb["bx"], gb["by"], gb["rotated"]], 1), o["placement"])
+    assert g["num_bins"] == o["num_bins"]
+    np.testing.assert_array_equal(g["owner"], o["owner"])
+
+
+def _run_index(wl, imp, weights, **kw):
+    p = _pipeline(wl, weights, **kw)
+    d_imp = torch.from_numpy(imp).cuda()
+    p.select(d_imp)
+    p.pack_step(d_imp)
+    return p, p.host_results()
+
+
+INDEX_CASES = [
+    ("c1", "blobs", {}),
+    ("c2f4", "blobs", {}),
+    ("c2f4", "levels", {}),
+    ("c2f4", "equal", {}),
+    ("c2f4", "checker", {}),
+    ("c2f4", "noisy", {}),
+    ("c2f4", "full", {"k": 40 * 23 * 4}),
+    ("c2f4", "noisy", {"connectivity": 4}),
+    ("c2f4", "levels", {"mode": 1, "tau": 5.0, "k": -1}),
+    ("c2f4", "blobs", {"mode": 1, "tau": 0.4, "k": 900}),
+    ("c2f4", "levels", {"scope": 2, "k": 37}),
+    ("c2f4", "blobs", {"scope": 1, "k": 500}),
+    ("c2f4", "blobs", {"order": 1}),
+    ("c3f2", "blobs", {}),
+    ("c5f2", "noisy", {}),
+]
+
+
+def _wl(name):
+    if name == "c2f4":
+        return synth.small(synth.CONFIGS["c2"], F=4)
+    if name == "c3f2":
+        return synth.small(synth.CONFIGS["c3"], F=2)
+    if name == "c5f2":
+        return synth.small(synth.CONFIGS["c5"], F=2)
+    return synth.CONFIGS[name]
+
+
+@pytest.mark.parametrize("name,kind,kw", INDEX_CASES)
+def test_index_path_bit_exact(name, kind, kw):
+    wl = _wl(name)
+    imp = synth.importance_maps(wl.S, wl.F, wl.GH, wl.GW, 11, kind)
+    w = synth.sr_weights(wl.sr, 0)
+    okw = dict(kw)
+    conv = okw.pop("connectivity", 8)
+    order = okw.pop("order", 0)
+    _, g = _run_index(wl, imp, w, **kw)
+    o = _oracle_index(wl, imp, conn=conv, order_policy=order, **okw)
+    _assert_index_equal(g, o)
+
+
+def test_index_path_small_max_bins_leaves_unplaced():
+    wl = dataclasses.replace(synth.small(synth.CONFIGS["c2"], F=3), max_bins=5)
+    imp = synth.importance_maps(wl.S, wl.F, wl.GH, wl.GW, 2)
+    _, g = _run_index(wl, imp, synth.sr_weights(wl.sr, 0))
+    o = _oracle_index(wl, imp)
+    assert (o["placement"][:, 0] < 0).any()
+    _assert_index_equal(g, o)
+
+
+def test_index_path_zero_k_and_empty():
+    wl = synth.small(synth.CONFIGS["c2"], F=2)
+    imp = synth.importance_maps(wl.S, wl.F, wl.GH, wl.GW, 2)
+    _, g = _run_index(wl, imp, synth.sr_weights(wl.sr, 0), k=0)
+    assert g["num_regions"] == 0 and g["num_boxes"] == 0 and g["num_bins"] == 0
+    assert (g["owner"] < 0).all() and g["sel"].sum() == 0
+
+
+@pytest.mark.parametrize("bf16", [True, False])
+def test_stitch_bins_bit_exact(bf16):
+    rg = _rg()
+    wl = synth.small(synth.CONFIGS["c2"], F=3)
+    wl = dataclasses.replace(wl, sr=dataclasses.replace(wl.sr, bf16=bf16))
+    imp = synth.importance_maps(wl.S, wl.F, wl.GH, wl.GW, 4, "noisy")
+    fr = synth.frames_rgb8(wl.S, wl.F, wl.H, wl.W, 4)
+    p, g = _run_index(wl, imp, synth.sr_weights(wl.sr, 0))
+    o = _oracle_index(wl, imp)
+    nb = o["num_bins"]
+    dt = torch.bfloat16 if bf16 else torch.float32
+    lr = torch.zeros((wl.max_bins, wl.bin_h, wl.bin_w, 4), dtype=dt, device="cuda")
+    rg.stitch_bins(p.geom, p.pack, rg.DTYPE_BF16 if bf16 else rg.DTYPE_FP32, torch.from_numpy(fr).cuda(), p.boxes,
+                   p.max_boxes, p.counts[1:2], p.num_bins, lr, p.ws)
+    ref = oracle.gather(fr, o["boxes"], o["placement"], wl.bin_w, wl.bin_h, nb, bf16)
+    got = lr[:nb, :, :, :3].float().cpu().numpy().astype(np.float64)
+    np.testing.assert_array_equal(got, ref)
+    assert (lr[:nb, :, :, 3] == 0).all()
+
+
+def _check_pixels(wl, seed=5, kind="blobs", box_sample=None, frame_sample=None):
+    imp = synth.importance_maps(wl.S, wl.F, wl.GH, wl.GW, seed, kind)
+    fr = synth.frames_rgb8(wl.S, wl.F, wl.H, wl.W, seed)
+    w = synth.sr_weights(wl.sr, seed)
+    p = _pipeline(wl, w)
+    out = p.run(torch.from_numpy(imp).cuda(), torch.from_numpy(fr).cuda())
+    g = p.host_results()
+    o = _oracle_index(wl, imp)
+    _assert_index_equal(g, o)
+    nb = o["num_bins"]
+    lr = oracle.gather(fr, o["boxes"], o["placement"], wl.bin_w, wl.bin_h, nb, wl.sr.bf16)
+    w64 = oracle.sr_weights_for(wl.sr, w)
+    nbox = len(o["boxes"])
+    boxes_to_check = range(nbox) if box_sample is None else box_sample(nbox)
+    hr_g = p.hr_bins[:nb].float().cpu().numpy()
+    tol = TOL[wl.sr.bf16]
+    s = wl.sr.scale
+    worst = 0.0
+    for b in boxes_to_check:
+        bin_, bx, by, rot = o["placement"][b]
+        if bin_ < 0:
+            continue
+        hr = oracle.enhance(wl.sr, w64, lr, o["boxes"], o["placement"], b, b + 1)
+        w_, h_ = o["boxes"][b, 8], o["boxes"][b, 9]
+        fw, fh = (h_, w_) if rot else (w_, h_)
+        sl = (bin_, slice(s * by, s * (by + fh)), slice(s * bx, s * (bx + fw)))
+        d = np.abs(hr_g[sl][..., :3] - hr[sl])
+        worst = max(worst, float(d.max()))
+        assert d.max() <= tol, f"box {b}: max err {d.max()}"
+    # HR bin pixels outside every box are zero
+    f_lo, f_hi = (0, wl.S * wl.F) if frame_sample is None else frame_sample
+    if box_sample is None:
+        hr_all = oracle.enhance(wl.sr, w64, lr, o["boxes"], o["placement"])
+        ref = oracle.scatter(fr, o["boxes"], o["placement"], o["owner"], hr_all, s, wl.bin_w, wl.bin_h, f_lo, f_hi)
+        got = out.reshape(-1, *out.shape[2:])[f_lo:f_hi].float().cpu().numpy()
+        d = np.abs(got - ref)
+        assert d.max() <= tol, f"frames: max err {d.max()}"
+    return worst
+
+
+def test_pixels_c1_fp32_full():
+    _check_pixels(synth.CONFIGS["c1"])
+
+
+def test_pixels_c2_bf16_small():
+    _check_pixels(synth.small(synth.CONFIGS["c2"], F=2), box_sample=lambda n: range(0, n, max(1, n // 12)))
+
+
+def test_pixels_tiny_bf16_x3_full_frames():
+    wl = dataclasses.replace(synth.small(synth.CONFIGS["c2"], F=2), sr=synth.SRConfig(3, 16, 0, 1.0, True))
+    _check_pixels(wl)
+
+
+def test_pixels_small_edsr_bf16_full_frames():
+    wl = dataclasses.replace(synth.small(synth.CONFIGS["c2"], F=1), sr=synth.SRConfig(3, 16, 1, 1.0, True))
+    _check_pixels(wl, kind="noisy")
+
+
+def test_pixels_small_edsr_fp32_x4_and_x2():
+    for s in (4, 2):
+        wl = dataclasses.replace(synth.small(synth.CONFIGS["c2"], F=1), sr=synth.SRConfig(s, 8, 1, 0.5, False))
+        _check_pixels(wl, box_sample=lambda n: range(0, n, max(1, n // 10)))
