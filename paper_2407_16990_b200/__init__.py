@@ -255,6 +255,16 @@ class Pipeline:
         self.enhance(frames, stream)
         return self.scatter(frames, out, stream)
 
+    def n_convs(self) -> int:
+        c = self.sr.cfg
+        if c.n_resblocks == 0:
+            return 2
+        return 1 + 2 * c.n_resblocks + 1 + (2 if c.scale == 4 else 1) + 1
+
+    def launches_per_step(self) -> int:
+        """Kernels libregen launches per run(): select 4, pack 7, enhance 2 + one per conv, scatter 1."""
+        return 4 + 7 + 2 + self.n_convs() + 1
+
     # ---- host-side views (sync), for tests and reporting
     def host_results(self) -> dict:
         t = self.torch

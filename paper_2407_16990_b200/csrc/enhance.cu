@@ -132,6 +132,7 @@ extern "C" regen_status regen_sr_destroy(void* handle) {
   SRNet* net = (SRNet*)handle;
   cudaFree(net->d_w32);
   cudaFree(net->d_wtc);
+  conv_tc_release(net);
   delete net;
   return REGEN_OK;
 }

@@ -41,6 +41,7 @@ struct SRNet {
   uint8_t* d_wtc = nullptr;    // tcgen05 B-operand images
   size_t wtc_bytes = 0;
   bool use_tc = false;
+  void* tc_plans = nullptr;   // tc::NetPlans (conv_tc.cu)
 };
 
 // enhance workspace layout
@@ -63,6 +64,7 @@ regen_status conv_simt_launch(const SRNet* net, const ConvDesc& cv, const void* 
                               cudaStream_t s);
 bool conv_tc_supported(const SRNet* net, const ConvDesc& cv);
 regen_status conv_tc_prepare(SRNet* net);
+void conv_tc_release(SRNet* net);
 regen_status conv_tc_launch(const SRNet* net, const ConvDesc& cv, const void* in, void* out, const void* skip,
                             const int32_t* map, int max_bins, const int32_t* d_num_bins, int bin_w, int bin_h,
                             cudaStream_t s);

