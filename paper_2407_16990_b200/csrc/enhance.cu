@@ -172,13 +172,20 @@ __device__ __forceinline__ float from_t<__nv_bfloat16>(__nv_bfloat16 v) { return
 // LAYOUT 0: activation layout chunk [bin][y][1][x][8]; LAYOUT 1: plain [bin][y][x][4]
 template <typename T, int LAYOUT>
 __global__ void gather_kernel(const uint8_t* frames, const regen_box* boxes, const int32_t* map,
-                              const int32_t* num_bins, int bin_w, int bin_h, int F, int W, int H, T* out) {
+                              const int32_t* num_bins, int bin_w, int bin_h, int F, int W, int H, T* out,
+                              uint32_t* mbits) {
   const int b = blockIdx.z;
   if (b >= *num_bins) return;
   const int y = blockIdx.y;
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int32_t id = x < bin_w ? map[((int64_t)b * bin_h + y) * bin_w + x] : -1;
+  if (mbits != nullptr) {
+    // per-row occupancy bitmask for the tensor-core epilogue: bit x%32 of word [b][y][x/32]
+    const uint32_t bits = __ballot_sync(0xffffffffu, id >= 0);
+    const int words = (bin_w + 31) / 32;
+    if ((threadIdx.x & 31) == 0 && x < bin_w) mbits[((int64_t)b * bin_h + y) * words + x / 32] = bits;
+  }
   if (x >= bin_w) return;
-  const int32_t id = map[((int64_t)b * bin_h + y) * bin_w + x];
   float v[3] = {0.f, 0.f, 0.f};
   if (id >= 0) {
     const regen_box bx = boxes[id];
@@ -328,6 +335,7 @@ EnhanceBufs enhance_bufs(const SRNet* net, const regen_pack_params& p, void* bas
   const size_t px = (size_t)p.max_bins * p.bin_w * p.bin_h;
   EnhanceBufs e;
   e.map = c.take<int32_t>(px);
+  e.mbits = c.take<uint32_t>((size_t)p.max_bins * p.bin_h * ((p.bin_w + 31) / 32));
   e.x0 = c.take<uint8_t>(px * 8 * es);
   e.a0 = c.take<uint8_t>(px * C8 * 8 * es);
   if (net->cfg.n_resblocks > 0) {
@@ -343,11 +351,11 @@ EnhanceBufs enhance_bufs(const SRNet* net, const regen_pack_params& p, void* bas
 }
 
 static regen_status run_conv(const SRNet* net, const ConvDesc& cv, const void* in, void* out, const void* skip,
-                             const int32_t* map, const regen_pack_params& p, const int32_t* d_num_bins,
+                             const EnhanceBufs& e, const regen_pack_params& p, const int32_t* d_num_bins,
                              cudaStream_t s) {
-  if (net->use_tc && conv_tc_supported(net, cv))
-    return conv_tc_launch(net, cv, in, out, skip, map, p.max_bins, d_num_bins, p.bin_w, p.bin_h, s);
-  return conv_simt_launch(net, cv, in, out, skip, map, p.max_bins, d_num_bins, p.bin_w, p.bin_h, s);
+  if (net->use_tc && conv_tc_supported(net, cv, p.bin_w))
+    return conv_tc_launch(net, cv, in, out, skip, e.mbits, p.max_bins, d_num_bins, p.bin_w, p.bin_h, s);
+  return conv_simt_launch(net, cv, in, out, skip, e.map, p.max_bins, d_num_bins, p.bin_w, p.bin_h, s);
 }
 
 static regen_status validate_pack(const regen_pack_params* p) {
@@ -363,7 +371,8 @@ namespace regen {
 
 regen_status stitch_into(const regen_geom& g, const regen_pack_params& p, int dtype, int layout,
                          const uint8_t* d_frames, const regen_box* d_boxes, const int64_t* d_num_boxes,
-                         int64_t max_boxes, const int32_t* d_num_bins, int32_t* map, void* out, cudaStream_t s) {
+                         int64_t max_boxes, const int32_t* d_num_bins, int32_t* map, void* out, cudaStream_t s,
+                         uint32_t* mbits = nullptr) {
   REGEN_CUDA(cudaMemsetAsync(map, 0xFF, (size_t)p.max_bins * p.bin_w * p.bin_h * 4, s));
   paint_kernel<<<(unsigned)max_boxes, 256, 0, s>>>(d_boxes, d_num_boxes, max_boxes, map, p.bin_w, p.bin_h);
   REGEN_LAUNCH_CHECK();
@@ -371,17 +380,17 @@ regen_status stitch_into(const regen_geom& g, const regen_pack_params& p, int dt
   if (dtype == REGEN_DTYPE_BF16) {
     if (layout == 0)
       gather_kernel<__nv_bfloat16, 0><<<grid, 128, 0, s>>>(d_frames, d_boxes, map, d_num_bins, p.bin_w, p.bin_h, g.F,
-                                                           g.frame_w, g.frame_h, (__nv_bfloat16*)out);
+                                                           g.frame_w, g.frame_h, (__nv_bfloat16*)out, mbits);
     else
       gather_kernel<__nv_bfloat16, 1><<<grid, 128, 0, s>>>(d_frames, d_boxes, map, d_num_bins, p.bin_w, p.bin_h, g.F,
-                                                           g.frame_w, g.frame_h, (__nv_bfloat16*)out);
+                                                           g.frame_w, g.frame_h, (__nv_bfloat16*)out, mbits);
   } else {
     if (layout == 0)
       gather_kernel<float, 0><<<grid, 128, 0, s>>>(d_frames, d_boxes, map, d_num_bins, p.bin_w, p.bin_h, g.F,
-                                                   g.frame_w, g.frame_h, (float*)out);
+                                                   g.frame_w, g.frame_h, (float*)out, mbits);
     else
       gather_kernel<float, 1><<<grid, 128, 0, s>>>(d_frames, d_boxes, map, d_num_bins, p.bin_w, p.bin_h, g.F,
-                                                   g.frame_w, g.frame_h, (float*)out);
+                                                   g.frame_w, g.frame_h, (float*)out, mbits);
   }
   REGEN_LAUNCH_CHECK();
   return REGEN_OK;
@@ -424,31 +433,32 @@ extern "C" regen_status regen_enhance_packed(void* sr, const regen_geom* geom, c
   REGEN_REQUIRE(d_ws && ws_bytes >= e.bytes, "workspace too small (%zu < %zu)", ws_bytes, e.bytes);
   e = enhance_bufs(net, *p, d_ws);
   cudaStream_t s = (cudaStream_t)stream;
-  st = stitch_into(*geom, *p, net->cfg.dtype, 0, d_frames, d_boxes, d_num_boxes, max_boxes, d_num_bins, e.map, e.x0, s);
+  st = stitch_into(*geom, *p, net->cfg.dtype, 0, d_frames, d_boxes, d_num_boxes, max_boxes, d_num_bins, e.map, e.x0, s,
+                   e.mbits);
   if (st != REGEN_OK) return st;
   const auto& cv = net->convs;
   if (net->cfg.n_resblocks == 0) {
-    st = run_conv(net, cv[0], e.x0, e.a0, nullptr, e.map, *p, d_num_bins, s);
-    if (st == REGEN_OK) st = run_conv(net, cv[1], e.a0, d_hr_bins, nullptr, e.map, *p, d_num_bins, s);
+    st = run_conv(net, cv[0], e.x0, e.a0, nullptr, e, *p, d_num_bins, s);
+    if (st == REGEN_OK) st = run_conv(net, cv[1], e.a0, d_hr_bins, nullptr, e, *p, d_num_bins, s);
     return st;
   }
   size_t i = 0;
-  st = run_conv(net, cv[i++], e.x0, e.a0, nullptr, e.map, *p, d_num_bins, s);            // head -> h
+  st = run_conv(net, cv[i++], e.x0, e.a0, nullptr, e, *p, d_num_bins, s);            // head -> h
   const void* r = e.a0;
   for (int k = 0; k < net->cfg.n_resblocks && st == REGEN_OK; ++k) {
-    st = run_conv(net, cv[i++], r, e.a2, nullptr, e.map, *p, d_num_bins, s);             // t = relu(conv(r))
+    st = run_conv(net, cv[i++], r, e.a2, nullptr, e, *p, d_num_bins, s);             // t = relu(conv(r))
     if (st != REGEN_OK) break;
-    st = run_conv(net, cv[i++], e.a2, e.a1, r, e.map, *p, d_num_bins, s);                // r' = r + s*conv(t)
+    st = run_conv(net, cv[i++], e.a2, e.a1, r, e, *p, d_num_bins, s);                // r' = r + s*conv(t)
     r = e.a1;
   }
-  if (st == REGEN_OK) st = run_conv(net, cv[i++], r, e.a2, e.a0, e.map, *p, d_num_bins, s);  // body + h
+  if (st == REGEN_OK) st = run_conv(net, cv[i++], r, e.a2, e.a0, e, *p, d_num_bins, s);  // body + h
   if (st != REGEN_OK) return st;
   if (net->cfg.scale == 4) {
-    st = run_conv(net, cv[i++], e.a2, e.u1, nullptr, e.map, *p, d_num_bins, s);
-    if (st == REGEN_OK) st = run_conv(net, cv[i++], e.u1, e.u, nullptr, e.map, *p, d_num_bins, s);
+    st = run_conv(net, cv[i++], e.a2, e.u1, nullptr, e, *p, d_num_bins, s);
+    if (st == REGEN_OK) st = run_conv(net, cv[i++], e.u1, e.u, nullptr, e, *p, d_num_bins, s);
   } else {
-    st = run_conv(net, cv[i++], e.a2, e.u, nullptr, e.map, *p, d_num_bins, s);
+    st = run_conv(net, cv[i++], e.a2, e.u, nullptr, e, *p, d_num_bins, s);
   }
-  if (st == REGEN_OK) st = run_conv(net, cv[i++], e.u, d_hr_bins, nullptr, e.map, *p, d_num_bins, s);  // tail
+  if (st == REGEN_OK) st = run_conv(net, cv[i++], e.u, d_hr_bins, nullptr, e, *p, d_num_bins, s);  // tail
   return st;
 }

@@ -42,11 +42,14 @@ struct SRNet {
   size_t wtc_bytes = 0;
   bool use_tc = false;
   void* tc_plans = nullptr;   // tc::NetPlans (conv_tc.cu)
+  std::vector<float> tc_weights;   // host copy of the (rounded) weights for B-image packing
+  int tc_bin_w = -1;             // bin width the B images were planned for
 };
 
 // enhance workspace layout
 struct EnhanceBufs {
   int32_t* map;      // [max_bins][bin_h][bin_w] box index covering the pixel, -1 outside boxes
+  uint32_t* mbits;   // [max_bins][bin_h][ceil(bin_w/32)] occupancy bits (map >= 0)
   void* x0;          // [max_bins][bin_h][1][bin_w][8]
   void* a0;          // [max_bins][bin_h][C/8][bin_w][8]  (h)
   void* a1;          // (r)
@@ -62,11 +65,11 @@ EnhanceBufs enhance_bufs(const SRNet* net, const regen_pack_params& p, void* bas
 regen_status conv_simt_launch(const SRNet* net, const ConvDesc& cv, const void* in, void* out, const void* skip,
                               const int32_t* map, int max_bins, const int32_t* d_num_bins, int bin_w, int bin_h,
                               cudaStream_t s);
-bool conv_tc_supported(const SRNet* net, const ConvDesc& cv);
+bool conv_tc_supported(const SRNet* net, const ConvDesc& cv, int bin_w);
 regen_status conv_tc_prepare(SRNet* net);
 void conv_tc_release(SRNet* net);
 regen_status conv_tc_launch(const SRNet* net, const ConvDesc& cv, const void* in, void* out, const void* skip,
-                            const int32_t* map, int max_bins, const int32_t* d_num_bins, int bin_w, int bin_h,
+                            const uint32_t* mbits, int max_bins, const int32_t* d_num_bins, int bin_w, int bin_h,
                             cudaStream_t s);
 
 }  // namespace regen

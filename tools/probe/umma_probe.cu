@@ -160,6 +160,166 @@ __global__ void tput_kernel(int iters, int nshift, long long* cyc, unsigned long
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(tbase));
 }
 
+
+// pattern kernel: N=96 M=128 SS; mode selects the D-column pattern
+//  0: D at col 0 always; 1: D at col 32 always; 2: D alternates 0/32 per MMA;
+//  3: SLIDE pattern: 6 MMAs per "row" into window at col base(r) = ((16 - r) & 15) * 32 (wrapped to 3 slots)
+//     (only the non-wrapping windows are used: r cycles over windows at cols 0,32,...,416)
+//  4: like 0 but A LBO = 2048
+template <int N>
+__global__ void pattern_kernel(int iters, int mode, long long* cyc) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x) ((uint32_t*)smem)[i] = 0x3c003c00u;
+  fence_async_smem();
+  int warp = threadIdx.x / 32;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" :: "r"(smem_u32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) { mbar_init(smem_u32(&bar), 1); asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint32_t tbase = tmem_base;
+  if (threadIdx.x == 0) {
+    uint32_t abase = smem_u32(smem);
+    uint32_t bbase = abase + 48 * 1024;
+    const uint32_t LBO_A = mode == 4 ? 2048 : 400 * 16;
+    const uint32_t idesc = make_idesc(128, N);
+    const uint64_t a0 = make_desc(abase, LBO_A, 128), b0 = make_desc(bbase, N * 16, 128);
+    __shared__ uint64_t bar2, bar3;
+    mbar_init(smem_u32(&bar2), 1);
+    mbar_init(smem_u32(&bar3), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // complete bar3's phase 0 once so waits on parity 0 succeed immediately
+    asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" :: "r"(smem_u32(&bar3)) : "memory");
+    long long c0 = clock64();
+    for (int it = 0; it < iters; it += 6) {
+      uint32_t d;
+      const int row = it / 6;
+      if (mode == 5 || mode == 8) mma_commit(smem_u32(&bar2));
+      if (mode == 6 || mode == 8) tc_fence_after();
+      if (mode == 7 || mode == 8) mbar_wait(smem_u32(&bar3), 0);
+      if (mode == 9) { mma_commit(smem_u32(&bar2)); mma_commit(smem_u32(&bar2)); mma_commit(smem_u32(&bar2)); }
+      if (mode == 10) {
+        uint32_t ok;
+        do {
+          asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.relaxed.cta.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+                       : "=r"(ok) : "r"(smem_u32(&bar3)), "r"(0) : "memory");
+        } while (!ok);
+      }
+      if (mode == 11) { while (*(volatile uint32_t*)&tmem_base == 0xFFFFFFFFu) {} }
+      if (mode == 12 && (row & 3) == 0) { mbar_wait(smem_u32(&bar3), 0); }
+      if (mode == 13) {
+        uint32_t ok;
+        do {
+          asm volatile("{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+                       : "=r"(ok) : "r"(smem_u32(&bar3)), "r"(0) : "memory");
+        } while (!ok);
+      }
+      if (mode == 3) d = tbase + (uint32_t)((13 - (row % 14)) * 32);
+      else d = tbase + (mode == 1 ? 32u : 0u);
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        uint32_t dd = (mode == 2 && (j & 1)) ? tbase + 32 : d;
+        mma_ss(dd, a0 + (uint32_t)(j * 8), b0 + (uint32_t)((j & 1) * 512), idesc, 1u);
+      }
+    }
+    mma_commit(smem_u32(&bar));
+    mbar_wait(smem_u32(&bar), 0);
+    cyc[blockIdx.x] = clock64() - c0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1 || warp == 0) {}
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(tbase));
+}
+
+void run_pattern(int mode) {
+  long long* dcyc; CK(cudaMalloc(&dcyc, 148 * 8));
+  int smem = 120 * 1024;
+  CK(cudaFuncSetAttribute(pattern_kernel<96>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int iters = 6 * 2000;
+  for (int rep = 0; rep < 2; ++rep) pattern_kernel<96><<<148, 128, smem>>>(iters, mode, dcyc);
+  CK(cudaGetLastError()); CK(cudaDeviceSynchronize());
+  std::vector<long long> cyc(148);
+  CK(cudaMemcpy(cyc.data(), dcyc, 148 * 8, cudaMemcpyDeviceToHost));
+  long long mx = 0; for (auto c : cyc) mx = c > mx ? c : mx;
+  printf("pattern N=96 mode=%d : %.1f cyc/mma\n", mode, (double)mx / iters);
+  cudaFree(dcyc);
+}
+
+
+// group kernel: per group: 2 waits on completed barriers, G*6 MMAs (N=96), 2 commits.
+// variant v: 0 = as described; 1 = no waits/commits; 2 = only commits; 3 = only waits; 4 = 8 ALU ops per row
+template <int G>
+__global__ void group_kernel(int ngroups, int v, long long* cyc) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar, bar2, bar3;
+  __shared__ uint32_t tmem_base;
+  for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x) ((uint32_t*)smem)[i] = 0x3c003c00u;
+  fence_async_smem();
+  int warp = threadIdx.x / 32;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" :: "r"(smem_u32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(&bar), 1); mbar_init(smem_u32(&bar2), 1); mbar_init(smem_u32(&bar3), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" :: "r"(smem_u32(&bar3)) : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint32_t tbase = tmem_base;
+  if (threadIdx.x == 0) {
+    uint32_t abase = smem_u32(smem);
+    uint32_t bbase = abase + 48 * 1024;
+    const uint32_t idesc = make_idesc(128, 96);
+    const uint64_t a0 = make_desc(abase, 6400, 128), b0 = make_desc(bbase, 96 * 16, 128);
+    uint32_t x = threadIdx.x + 7;
+    long long c0 = clock64();
+    for (int g = 0; g < ngroups; ++g) {
+      if (v == 0 || v == 3) { mbar_wait(smem_u32(&bar3), 0); mbar_wait(smem_u32(&bar3), 0); }
+#pragma unroll
+      for (int r = 0; r < G; ++r) {
+        const uint32_t d = tbase + (uint32_t)(((13 - r) & 15) * 32);
+#pragma unroll
+        for (int j = 0; j < 6; ++j) mma_ss(d, a0 + (uint32_t)(j * 8 + r), b0 + (uint32_t)((j & 1) * 512), idesc, 1u);
+        if (v == 4) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) x = x * 1664525u + 1013904223u;
+        }
+      }
+      if (v == 0 || v == 2) { mma_commit(smem_u32(&bar2)); mma_commit(smem_u32(&bar2)); }
+    }
+    mma_commit(smem_u32(&bar));
+    mbar_wait(smem_u32(&bar), 0);
+    cyc[blockIdx.x] = clock64() - c0 + (x == 12345 ? 1 : 0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(tbase));
+}
+
+template <int G>
+void run_group(int v) {
+  long long* dcyc; CK(cudaMalloc(&dcyc, 148 * 8));
+  int smem = 120 * 1024;
+  CK(cudaFuncSetAttribute(group_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int ng = 12000 / (6 * G);
+  for (int rep = 0; rep < 2; ++rep) group_kernel<G><<<148, 128, smem>>>(ng, v, dcyc);
+  CK(cudaGetLastError()); CK(cudaDeviceSynchronize());
+  std::vector<long long> cyc(148);
+  CK(cudaMemcpy(cyc.data(), dcyc, 148 * 8, cudaMemcpyDeviceToHost));
+  long long mx = 0; for (auto c : cyc) mx = c > mx ? c : mx;
+  printf("group G=%d v=%d : %.1f cyc/mma  (%.0f cyc/group)\n", G, v, (double)mx / (ng * 6 * G), (double)mx / ng);
+  cudaFree(dcyc);
+}
+
 template <int N>
 bool run_probe(int mode) {
   const int ROWS = 144;
@@ -211,10 +371,7 @@ void run_tput(int nshift) {
 
 int main() {
   bool ok = true;
-  ok &= run_probe<32>(0); ok &= run_probe<32>(1); ok &= run_probe<32>(2);
-  ok &= run_probe<96>(0); ok &= run_probe<16>(0); ok &= run_probe<144>(1); ok &= run_probe<256>(0);
-  run_tput<16>(1); run_tput<32>(1); run_tput<32>(9); run_tput<48>(1); run_tput<64>(1); run_tput<64>(9);
-  run_tput<96>(1); run_tput<96>(3); run_tput<128>(1); run_tput<144>(1); run_tput<192>(1); run_tput<256>(1);
+  for (int v = 0; v < 5; ++v) { run_group<1>(v); run_group<2>(v); run_group<4>(v); run_group<8>(v); }
   printf("ALL_PROBES %s\n", ok ? "OK" : "FAIL");
   return 0;
 }
