@@ -58,6 +58,7 @@ struct Params {
   int ngs, gslog;           // input group slots (power of two) and log2
   float res_scale;
   unsigned long long* prof; // optional wait-time counters (REGEN_TC_PROF=1), else null
+  int* counter;             // dynamic unit scheduler (zeroed before the launch)
 };
 
 // ------------------------------------------------------------------------------- PTX wrappers
@@ -201,6 +202,17 @@ __device__ __forceinline__ void epi_act(uint32_t taddr, __nv_bfloat16* o, size_t
   }
 }
 
+// upsampler column order: global column n (chunk c = n / CP) -> original output channel (PyTorch
+// PixelShuffle order co = ch * PS^2 + sub-position). Chunk c = i * NG + g covers sub-row i and channel
+// group g (CG = CP / PS channels); column n % CP = j * CG + e is sub-column j, channel g * CG + e.
+template <int C, int CP, int PS>
+__host__ __device__ constexpr int up_column(int n) {
+  constexpr int CG = CP / PS, NG = C / CG;
+  const int c = n / CP, w = n - c * CP;
+  const int i = c / NG, g = c - i * NG, j = w / CG, e = w - j * CG;
+  return (g * CG + e) * PS * PS + i * PS + j;
+}
+
 // ------------------------------------------------------------------------------- kernel
 template <int ROLE, int C, int CP, int R, int G, int T, int PS>
 __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_constant__ Params p) {
@@ -210,7 +222,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
   __shared__ __align__(8) uint64_t acc_full[MAX_OG], acc_empty[MAX_OG];
   __shared__ __align__(8) uint64_t b_full, b_empty;
   __shared__ uint32_t tmem_base_sh;
-  __shared__ __align__(16) float bias_sm[512];   // bias per accumulator column (all chunks)
+  __shared__ __align__(16) float bias_sm[768];   // bias per accumulator column (all chunks)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cin8 = S::HEAD ? 1 : C / 8;
@@ -220,28 +232,35 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
   // SMEM: [1 KB guard][ngs x G rows][B image]
   uint8_t* ring = smem_raw + 1024;
   uint8_t* bimg = ring + ngs * grp_bytes;
-  const int nbins = *p.num_bins;
-  const int per_chunk = p.max_bins * p.nbands;
+  // units are (chunk, bin, band), chunk-major, over the bins actually used; they are handed out by
+  // an atomic counter (the producer) through a small SMEM ring, so CTAs that start late (an SM busy
+  // with another stream's kernel) simply take fewer units
+  const int nbins = min(*p.num_bins, p.max_bins);
+  const int per_chunk = nbins * p.nbands;
   const int total_units = per_chunk * p.nchunk;
+  __shared__ int unit_ring[4];
+  __shared__ __align__(8) uint64_t unit_full[4], unit_empty[4];
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < (int)ngs; ++i) { mbar_init(&in_full[i], 1); mbar_init(&in_empty[i], 1); }
     for (int i = 0; i < S::OGR; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
     mbar_init(&b_full, 1);
     mbar_init(&b_empty, 1);
+    for (int i = 0; i < 4; ++i) { mbar_init(&unit_full[i], 1); mbar_init(&unit_empty[i], 9); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_sh)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  // bias in accumulator-column order: chunk j column n = global column j*CP + n; for the upsampler
-  // the global column g = sub-position sp * C + channel c holds original channel c * PS^2 + sp
-  for (int n = threadIdx.x; n < 512; n += NTHREADS) {
+  // bias in accumulator-column order: chunk c column n = global column c*CP + n. Upsampler chunks are
+  // (sub-row i, channel group g) with columns n = j*CG + e (sub-column j, channel g*CG + e): see
+  // up_column() — each chunk then writes whole HR pixels of CG channels for all sub-columns j.
+  for (int n = threadIdx.x; n < 768; n += NTHREADS) {
     float b = 0.f;
     if (ROLE == ROLE_UP) {
-      const int sp = n / C, c = n - sp * C, co = c * PS * PS + sp;
-      if (sp < PS * PS && co < p.cout) b = __ldg(p.bias + co);
+      const int co = up_column<C, CP, PS>(n);
+      if (co < p.cout) b = __ldg(p.bias + co);
     } else if (n < p.cout) {
       b = __ldg(p.bias + n);
     }
@@ -277,10 +296,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
       uint32_t ig = 0;          // input groups loaded (ring sequence)
       int loaded_chunk = -1;
       uint32_t bload = 0;
-      for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+      for (uint32_t us = 0;; ++us) {
+        int u = atomicAdd(p.counter, 1);
+        if (u >= total_units) u = -1;
+        mbar_wait(&unit_empty[us & 3], ((us >> 2) & 1) ^ 1);
+        unit_ring[us & 3] = u;
+        mbar_arrive(&unit_full[us & 3]);
+        if (u < 0) break;
         const int chunk = u / per_chunk, v = u - chunk * per_chunk;
         const int bin = v / p.nbands, y0 = (v - bin * p.nbands) * BR;
-        if (bin >= nbins) continue;
         if (chunk != loaded_chunk) {
           if (bload > 0) mbar_wait(&b_empty, (bload - 1) & 1);
           mbar_expect_tx(&b_full, p.b_bytes);
@@ -320,10 +344,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
       const uint32_t row16 = row_bytes >> 4, grp16 = grp_bytes >> 4;
       const uint32_t plane16 = (uint32_t)p.Wr;              // A plane stride (16-B units)
       constexpr uint32_t BLBO = (uint32_t)S::N;              // B chunk-plane stride (16-B units)
-      for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+      for (uint32_t us = 0;; ++us) {
+        mbar_wait(&unit_full[us & 3], (us >> 2) & 1);
+        const int u = *(volatile int*)&unit_ring[us & 3];
+        mbar_arrive(&unit_empty[us & 3]);
+        if (u < 0) break;
         const int chunk = u / per_chunk, v = u - chunk * per_chunk;
         const int bin = v / p.nbands, y0 = (v - bin * p.nbands) * BR;
-        if (bin >= nbins) continue;
         if (chunk != cur_chunk) {
           if (cur_chunk >= 0) mma_commit(&b_empty);         // previous B image no longer needed
           mbar_wait(&b_full, bwait & 1);
@@ -403,10 +430,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
     const size_t bin_px = (size_t)p.Hr * p.Wr;
     const size_t pstride = (size_t)p.Wr * 8;                 // elements between planes of one row
     uint32_t og = 0;
-    for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+    for (uint32_t us = 0;; ++us) {
+      mbar_wait(&unit_full[us & 3], (us >> 2) & 1);
+      const int u = *(volatile int*)&unit_ring[us & 3];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&unit_empty[us & 3]);
+      if (u < 0) break;
       const int chunk = u / per_chunk, v = u - chunk * per_chunk;
       const int bin = v / p.nbands, y0 = (v - bin * p.nbands) * BR;
-      if (bin >= nbins) continue;
       const int nrows = min(BR, p.Hr - y0);
       for (int k = 0; k < S::NG_OUT; ++k) {
         const uint32_t og_k = og + k;
@@ -454,23 +485,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
                 val.y = pack_bf16x2(occ ? __uint_as_float(r[2]) : 0.f, 0.f);
                 *reinterpret_cast<uint2*>(p.out + ((size_t)bin * bin_px + (size_t)y * p.Wr + x) * 4) = val;
               } else if (ROLE == ROLE_UP) {
-                // chunk columns [chunk*CP, chunk*CP+CP): + bias, PixelShuffle(PS) into [bin][Y][C/8][X][8]
+                // chunk = (sub-row i, channel group g): + bias, PixelShuffle(PS) into [bin][Y][C/8][X][8];
+                // per plane the PS sub-columns of a pixel are adjacent 16-B chunks (full sectors)
+                constexpr int CG = CP / PS, NG = C / CG;
+                const int i2 = chunk / NG, g2 = chunk - i2 * NG;
                 const int Wo = p.Wr * PS;
-                __nv_bfloat16* obin = p.out + (size_t)bin * bin_px * PS * PS * C;
+                __nv_bfloat16* orow = p.out + (size_t)bin * bin_px * PS * PS * C +
+                                      (size_t)(y * PS + i2) * (C / 8) * Wo * 8 + (size_t)(x * PS) * 8;
                 uint32_t r[CP];
 #pragma unroll
                 for (int c = 0; c < CP; c += 16) tmem_ld16(taddr + (uint32_t)c, r + c);
                 tmem_ld_wait();
 #pragma unroll
-                for (int g = 0; g < CP / 8; ++g) {
-                  const int n0 = chunk * CP + 8 * g;
-                  const int sp = n0 / C, c = n0 - sp * C;
-                  const int i2 = sp / PS, j2 = sp - i2 * PS;
-                  float vv[8];
+                for (int q = 0; q < CG / 8; ++q) {
+                  __nv_bfloat16* o = orow + (size_t)(g2 * (CG / 8) + q) * Wo * 8;
 #pragma unroll
-                  for (int e = 0; e < 8; ++e) vv[e] = __uint_as_float(r[8 * g + e]) + bias_sm[n0 + e];
-                  __nv_bfloat16* o = obin + (((size_t)(y * PS + i2) * (C / 8) + c / 8) * Wo + (x * PS + j2)) * 8;
-                  *reinterpret_cast<uint4*>(o) = pack8(vv, occ);
+                  for (int j2 = 0; j2 < PS; ++j2) {
+                    const int cl = j2 * CG + 8 * q;      // column within the chunk
+                    float vv[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) vv[e] = __uint_as_float(r[cl + e]) + bias_sm[chunk * CP + cl + e];
+                    *reinterpret_cast<uint4*>(o + j2 * 8) = pack8(vv, occ);
+                  }
                 }
               } else {
                 const size_t act = (size_t)bin * bin_px * p.out_c8 * 8 + (size_t)y * p.out_c8 * pstride + (size_t)x * 8;
@@ -572,11 +608,15 @@ static bool plan_conv(const ConvDesc& d, int C, int res, int bin_w, Plan& pl, st
   const uint32_t row_bytes = (uint32_t)(head ? 1 : d.cin / 8) * Wr * 16;
   const int kc = head ? 1 : d.cin / 16, nsteps = head ? 2 : 3 * kc;
   if (d.role == ROLE_UP) {
-    for (int cand : {64, 48, 32, 16})
-      if (d.cout % cand == 0 && ring_shape(cand, pl.T, row_bytes, (uint32_t)(nsteps * 3 * cand * 32), pl.R, pl.G)) {
+    // chunk = (sub-row, group of CG channels x PS sub-columns): CP = PS * CG
+    for (int cg : {32, 16}) {
+      const int cand = d.ps * cg;
+      if (C % cg == 0 && 3 * cand <= 256 && cand % 16 == 0 &&
+          ring_shape(cand, pl.T, row_bytes, (uint32_t)(nsteps * 3 * cand * 32), pl.R, pl.G)) {
         CP = cand;
         break;
       }
+    }
     if (CP == 0) return false;
   } else {
     CP = (d.cout + 15) / 16 * 16;
@@ -598,8 +638,9 @@ static bool plan_conv(const ConvDesc& d, int C, int res, int bin_w, Plan& pl, st
         for (int n = 0; n < CP; ++n) {
           int co;
           if (d.role == ROLE_UP) {
-            const int col = j * CP + n, sp = col / C, c = col % C;
-            co = c * s2 + sp;
+            const int col = j * CP + n, cg = CP / d.ps, ng = C / cg;
+            const int cc = col / CP, w = col - cc * CP, i = cc / ng, gg = cc - i * ng, jj = w / cg, e = w - jj * cg;
+            co = (gg * cg + e) * s2 + i * d.ps + jj;
           } else {
             co = n;
           }
@@ -647,9 +688,9 @@ static KernFn lookup(int role, int C, int CP, int R, int G, int T, int PS) {
   K(ROLE_TAIL, 16, 16, 8, 2, 3, 1)
   K(ROLE_TAIL, 16, 16, 8, 2, 4, 1)
   K(ROLE_TINY0, 16, 16, 16, 4, 1, 1)
+  K(ROLE_UP, 16, 32, 16, 4, 1, 2)
+  K(ROLE_UP, 16, 32, 8, 2, 2, 2)
   K(ROLE_UP, 16, 48, 8, 2, 1, 3)
-  K(ROLE_UP, 16, 64, 8, 2, 1, 2)
-  K(ROLE_UP, 16, 64, 4, 1, 2, 2)
   K(ROLE_BODY, 32, 32, 16, 4, 1, 1)
   K(ROLE_HEAD, 32, 32, 16, 4, 1, 1)
   K(ROLE_RES_A, 32, 32, 16, 4, 1, 1)
@@ -669,9 +710,9 @@ static KernFn lookup(int role, int C, int CP, int R, int G, int T, int PS) {
   K(ROLE_TAIL, 48, 16, 8, 2, 3, 1)
   K(ROLE_TAIL, 48, 16, 8, 2, 4, 1)
   K(ROLE_TINY0, 48, 48, 8, 2, 1, 1)
+  K(ROLE_UP, 48, 32, 16, 4, 1, 2)
+  K(ROLE_UP, 48, 32, 8, 2, 2, 2)
   K(ROLE_UP, 48, 48, 8, 2, 1, 3)
-  K(ROLE_UP, 48, 64, 8, 2, 1, 2)
-  K(ROLE_UP, 48, 64, 4, 1, 2, 2)
   K(ROLE_BODY, 64, 64, 8, 2, 1, 1)
   K(ROLE_HEAD, 64, 64, 8, 2, 1, 1)
   K(ROLE_RES_A, 64, 64, 8, 2, 1, 1)
@@ -680,8 +721,8 @@ static KernFn lookup(int role, int C, int CP, int R, int G, int T, int PS) {
   K(ROLE_TAIL, 64, 16, 8, 2, 3, 1)
   K(ROLE_TAIL, 64, 16, 8, 1, 4, 1)
   K(ROLE_TINY0, 64, 64, 8, 2, 1, 1)
+  K(ROLE_UP, 64, 48, 8, 2, 1, 3)
   K(ROLE_UP, 64, 64, 8, 2, 1, 2)
-  K(ROLE_UP, 64, 64, 8, 2, 1, 3)
   K(ROLE_UP, 64, 64, 4, 1, 2, 2)
 #undef K
   return nullptr;
@@ -770,7 +811,7 @@ bool conv_tc_supported(const SRNet* net, const ConvDesc& cv, int bin_w) {
 
 regen_status conv_tc_launch(const SRNet* net, const ConvDesc& cv, const void* in, void* out, const void* skip,
                             const uint32_t* mbits, int max_bins, const int32_t* d_num_bins, int bin_w, int bin_h,
-                            cudaStream_t s) {
+                            int* counter, cudaStream_t s) {
   using namespace tc;
   const Plan* pl = get_plan(const_cast<SRNet*>(net), cv, bin_w);
   REGEN_REQUIRE(pl != nullptr, "no tcgen05 plan for conv");
@@ -795,6 +836,7 @@ regen_status conv_tc_launch(const SRNet* net, const ConvDesc& cv, const void* in
   p.max_bins = max_bins;
   p.out_c8 = cv.role == ROLE_UP ? net->cfg.channels / 8 : (cv.cout + 7) / 8;
   p.res_scale = cv.role == ROLE_RES_B ? net->cfg.res_scale : 1.0f;
+  p.counter = counter;
   const int cin8 = cv.cin == 3 ? 1 : cv.cin / 8;
   const uint32_t grp_bytes = (uint32_t)cin8 * p.Wr * 16 * pl->G;
   // deepest input ring that fits (row loads are latency-bound: more rows in flight per SM)

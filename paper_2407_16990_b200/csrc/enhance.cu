@@ -336,6 +336,7 @@ EnhanceBufs enhance_bufs(const SRNet* net, const regen_pack_params& p, void* bas
   EnhanceBufs e;
   e.map = c.take<int32_t>(px);
   e.mbits = c.take<uint32_t>((size_t)p.max_bins * p.bin_h * ((p.bin_w + 31) / 32));
+  e.counters = c.take<int32_t>(64);
   e.x0 = c.take<uint8_t>(px * 8 * es);
   e.a0 = c.take<uint8_t>(px * C8 * 8 * es);
   if (net->cfg.n_resblocks > 0) {
@@ -354,7 +355,8 @@ static regen_status run_conv(const SRNet* net, const ConvDesc& cv, const void* i
                              const EnhanceBufs& e, const regen_pack_params& p, const int32_t* d_num_bins,
                              cudaStream_t s) {
   if (net->use_tc && conv_tc_supported(net, cv, p.bin_w))
-    return conv_tc_launch(net, cv, in, out, skip, e.mbits, p.max_bins, d_num_bins, p.bin_w, p.bin_h, s);
+    return conv_tc_launch(net, cv, in, out, skip, e.mbits, p.max_bins, d_num_bins, p.bin_w, p.bin_h,
+                          e.counters + (&cv - net->convs.data()), s);
   return conv_simt_launch(net, cv, in, out, skip, e.map, p.max_bins, d_num_bins, p.bin_w, p.bin_h, s);
 }
 
@@ -433,6 +435,7 @@ extern "C" regen_status regen_enhance_packed(void* sr, const regen_geom* geom, c
   REGEN_REQUIRE(d_ws && ws_bytes >= e.bytes, "workspace too small (%zu < %zu)", ws_bytes, e.bytes);
   e = enhance_bufs(net, *p, d_ws);
   cudaStream_t s = (cudaStream_t)stream;
+  REGEN_CUDA(cudaMemsetAsync(e.counters, 0, 64 * sizeof(int32_t), s));
   st = stitch_into(*geom, *p, net->cfg.dtype, 0, d_frames, d_boxes, d_num_boxes, max_boxes, d_num_bins, e.map, e.x0, s,
                    e.mbits);
   if (st != REGEN_OK) return st;

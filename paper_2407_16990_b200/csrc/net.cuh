@@ -50,6 +50,7 @@ struct SRNet {
 struct EnhanceBufs {
   int32_t* map;      // [max_bins][bin_h][bin_w] box index covering the pixel, -1 outside boxes
   uint32_t* mbits;   // [max_bins][bin_h][ceil(bin_w/32)] occupancy bits (map >= 0)
+  int32_t* counters; // [64] per-conv dynamic scheduler counters, zeroed per call
   void* x0;          // [max_bins][bin_h][1][bin_w][8]
   void* a0;          // [max_bins][bin_h][C/8][bin_w][8]  (h)
   void* a1;          // (r)
@@ -70,6 +71,6 @@ regen_status conv_tc_prepare(SRNet* net);
 void conv_tc_release(SRNet* net);
 regen_status conv_tc_launch(const SRNet* net, const ConvDesc& cv, const void* in, void* out, const void* skip,
                             const uint32_t* mbits, int max_bins, const int32_t* d_num_bins, int bin_w, int bin_h,
-                            cudaStream_t s);
+                            int* counter, cudaStream_t s);
 
 }  // namespace regen

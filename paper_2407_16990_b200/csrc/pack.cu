@@ -10,6 +10,8 @@
 //                      threads; per box one block-wide min-reduction finds the first fitting free area
 //                      in (bin, seq) order (D12); every thread replays the same decision and the slot
 //                      owners apply the guillotine remainders (D6). Unopened bins are implicit.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace regen {
@@ -179,8 +181,8 @@ __global__ void __launch_bounds__(256) sort_rank_kernel(regen_box* boxes, const 
 
 // ------------------------------------------------------------------------------------ pack
 
-constexpr int PACK_THREADS = 512;
-constexpr int PACK_POOL = 12288;              // free-area slots (SMEM), statically owned: slot % PACK_THREADS
+constexpr int PACK_POOL = 8192;   // live free areas (SMEM), kept compact
+constexpr int PACK_DIMS = 8192;   // box footprints + indices staged in SMEM in packing order
 
 struct PackArgs {
   regen_box* boxes;
@@ -190,90 +192,111 @@ struct PackArgs {
   int32_t* num_bins;
   int32_t* status;
   int bin_w, bin_h, max_bins, gutter;
+  int prof;   // REGEN_PACK_PROF=1: print per-phase cycle counts
 };
 
-// slot record: key = bin<<44 | seq<<18 | slot (unique; min = first in (bin, seq) order)
-__global__ void __launch_bounds__(PACK_THREADS, 1) pack_kernel(PackArgs a) {
+// One warp. The live free areas of the opened bins form a compact pool in SMEM: key = bin << 32 |
+// creation sequence (unique; its minimum is the first area in (bin, seq) order, D12), rect = x | y<<16
+// | w<<32 | h<<48. Per box: lanes scan the pool (fit test unrotated or rotated), a warp
+// min-reduction picks the first fit, every lane replays the placement and lane 0 applies the
+// guillotine remainders (D6): the consumed area is overwritten by the first kept remainder (or by the
+// pool's last entry), the second is appended. Unopened bins are implicit (opened lazily in order).
+__global__ void __launch_bounds__(32, 1) pack_kernel(PackArgs a) {
   extern __shared__ uint8_t psm[];
-  uint64_t* key = (uint64_t*)psm;                       // PACK_POOL; ~0 = empty
-  uint64_t* rect = key + PACK_POOL;                     // x | y<<16 | w<<32 | h<<48
-  __shared__ uint64_t wmin[2][PACK_THREADS / 32];
-  __shared__ uint64_t wrect[2][PACK_THREADS / 32];
-  __shared__ int s_minA, s_minB;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint64_t* key = (uint64_t*)psm;                       // PACK_POOL
+  uint64_t* rect = key + PACK_POOL;                     // PACK_POOL
+  uint32_t* dims = (uint32_t*)(rect + PACK_POOL);       // (w+g) | (h+g)<<16 of the oi-th box in order
+  int32_t* ords = (int32_t*)(dims + PACK_DIMS);         // box index of the oi-th box in order
+  const int lane = threadIdx.x;
   const int64_t n = min(*a.num_boxes, a.max_boxes);
-  for (int i = tid; i < PACK_POOL; i += PACK_THREADS) key[i] = ~0ull;
-  // placement-invariant pruning bounds: a free area narrower than every box can never be used
+  // placement-invariant pruning bounds: a free area no box fits in (either orientation) is never stored
   int mA = 1 << 30, mB = 1 << 30;
-  for (int64_t i = tid; i < n; i += PACK_THREADS) {
-    const int pw = a.boxes[i].w + a.gutter, ph = a.boxes[i].h + a.gutter;
+  for (int64_t i = lane; i < n; i += 32) {
+    const int bi = a.order[i];
+    const regen_box& bx = a.boxes[bi];
+    const int pw = bx.w + a.gutter, ph = bx.h + a.gutter;
     mA = min(mA, min(pw, ph));
     mB = min(mB, max(pw, ph));
+    if (i < PACK_DIMS) {
+      dims[i] = (uint32_t)pw | ((uint32_t)ph << 16);
+      ords[i] = bi;
+    }
   }
-  if (tid == 0) { s_minA = 1 << 30; s_minB = 1 << 30; }
-  __syncthreads();
-  atomicMin(&s_minA, mA);
-  atomicMin(&s_minB, mB);
-  __syncthreads();
-  const int minA = s_minA, minB = s_minB;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mA = min(mA, __shfl_xor_sync(0xffffffffu, mA, o));
+    mB = min(mB, __shfl_xor_sync(0xffffffffu, mB, o));
+  }
+  __syncwarp();
   const int FW = a.bin_w - 1, FH = a.bin_h + a.gutter;   // a fresh bin's free area (x=1, y=0)
-  int hw = 0;        // slots in use: [0, hw)
+  int hw = 0;        // live areas: [0, hw)
   int opened = 0;    // bins opened (lazily, in index order)
-  uint32_t seq = 0;
+  uint64_t seq = 0;
   int used = 0;
   bool overflow = false;
+  long long c_scan = 0, c_dec = 0, c_upd = 0, hw_sum = 0;
   for (int64_t oi = 0; oi < n; ++oi) {
-    const int b = a.order[oi];
-    const int pw = a.boxes[b].w + a.gutter, ph = a.boxes[b].h + a.gutter;
-    // phase A: first fitting free area among my slots (key, rect) pairs
+    const long long t0 = clock64();
+    int pw, ph, b;
+    if (oi < PACK_DIMS) {
+      const uint32_t d = dims[oi];
+      pw = (int)(d & 0xFFFF);
+      ph = (int)(d >> 16);
+      b = ords[oi];
+    } else {
+      b = a.order[oi];
+      pw = a.boxes[b].w + a.gutter;
+      ph = a.boxes[b].h + a.gutter;
+    }
     uint64_t best = ~0ull, brect = 0;
-    for (int s = tid; s < hw; s += PACK_THREADS) {
-      const uint64_t k = key[s];
-      if (k == ~0ull) continue;
-      const uint64_t rr = rect[s];
-      const int fw = (int)((rr >> 32) & 0xFFFF), fh = (int)(rr >> 48);
-      if (((fw >= pw && fh >= ph) || (fw >= ph && fh >= pw)) && k < best) { best = k; brect = rr; }
-    }
+    int bslot = -1;
+    // 4 independent SMEM loads in flight per lane per step
+    for (int s0 = lane; s0 < hw; s0 += 128) {
+      uint64_t kk[4], rr[4];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint64_t k2 = __shfl_xor_sync(0xffffffffu, best, o);
-      const uint64_t r2 = __shfl_xor_sync(0xffffffffu, brect, o);
-      if (k2 < best) { best = k2; brect = r2; }
-    }
-    const int buf = (int)(oi & 1);
-    if (lane == 0) { wmin[buf][warp] = best; wrect[buf][warp] = brect; }
-    __syncthreads();
-    best = lane < PACK_THREADS / 32 ? wmin[buf][lane] : ~0ull;
-    brect = lane < PACK_THREADS / 32 ? wrect[buf][lane] : 0;
+      for (int u = 0; u < 4; ++u) {
+        const int s = s0 + 32 * u;
+        kk[u] = s < hw ? key[s] : ~0ull;
+        rr[u] = s < hw ? rect[s] : 0ull;
+      }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint64_t k2 = __shfl_xor_sync(0xffffffffu, best, o);
-      const uint64_t r2 = __shfl_xor_sync(0xffffffffu, brect, o);
-      if (k2 < best) { best = k2; brect = r2; }
+      for (int u = 0; u < 4; ++u) {
+        const int fw = (int)((rr[u] >> 32) & 0xFFFF), fh = (int)(rr[u] >> 48);
+        if (((fw >= pw && fh >= ph) || (fw >= ph && fh >= pw)) && kk[u] < best) {
+          best = kk[u]; brect = rr[u]; bslot = s0 + 32 * u;
+        }
+      }
     }
-    // replicated decision (every thread computes the same placement)
+    const long long t1 = clock64();
+    hw_sum += hw;
+    // 64-bit warp min as two 32-bit REDUX (bin in the high word, sequence in the low word)
+    const uint32_t bhi = (uint32_t)(best >> 32);
+    const uint32_t mhi = __reduce_min_sync(0xffffffffu, bhi);
+    const uint32_t mlo = __reduce_min_sync(0xffffffffu, bhi == mhi ? (uint32_t)best : 0xFFFFFFFFu);
+    const uint64_t wbest = ((uint64_t)mhi << 32) | mlo;
     int fx = 0, fy = 0, fw = 0, fh = 0, bin = 0, slot = -1;
     bool place = false;
-    if (best != ~0ull) {
-      slot = (int)(best & 0x3FFFF);
+    if (wbest != ~0ull) {
+      // the lane holding the winner broadcasts its rect and slot
+      const uint32_t holder = __ballot_sync(0xffffffffu, best == wbest);
+      const int hl = __ffs(holder) - 1;
+      brect = __shfl_sync(0xffffffffu, brect, hl);
+      slot = __shfl_sync(0xffffffffu, bslot, hl);
       fx = (int)(brect & 0xFFFF); fy = (int)((brect >> 16) & 0xFFFF);
       fw = (int)((brect >> 32) & 0xFFFF); fh = (int)(brect >> 48);
-      bin = (int)(best >> 44);
+      bin = (int)(wbest >> 32);
       place = true;
     } else if (opened < a.max_bins && ((FW >= pw && FH >= ph) || (FW >= ph && FH >= pw))) {
       bin = opened++;
       fx = 1; fy = 0; fw = FW; fh = FH;
       place = true;
     }
+    const long long t2 = clock64();
+    c_scan += t1 - t0;
+    c_dec += t2 - t1;
     if (place) {
       const bool rot = !(fw >= pw && fh >= ph);
       const int uw = rot ? ph : pw, uh = rot ? pw : ph;
-      if (tid == 0) {
-        a.boxes[b].bin = bin;
-        a.boxes[b].bx = fx;
-        a.boxes[b].by = fy;
-        a.boxes[b].rotated = rot ? 1 : 0;
-      }
       used = max(used, bin + 1);
       // InnerFree (D6): guillotine remainders
       const int64_t v_a = (int64_t)(fw - uw) * fh, v_b = (int64_t)uw * (fh - uh);
@@ -287,27 +310,39 @@ __global__ void __launch_bounds__(PACK_THREADS, 1) pack_kernel(PackArgs a) {
         rx[0] = fx; ry[0] = fy + uh; rw[0] = fw; rh[0] = fh - uh;
         rx[1] = fx + uw; ry[1] = fy; rw[1] = fw - uw; rh[1] = uh;
       }
-      int reuse = slot;  // the consumed slot is reused by the first kept remainder
-      if (slot >= 0 && tid == (slot % PACK_THREADS)) key[slot] = ~0ull;
+      if (lane == 0) {
+        a.boxes[b].bin = bin;
+        a.boxes[b].bx = fx;
+        a.boxes[b].by = fy;
+        a.boxes[b].rotated = rot ? 1 : 0;
+      }
+      // every lane replays the pool bookkeeping (identical state); lane 0 performs the SMEM writes
+      int free_slot = slot;   // the consumed area's slot, to be refilled
       for (int t = 0; t < 2; ++t) {
         if (rw[t] <= 0 || rh[t] <= 0) continue;
-        const uint32_t sq = seq++;   // sequence numbers follow the oracle's creation order
-        // prune areas no box of this call can ever use (placement-invariant)
-        if (min(rw[t], rh[t]) < minA || max(rw[t], rh[t]) < minB) continue;
+        const uint64_t sq = seq++;   // sequence numbers follow the oracle's creation order
+        if (min(rw[t], rh[t]) < mA || max(rw[t], rh[t]) < mB) continue;   // unusable: never stored
         int dst;
-        if (reuse >= 0) { dst = reuse; reuse = -1; }
-        else {
-          if (hw >= PACK_POOL) { overflow = true; continue; }
-          dst = hw++;
-        }
-        if (tid == (dst % PACK_THREADS)) {
-          key[dst] = ((uint64_t)bin << 44) | ((uint64_t)sq << 18) | (uint64_t)dst;
+        if (free_slot >= 0) { dst = free_slot; free_slot = -1; }
+        else if (hw < PACK_POOL) dst = hw++;
+        else { overflow = true; continue; }
+        if (lane == 0) {
+          key[dst] = ((uint64_t)bin << 32) | (uint32_t)sq;
           rect[dst] = (uint64_t)rx[t] | ((uint64_t)ry[t] << 16) | ((uint64_t)rw[t] << 32) | ((uint64_t)rh[t] << 48);
         }
       }
+      if (free_slot >= 0) {   // nothing refilled the consumed slot: move the last live area into it
+        --hw;
+        if (lane == 0 && free_slot != hw) { key[free_slot] = key[hw]; rect[free_slot] = rect[hw]; }
+      }
+      __syncwarp();
     }
+    c_upd += clock64() - t2;
   }
-  if (tid == 0) {
+  if (a.prof && lane == 0)
+    printf("[pack-prof] boxes %lld scan %lld dec %lld upd %lld cycles, mean live areas %.1f, bins %d\n", (long long)n,
+           c_scan, c_dec, c_upd, n ? (double)hw_sum / n : 0.0, used);
+  if (lane == 0) {
     *a.num_bins = used;
     if (overflow) atomicOr(a.status, REGEN_ST_FREELIST_OVERFLOW);
   }
@@ -416,10 +451,18 @@ extern "C" regen_status regen_pack_regions(const regen_geom* geom, const regen_p
   k.bin_h = p->bin_h;
   k.max_bins = p->max_bins;
   k.gutter = p->gutter;
-  const size_t smem = (size_t)PACK_POOL * 16;
+  {
+    const char* e = getenv("REGEN_PACK_PROF");
+    k.prof = (e && e[0] == '1') ? 1 : 0;
+  }
+  const size_t smem = (size_t)PACK_POOL * 16 + (size_t)PACK_DIMS * 8;
   REGEN_CUDA(cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  pack_kernel<<<1, PACK_THREADS, smem, s>>>(k);
+  pack_kernel<<<1, 32, smem, s>>>(k);
   REGEN_LAUNCH_CHECK();
+  if (k.prof) {
+    cudaStreamSynchronize(s);
+    fflush(stdout);
+  }
   owner_fix_kernel<<<(unsigned)((n_mbs(g) + 255) / 256), 256, 0, s>>>(d_mb_owner, n_mbs(g), d_boxes, d_num_boxes,
                                                                        max_boxes);
   REGEN_LAUNCH_CHECK();

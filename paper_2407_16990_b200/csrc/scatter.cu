@@ -29,55 +29,75 @@ __global__ void __launch_bounds__(128) scatter_kernel(ScatterArgs a) {
   const int64_t sf = blockIdx.z;
   const int Y = blockIdx.y;
   const int X0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  // separable bilinear (D10): the block first interpolates the LR row pair vertically for the LR
+  // columns its 8*128 HR pixels touch, into SMEM
+  __shared__ float vrow[3 * (8 * 128 / 2 + 4)];
+  const int Xb = blockIdx.x * blockDim.x * 8;
+  const int xa_blk = min((int)fmaxf(((float)Xb + 0.5f) * a.inv_s - 0.5f, 0.0f), a.W - 1);
+  const int xb_blk = min((int)fmaxf(((float)min(Xb + 8 * (int)blockDim.x, a.OW) - 0.5f) * a.inv_s - 0.5f, 0.0f) + 1, a.W - 1);
+  {
+    const uint8_t* img = a.frames + sf * (int64_t)a.H * a.W * 3;
+    const float sy = fmaxf(((float)Y + 0.5f) * a.inv_s - 0.5f, 0.0f);
+    const int yl0 = min((int)sy, a.H - 1);
+    const int yl1 = min(yl0 + 1, a.H - 1);
+    const float ly = sy - (float)yl0;
+    const uint8_t* r0 = img + ((size_t)yl0 * a.W + xa_blk) * 3;
+    const uint8_t* r1 = img + ((size_t)yl1 * a.W + xa_blk) * 3;
+    const int n = (xb_blk - xa_blk + 1) * 3;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const float p0 = (float)r0[i], p1 = (float)r1[i];
+      vrow[i] = fmaf(ly, p1 - p0, p0);
+    }
+  }
+  __syncthreads();
   if (X0 >= a.OW) return;
-  const uint8_t* img = a.frames + sf * (int64_t)a.H * a.W * 3;
-  // vertical bilinear taps (shared by the 8 pixels)
-  float sy = fmaxf(((float)Y + 0.5f) * a.inv_s - 0.5f, 0.0f);
-  int y0 = min((int)sy, a.H - 1);
-  const int y1 = min(y0 + 1, a.H - 1);
-  const float ly = sy - (float)y0;
-  const int my = Y / (a.mb * a.s);
-  const int32_t* own_row = a.owner + (sf * a.GH + my) * a.GW;
-  const int HW = a.s * a.bin_w, HH = a.s * a.bin_h;
   float o[24];
+  // the 8 pixels lie in one MB column (16*s is a multiple of 8), so one owner lookup serves them all
+  const int32_t b = a.owner[(sf * a.GH + Y / (a.mb * a.s)) * a.GW + X0 / (a.mb * a.s)];
+  if (b >= 0) {
+    const regen_box* bp = a.boxes + b;
+    const int x0 = bp->x0, y0 = bp->y0, hh = bp->h, bin = bp->bin, bbx = bp->bx, bby = bp->by, rot = bp->rotated;
+    const int HW = a.s * a.bin_w, HH = a.s * a.bin_h;
+    const int u0 = X0 - a.s * x0, v = Y - a.s * y0;
+    const TH* hb = (const TH*)a.hr + (size_t)bin * HH * HW * 4;
+    // 8 B per pixel (4 channels); one 8-B load per pixel
+    const TH* src = !rot ? hb + ((size_t)(a.s * bby + v) * HW + a.s * bbx + u0) * 4
+                         : hb + ((size_t)(a.s * bby + u0) * HW + a.s * bbx + (a.s * hh - 1 - v)) * 4;
+    const size_t step = !rot ? 4 : (size_t)HW * 4;   // rotated 90 deg CW: box-local (u, v) <- bin (s*h-1-v, u)
+    if (sizeof(TH) == 2) {
+      uint2 q[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int X = X0 + k;
-    float r0 = 0.f, r1 = 0.f, r2 = 0.f;
-    if (X < a.OW) {
-      const int32_t b = own_row[X / (a.mb * a.s)];
-      if (b >= 0) {
-        const regen_box bx = a.boxes[b];
-        const int u = X - a.s * bx.x0, v = Y - a.s * bx.y0;
-        int xb, yb;
-        if (bx.rotated) { xb = a.s * bx.bx + (a.s * bx.h - 1 - v); yb = a.s * bx.by + u; }
-        else { xb = a.s * bx.bx + u; yb = a.s * bx.by + v; }
-        const TH* src = (const TH*)a.hr + (((int64_t)bx.bin * HH + yb) * HW + xb) * 4;
-        r0 = ld_hr<TH>(src);
-        r1 = ld_hr<TH>(src + 1);
-        r2 = ld_hr<TH>(src + 2);
-      } else {
-        float sx = fmaxf(((float)X + 0.5f) * a.inv_s - 0.5f, 0.0f);
-        const int x0 = min((int)sx, a.W - 1);
-        const int x1 = min(x0 + 1, a.W - 1);
-        const float lx = sx - (float)x0;
-        const uint8_t* p00 = img + ((int64_t)y0 * a.W + x0) * 3;
-        const uint8_t* p01 = img + ((int64_t)y0 * a.W + x1) * 3;
-        const uint8_t* p10 = img + ((int64_t)y1 * a.W + x0) * 3;
-        const uint8_t* p11 = img + ((int64_t)y1 * a.W + x1) * 3;
-        float v3[3];
+      for (int k = 0; k < 8; ++k) q[k] = *reinterpret_cast<const uint2*>(src + (size_t)k * step);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const float top = (1.f - lx) * (float)p00[c] + lx * (float)p01[c];
-          const float bot = (1.f - lx) * (float)p10[c] + lx * (float)p11[c];
-          v3[c] = ((1.f - ly) * top + ly * bot) * (1.0f / 255.0f);
-        }
-        r0 = v3[0]; r1 = v3[1]; r2 = v3[2];
+      for (int k = 0; k < 8; ++k) {
+        const float2 f01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&q[k].x));
+        const float2 f23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&q[k].y));
+        o[3 * k] = f01.x;
+        o[3 * k + 1] = f01.y;
+        o[3 * k + 2] = f23.x;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float4 f = *reinterpret_cast<const float4*>(src + (size_t)k * step);
+        o[3 * k] = f.x;
+        o[3 * k + 1] = f.y;
+        o[3 * k + 2] = f.z;
       }
     }
-    o[3 * k] = r0;
-    o[3 * k + 1] = r1;
-    o[3 * k + 2] = r2;
+  } else {
+    // horizontal pass over the block's vertically interpolated LR row segment (SMEM)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float sx = fmaxf(((float)(X0 + k) + 0.5f) * a.inv_s - 0.5f, 0.0f);
+      const int xl0 = min((int)sx, a.W - 1);
+      const int xl1 = min(xl0 + 1, a.W - 1);
+      const float lx = sx - (float)xl0;
+      const float* v0 = vrow + 3 * (xl0 - xa_blk);
+      const float* v1 = vrow + 3 * (xl1 - xa_blk);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) o[3 * k + c] = fmaf(lx, v1[c] - v0[c], v0[c]) * (1.0f / 255.0f);
+    }
   }
   TO* dst = (TO*)a.out + ((sf * a.OH + Y) * (int64_t)a.OW + X0) * 3;
   if (X0 + 8 <= a.OW && ((((uintptr_t)dst) & 15) == 0)) {
@@ -116,7 +136,7 @@ extern "C" regen_status regen_scatter_blend(const regen_geom* geom, const regen_
   regen_status st = validate_geom(geom);
   if (st != REGEN_OK) return st;
   REGEN_REQUIRE(p != nullptr, "pack params null");
-  REGEN_REQUIRE(scale >= 1 && scale <= 8, "bad scale");
+  REGEN_REQUIRE(scale >= 2 && scale <= 8, "scale must be in [2, 8]");
   REGEN_REQUIRE(hr_dtype == REGEN_DTYPE_BF16 || hr_dtype == REGEN_DTYPE_FP32, "bad hr dtype");
   REGEN_REQUIRE(out_dtype == REGEN_DTYPE_BF16 || out_dtype == REGEN_DTYPE_FP32, "bad out dtype");
   REGEN_REQUIRE(d_frames && d_boxes && d_mb_owner && d_hr_bins && d_out, "null device pointer");
