@@ -256,10 +256,13 @@ class Pipeline:
         return self.scatter(frames, out, stream)
 
     def n_convs(self) -> int:
+        """Conv kernel launches per enhance call (a fused residual block is one launch)."""
         c = self.sr.cfg
         if c.n_resblocks == 0:
             return 2
-        return 1 + 2 * c.n_resblocks + 1 + (2 if c.scale == 4 else 1) + 1
+        fused = (c.dtype == DTYPE_BF16 and c.channels in (16, 32) and self.pack.bin_w == 128
+                 and os.environ.get("REGEN_NO_FUSED_RESBLOCK", "0") != "1")
+        return 1 + (1 if fused else 2) * c.n_resblocks + 1 + (2 if c.scale == 4 else 1) + 1
 
     def launches_per_step(self) -> int:
         """Kernels libregen launches per run(): select 4, pack 7, enhance 2 + one per conv, scatter 1."""

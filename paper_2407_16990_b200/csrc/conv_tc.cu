@@ -29,7 +29,7 @@
 
 #include <vector>
 
-#include "net.cuh"
+#include "tc_common.cuh"
 
 namespace regen {
 
@@ -60,97 +60,6 @@ struct Params {
   unsigned long long* prof; // optional wait-time counters (REGEN_TC_PROF=1), else null
   int* counter;             // dynamic unit scheduler (zeroed before the launch)
 };
-
-// ------------------------------------------------------------------------------- PTX wrappers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__host__ __device__ constexpr uint32_t make_idesc(int N) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-}
-constexpr uint32_t DESC_HI = (128u >> 4) | (1u << 14);   // SBO = 128 B, descriptor version 1
-
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint32_t a_lo, uint32_t b_lo, uint32_t idesc,
-                                         uint32_t enable) {
-  // D[tmem] += A[smem] * B[smem]; issued only if `enable` (predicated, no branch)
-  const uint64_t a = ((uint64_t)DESC_HI << 32) | a_lo, b = ((uint64_t)DESC_HI << 32) | b_lo;
-  asm volatile(
-      "{\n.reg .pred e;\nsetp.ne.b32 e, %4, 0;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 1;\n}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(enable));
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t cnt) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(cnt) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = smem_u32(bar);
-  uint32_t ok;
-  do {
-    asm volatile(
-        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(a), "r"(parity)
-        : "memory");
-  } while (!ok);
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ bool elect_one() {
-  uint32_t pred;
-  asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n" : "=r"(pred));
-  return pred != 0;
-}
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
-          taddr),
-      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
-      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
-      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])),
-      "r"(__float_as_uint(v[11])), "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])),
-      "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
-      : "memory");
-}
-__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
-__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
-  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<uint32_t*>(&h);
-}
-__device__ __forceinline__ uint4 pack8(const float* r, bool occ) {
-  uint4 val;
-  val.x = pack_bf16x2(occ ? r[0] : 0.f, occ ? r[1] : 0.f);
-  val.y = pack_bf16x2(occ ? r[2] : 0.f, occ ? r[3] : 0.f);
-  val.z = pack_bf16x2(occ ? r[4] : 0.f, occ ? r[5] : 0.f);
-  val.w = pack_bf16x2(occ ? r[6] : 0.f, occ ? r[7] : 0.f);
-  return val;
-}
 
 // ------------------------------------------------------------------------------- compile-time shape
 template <int ROLE, int C, int CP, int R, int G, int T, int PS>
@@ -220,7 +129,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t in_full[MAX_GSLOTS], in_empty[MAX_GSLOTS];
   __shared__ __align__(8) uint64_t acc_full[MAX_OG], acc_empty[MAX_OG];
-  __shared__ __align__(8) uint64_t b_full, b_empty;
+  __shared__ __align__(8) uint64_t b_full[2], b_empty[2];
   __shared__ uint32_t tmem_base_sh;
   __shared__ __align__(16) float bias_sm[768];   // bias per accumulator column (all chunks)
 
@@ -232,7 +141,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
   // SMEM: [1 KB guard][ngs x G rows][B image]
   uint8_t* ring = smem_raw + 1024;
   uint8_t* bimg = ring + ngs * grp_bytes;
-  // units are (chunk, bin, band), chunk-major, over the bins actually used; they are handed out by
+  // units are (bin, band, chunk), chunk fastest (the chunks of a band re-read its input rows from L2),
+  // over the bins actually used; B images are double-buffered per unit when there are several chunks.
+  // Units are handed out by
   // an atomic counter (the producer) through a small SMEM ring, so CTAs that start late (an SM busy
   // with another stream's kernel) simply take fewer units
   const int nbins = min(*p.num_bins, p.max_bins);
@@ -244,8 +155,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < (int)ngs; ++i) { mbar_init(&in_full[i], 1); mbar_init(&in_empty[i], 1); }
     for (int i = 0; i < S::OGR; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
-    mbar_init(&b_full, 1);
-    mbar_init(&b_empty, 1);
+    for (int i = 0; i < 2; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
     for (int i = 0; i < 4; ++i) { mbar_init(&unit_full[i], 1); mbar_init(&unit_empty[i], 9); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -294,7 +204,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
     // =============================== producer ===============================
     if (lane == 0) {
       uint32_t ig = 0;          // input groups loaded (ring sequence)
-      int loaded_chunk = -1;
       uint32_t bload = 0;
       for (uint32_t us = 0;; ++us) {
         int u = atomicAdd(p.counter, 1);
@@ -303,14 +212,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
         unit_ring[us & 3] = u;
         mbar_arrive(&unit_full[us & 3]);
         if (u < 0) break;
-        const int chunk = u / per_chunk, v = u - chunk * per_chunk;
+        const int v = u / p.nchunk, chunk = u - v * p.nchunk;
         const int bin = v / p.nbands, y0 = (v - bin * p.nbands) * BR;
-        if (chunk != loaded_chunk) {
-          if (bload > 0) mbar_wait(&b_empty, (bload - 1) & 1);
-          mbar_expect_tx(&b_full, p.b_bytes);
-          bulk_g2s(bimg, p.wimg + (size_t)chunk * p.b_bytes, p.b_bytes, &b_full);
+        if (p.nchunk > 1 || bload == 0) {
+          const uint32_t bs = bload & 1;
+          mbar_wait(&b_empty[bs], ((bload >> 1) & 1) ^ 1);
+          mbar_expect_tx(&b_full[bs], p.b_bytes);
+          bulk_g2s(bimg + bs * p.b_bytes, p.wimg + (size_t)chunk * p.b_bytes, p.b_bytes, &b_full[bs]);
           ++bload;
-          loaded_chunk = chunk;
         }
         const int y1 = min(p.Hr, y0 + BR);
         const int rlo = max(y0 - 1, 0), rhi = min(y1, p.Hr - 1);   // input rows this unit reads
@@ -339,8 +248,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
     // =============================== MMA issuer ===============================
     if (elect_one()) {
       uint32_t ig = 0, og = 0, bwait = 0;
-      int cur_chunk = -1;
-      const uint32_t ring16 = smem_u32(ring) >> 4, b16 = smem_u32(bimg) >> 4;
+      uint32_t b16 = smem_u32(bimg) >> 4, bs = 0;
+      const uint32_t ring16 = smem_u32(ring) >> 4;
       const uint32_t row16 = row_bytes >> 4, grp16 = grp_bytes >> 4;
       const uint32_t plane16 = (uint32_t)p.Wr;              // A plane stride (16-B units)
       constexpr uint32_t BLBO = (uint32_t)S::N;              // B chunk-plane stride (16-B units)
@@ -349,13 +258,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
         const int u = *(volatile int*)&unit_ring[us & 3];
         mbar_arrive(&unit_empty[us & 3]);
         if (u < 0) break;
-        const int chunk = u / per_chunk, v = u - chunk * per_chunk;
+        const int v = u / p.nchunk, chunk = u - v * p.nchunk;
         const int bin = v / p.nbands, y0 = (v - bin * p.nbands) * BR;
-        if (chunk != cur_chunk) {
-          if (cur_chunk >= 0) mma_commit(&b_empty);         // previous B image no longer needed
-          mbar_wait(&b_full, bwait & 1);
+        if (p.nchunk > 1 || bwait == 0) {
+          bs = bwait & 1;
+          mbar_wait(&b_full[bs], (bwait >> 1) & 1);
           ++bwait;
-          cur_chunk = chunk;
+          b16 = (smem_u32(bimg) + bs * p.b_bytes) >> 4;
         }
         const int rlo = max(y0 - 1, 0), rhi = min(min(y0 + BR, p.Hr), p.Hr - 1);
 #pragma unroll
@@ -413,6 +322,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
           // last row): after input group c + 1 (G >= 2) or c + 2 (G == 1)
           if (k >= S::DONE_LAG && k - S::DONE_LAG < S::NG_OUT) mma_commit(&acc_full[(og + k - S::DONE_LAG) % S::OGR]);
         }
+        if (p.nchunk > 1) mma_commit(&b_empty[bs]);   // this unit's B image can be overwritten
         ig += S::NG_IN;
         og += S::NG_OUT;
       }
@@ -436,7 +346,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
       __syncwarp();
       if (lane == 0) mbar_arrive(&unit_empty[us & 3]);
       if (u < 0) break;
-      const int chunk = u / per_chunk, v = u - chunk * per_chunk;
+      const int v = u / p.nchunk, chunk = u - v * p.nchunk;
       const int bin = v / p.nbands, y0 = (v - bin * p.nbands) * BR;
       const int nrows = min(BR, p.Hr - y0);
       for (int k = 0; k < S::NG_OUT; ++k) {
@@ -840,11 +750,12 @@ regen_status conv_tc_launch(const SRNet* net, const ConvDesc& cv, const void* in
   const int cin8 = cv.cin == 3 ? 1 : cv.cin / 8;
   const uint32_t grp_bytes = (uint32_t)cin8 * p.Wr * 16 * pl->G;
   // deepest input ring that fits (row loads are latency-bound: more rows in flight per SM)
+  const size_t bbytes_all = (size_t)pl->b_bytes * (pl->nchunk > 1 ? 2 : 1);
   int gslog = 3;
-  while (gslog > 0 && 1024 + ((size_t)1 << gslog) * grp_bytes + pl->b_bytes > 220 * 1024) --gslog;
+  while (gslog > 0 && 1024 + ((size_t)1 << gslog) * grp_bytes + bbytes_all > 220 * 1024) --gslog;
   p.ngs = 1 << gslog;
   p.gslog = gslog;
-  const size_t smem = 1024 + (size_t)p.ngs * grp_bytes + pl->b_bytes;
+  const size_t smem = 1024 + (size_t)p.ngs * grp_bytes + bbytes_all;
   REGEN_REQUIRE(smem <= 227 * 1024, "conv SMEM %zu too large", smem);
   KernFn kern = lookup(cv.role, net->cfg.channels, pl->cp, pl->R, pl->G, pl->T, cv.ps);
   REGEN_REQUIRE(kern != nullptr, "no tcgen05 kernel instance");

@@ -133,6 +133,7 @@ extern "C" regen_status regen_sr_destroy(void* handle) {
   cudaFree(net->d_w32);
   cudaFree(net->d_wtc);
   conv_tc_release(net);
+  resblock_tc_release(net);
   delete net;
   return REGEN_OK;
 }
@@ -448,19 +449,31 @@ extern "C" regen_status regen_enhance_packed(void* sr, const regen_geom* geom, c
   size_t i = 0;
   st = run_conv(net, cv[i++], e.x0, e.a0, nullptr, e, *p, d_num_bins, s);            // head -> h
   const void* r = e.a0;
-  for (int k = 0; k < net->cfg.n_resblocks && st == REGEN_OK; ++k) {
-    st = run_conv(net, cv[i++], r, e.a2, nullptr, e, *p, d_num_bins, s);             // t = relu(conv(r))
-    if (st != REGEN_OK) break;
-    st = run_conv(net, cv[i++], e.a2, e.a1, r, e, *p, d_num_bins, s);                // r' = r + s*conv(t)
-    r = e.a1;
+  void* body_out = e.a2;
+  if (resblock_tc_supported(net, p->bin_w)) {
+    // fused residual blocks (t stays in SMEM), ping-pong a1 <-> a2
+    for (int k = 0; k < net->cfg.n_resblocks && st == REGEN_OK; ++k) {
+      void* o = (k & 1) ? e.a2 : e.a1;
+      st = resblock_tc_launch(net, k, r, o, e.mbits, p->max_bins, d_num_bins, p->bin_w, p->bin_h, e.counters + 32 + k, s);
+      r = o;
+      i += 2;
+    }
+    body_out = (r == e.a1) ? e.a2 : e.a1;
+  } else {
+    for (int k = 0; k < net->cfg.n_resblocks && st == REGEN_OK; ++k) {
+      st = run_conv(net, cv[i++], r, e.a2, nullptr, e, *p, d_num_bins, s);             // t = relu(conv(r))
+      if (st != REGEN_OK) break;
+      st = run_conv(net, cv[i++], e.a2, e.a1, r, e, *p, d_num_bins, s);                // r' = r + s*conv(t)
+      r = e.a1;
+    }
   }
-  if (st == REGEN_OK) st = run_conv(net, cv[i++], r, e.a2, e.a0, e, *p, d_num_bins, s);  // body + h
+  if (st == REGEN_OK) st = run_conv(net, cv[i++], r, body_out, e.a0, e, *p, d_num_bins, s);  // body + h
   if (st != REGEN_OK) return st;
   if (net->cfg.scale == 4) {
-    st = run_conv(net, cv[i++], e.a2, e.u1, nullptr, e, *p, d_num_bins, s);
+    st = run_conv(net, cv[i++], body_out, e.u1, nullptr, e, *p, d_num_bins, s);
     if (st == REGEN_OK) st = run_conv(net, cv[i++], e.u1, e.u, nullptr, e, *p, d_num_bins, s);
   } else {
-    st = run_conv(net, cv[i++], e.a2, e.u, nullptr, e, *p, d_num_bins, s);
+    st = run_conv(net, cv[i++], body_out, e.u, nullptr, e, *p, d_num_bins, s);
   }
   if (st == REGEN_OK) st = run_conv(net, cv[i++], e.u, d_hr_bins, nullptr, e, *p, d_num_bins, s);  // tail
   return st;

@@ -44,6 +44,7 @@ struct SRNet {
   void* tc_plans = nullptr;   // tc::NetPlans (conv_tc.cu)
   std::vector<float> tc_weights;   // host copy of the (rounded) weights for B-image packing
   int tc_bin_w = -1;             // bin width the B images were planned for
+  void* rb_images = nullptr;     // fused-resblock B images (resblock_tc.cu)
 };
 
 // enhance workspace layout
@@ -69,6 +70,11 @@ regen_status conv_simt_launch(const SRNet* net, const ConvDesc& cv, const void* 
 bool conv_tc_supported(const SRNet* net, const ConvDesc& cv, int bin_w);
 regen_status conv_tc_prepare(SRNet* net);
 void conv_tc_release(SRNet* net);
+bool resblock_tc_supported(const SRNet* net, int bin_w);
+void resblock_tc_release(SRNet* net);
+regen_status resblock_tc_launch(const SRNet* net, int block, const void* in, void* out, const uint32_t* mbits,
+                                int max_bins, const int32_t* d_num_bins, int bin_w, int bin_h, int* counter,
+                                cudaStream_t s);
 regen_status conv_tc_launch(const SRNet* net, const ConvDesc& cv, const void* in, void* out, const void* skip,
                             const uint32_t* mbits, int max_bins, const int32_t* d_num_bins, int bin_w, int bin_h,
                             int* counter, cudaStream_t s);

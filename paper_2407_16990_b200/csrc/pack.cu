@@ -335,8 +335,8 @@ __global__ void __launch_bounds__(32, 1) pack_kernel(PackArgs a) {
         --hw;
         if (lane == 0 && free_slot != hw) { key[free_slot] = key[hw]; rect[free_slot] = rect[hw]; }
       }
-      __syncwarp();
     }
+    __syncwarp();   // lane 0's pool writes are visible to every lane before the next scan
     c_upd += clock64() - t2;
   }
   if (a.prof && lane == 0)

@@ -1,0 +1,538 @@
+// Fused EDSR residual block on tcgen05 (sm_100a): r' = mask * (r + res_scale * conv_b(relu(conv_a(r))))
+// with the intermediate t = mask * relu(conv_a(r)) kept in SMEM (reading D8/D11 of DESIGN.md).
+//
+// Both convs use the sliding-window mapping of conv_tc.cu (kernel rows folded into N = 3*C, one MMA
+// per (dx, K-chunk pair) per input row, output-row accumulators in a TMEM ring at decreasing
+// columns). A work unit is a band of BR = 32 output rows of one bin:
+//   conv_a reads r rows y0-2 .. y1+1 (36 rows, bulk-copied in groups of G) and produces t rows
+//   y0-1 .. y1 (34 rows) into TMEM ring A; epilogue quad A (warps 2-5) applies bias/ReLU/mask and
+//   writes each t row into an SMEM ring in the UMMA operand layout (generic-proxy stores + proxy fence);
+//   conv_b consumes those t rows from SMEM into TMEM ring B; epilogue quad B (warps 6-9) adds the
+//   residual (r, prefetched from HBM/L2) and stores r'.
+// One thread (warp 1) issues both convs' MMAs, interleaving conv_b group k with conv_a group k+LAG.
+// Synchronisation is per group of G rows: r ring (in_full/in_empty), TMEM ring A and B
+// (acc*_full/acc*_empty), t ring (t_full by quad A, t_empty by tcgen05.commit). TMEM columns are
+// computed at run time from the per-CTA row sequence (no branches in the MMA stream).
+// HBM traffic per block: read r (+ its L2-hot re-read as the residual) and write r' once, instead
+// of r, t, t, r, r' for two separate convs.
+#include <stdlib.h>
+
+#include <vector>
+
+#include "tc_common.cuh"
+
+namespace regen {
+namespace tc {
+
+namespace rb {
+
+constexpr int NTHREADS = 320;
+constexpr int BR = 32;        // output rows per unit
+constexpr int NA_OUT = BR + 2;   // t rows per unit
+constexpr int NA_IN = BR + 4;    // r rows per unit
+constexpr int NSLOT = 4;      // r-ring and t-ring groups (power of two)
+constexpr int LAG = 3;        // conv_b group k is issued after conv_a group k + LAG
+
+struct Params {
+  const __nv_bfloat16* in;    // r
+  __nv_bfloat16* out;         // r'
+  const float* bias_a;
+  const float* bias_b;
+  const uint32_t* mbits;
+  const int32_t* num_bins;
+  const uint8_t* wimg;        // [B image conv_a][B image conv_b]
+  uint32_t b_bytes;           // bytes of one image
+  int Hr, bin_w, bin_h, max_bins, nbands;
+  float res_scale;
+  int* counter;
+  unsigned long long* prof;   // REGEN_TC_PROF=1: wait-time counters
+};
+
+template <int C, int R, int G>
+struct RShape {
+  static constexpr int KC = C / 16, NS = 3 * KC, N = 3 * C;
+  static constexpr int NGA_IN = (NA_IN + G - 1) / G;
+  static constexpr int NGA_OUT = (NA_OUT + G - 1) / G;   // = t groups = conv_b input groups
+
+  static constexpr int NGB_OUT = BR / G;
+  static constexpr int OGR = R / G;
+  static constexpr int COLB = R * C;                     // TMEM column of ring B
+  static_assert(2 * R * C <= 512 && R % G == 0 && OGR >= 3 && BR % G == 0 && OGR <= 8, "shape");
+  // input group whose processing completes accumulator group k of a conv with NOUT real rows
+  __host__ __device__ static constexpr int done_group(int k, int nout) {
+    return ((G * k + G - 1 < nout ? G * k + G - 1 : nout - 1) + 2) / G;
+  }
+};
+
+__device__ __forceinline__ uint32_t ring_slot(uint32_t seq, uint32_t Rm) { return (0u - seq) & Rm; }
+
+// Issue the sliding-window MMAs of one input row: `i` = unit-local input row, `nout` = number of real
+// output rows, `seq0` = accumulator sequence of the unit's output row 0, `tmem` = TMEM column of the
+// ring, `a_row16` = the row's SMEM address (16-B units), `b16` = B image base (16-B units).
+template <int C, int R, int G>
+__device__ __forceinline__ void issue_row(int i, int nout, uint32_t seq0, uint32_t tmem, uint32_t a_row16,
+                                         uint32_t b16, uint32_t en) {
+  using S = RShape<C, R, G>;
+  constexpr uint32_t Rm = R - 1;
+  constexpr uint32_t BLBO = (uint32_t)S::N;
+  const int gA = i < nout ? 0 : (i - 1 < nout ? 1 : 2);
+  const int gB = i >= 2 ? 3 : (i >= 1 ? 2 : 1);
+  if (gA >= gB) return;   // compile-time after unrolling
+  const uint32_t ng = (uint32_t)(gB - gA);
+  const uint32_t s0 = ring_slot(seq0 + (uint32_t)(i - gA), Rm);
+  const uint32_t len1 = min(ng, (uint32_t)R - s0);
+  const uint32_t two = (len1 < ng && en) ? 1u : 0u;
+  const uint32_t idesc1 = make_idesc((int)(len1 * C)), idesc2 = make_idesc((int)((ng - len1) * C));
+  const uint32_t d1 = tmem + s0 * (uint32_t)C;
+#pragma unroll
+  for (int st = 0; st < S::NS; ++st) {
+    const int dx = st / S::KC - 1, plane = 2 * (st % S::KC);
+    const uint32_t a_lo = (a_row16 + (uint32_t)(plane * 128) + (uint32_t)dx) + (128u << 16);   // LBO = plane
+    const uint32_t b_lo = (b16 + (uint32_t)(st * S::N * 2) + (uint32_t)(gA * C)) + (BLBO << 16);
+    mma_bf16(d1, a_lo, b_lo, idesc1, en);
+    mma_bf16(tmem, a_lo, b_lo + len1 * (uint32_t)C, idesc2, two);
+  }
+}
+
+template <int C, int R, int G>
+__global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_constant__ Params p) {
+  using S = RShape<C, R, G>;
+  constexpr int ROW_BYTES = (C / 8) * 128 * 16;
+  constexpr int GRP = G * ROW_BYTES;
+  constexpr uint32_t Rm = R - 1;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t in_full[NSLOT], in_empty[NSLOT], t_full[NSLOT], t_empty[NSLOT];
+  __shared__ __align__(8) uint64_t a_full[8], a_empty[8], b_fullacc[8], b_emptyacc[8];
+  __shared__ __align__(8) uint64_t w_full;
+  __shared__ __align__(8) uint64_t unit_full[4], unit_empty[4];
+  __shared__ int unit_ring[4];
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ __align__(16) float bias_sm[2][64];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* rring = smem_raw + 1024;
+  uint8_t* tring = rring + NSLOT * GRP;
+  uint8_t* wimg = tring + NSLOT * GRP;
+  const int nbins = min(*p.num_bins, p.max_bins);
+  const int total_units = nbins * p.nbands;
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < NSLOT; ++i) {
+      mbar_init(&in_full[i], 1); mbar_init(&in_empty[i], 1);
+      mbar_init(&t_full[i], 4); mbar_init(&t_empty[i], 1);
+    }
+    for (int i = 0; i < S::OGR; ++i) {
+      mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 4);
+      mbar_init(&b_fullacc[i], 1); mbar_init(&b_emptyacc[i], 4);
+    }
+    mbar_init(&w_full, 1);
+    for (int i = 0; i < 4; ++i) { mbar_init(&unit_full[i], 1); mbar_init(&unit_empty[i], 9); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base_sh)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int n = threadIdx.x; n < 64; n += NTHREADS) {
+    bias_sm[0][n] = n < C ? __ldg(p.bias_a + n) : 0.f;
+    bias_sm[1][n] = n < C ? __ldg(p.bias_b + n) : 0.f;
+  }
+  // zero the t ring (rows read at the left/right halo of masked pixels must be finite)
+  for (int i = threadIdx.x; i < NSLOT * GRP / 16; i += NTHREADS) reinterpret_cast<uint4*>(tring)[i] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  // arm both accumulator rings with their biases
+  if (warp >= 2) {
+    const int quad = (warp - 2) >> 2, q4 = warp & 3;
+    for (int s = 0; s < R; ++s)
+#pragma unroll
+      for (int c0 = 0; c0 < C; c0 += 16)
+        tmem_st16(tmem + ((uint32_t)(32 * q4) << 16) + (uint32_t)(quad * S::COLB + s * C + c0), bias_sm[quad] + c0);
+    tmem_st_wait();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  long long w_ae = 0, w_if = 0, w_be = 0, w_tf = 0, w_ea = 0, w_te = 0, w_eb = 0;
+  const long long pstart = clock64();
+
+  if (warp == 0) {
+    // =============================== producer ===============================
+    if (lane == 0) {
+      mbar_expect_tx(&w_full, 2 * p.b_bytes);
+      bulk_g2s(wimg, p.wimg, 2 * p.b_bytes, &w_full);
+      uint32_t ig = 0;
+      for (uint32_t us = 0;; ++us) {
+        int u = atomicAdd(p.counter, 1);
+        if (u >= total_units) u = -1;
+        mbar_wait(&unit_empty[us & 3], ((us >> 2) & 1) ^ 1);
+        unit_ring[us & 3] = u;
+        mbar_arrive(&unit_full[us & 3]);
+        if (u < 0) break;
+        const int bin = u / p.nbands, y0 = (u - bin * p.nbands) * BR;
+        const int y1 = min(p.Hr, y0 + BR);
+        const int rlo = max(y0 - 2, 0), rhi = min(y1 + 1, p.Hr - 1);
+        for (int k = 0; k < S::NGA_IN; ++k, ++ig) {
+          const uint32_t slot = ig & (NSLOT - 1);
+          mbar_wait(&in_empty[slot], ((ig / NSLOT) & 1) ^ 1);
+          const int g0 = y0 - 2 + G * k;
+          const int a = max(g0, rlo), b = min(g0 + G - 1, rhi);
+          if (a <= b) {
+            mbar_expect_tx(&in_full[slot], (uint32_t)(b - a + 1) * ROW_BYTES);
+            bulk_g2s(rring + slot * GRP + (uint32_t)(a - g0) * ROW_BYTES,
+                     p.in + ((size_t)bin * p.Hr + a) * (ROW_BYTES / 2), (uint32_t)(b - a + 1) * ROW_BYTES,
+                     &in_full[slot]);
+          } else {
+            mbar_arrive(&in_full[slot]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // =============================== MMA issuer (both convs) ===============================
+    if (elect_one()) {
+      uint32_t ig = 0, tg = 0;      // r-ring groups consumed, t-ring groups consumed
+      uint32_t qa = 0, qb = 0;      // accumulator group sequences (ring A, ring B)
+      const uint32_t r16 = smem_u32(rring) >> 4, t16 = smem_u32(tring) >> 4;
+      const uint32_t ba16 = smem_u32(wimg) >> 4, bb16 = (smem_u32(wimg) + p.b_bytes) >> 4;
+      mbar_wait(&w_full, 0);
+      for (uint32_t us = 0;; ++us) {
+        mbar_wait(&unit_full[us & 3], (us >> 2) & 1);
+        const int u = *(volatile int*)&unit_ring[us & 3];
+        mbar_arrive(&unit_empty[us & 3]);
+        if (u < 0) break;
+        const int bin = u / p.nbands, y0 = (u - bin * p.nbands) * BR;
+        const int y1 = min(p.Hr, y0 + BR);
+        const int rlo = max(y0 - 2, 0), rhi = min(y1 + 1, p.Hr - 1);
+        const uint32_t seqA = qa * G, seqB = qb * G;
+#pragma unroll
+        for (int step = 0; step < S::NGA_IN + LAG; ++step) {
+          if (step < S::NGA_IN) {
+            // ---- conv_a, input group k: r rows y0-2 + G*k ...
+            const int k = step;
+            const uint32_t slot = (ig + k) & (NSLOT - 1);
+            if (k < S::NGA_OUT) { const long long t0_ = clock64(); mbar_wait(&a_empty[(qa + k) % S::OGR], (((qa + k) / S::OGR) & 1) ^ 1); if (p.prof) w_ae += clock64() - t0_; }
+            { const long long t0_ = clock64(); mbar_wait(&in_full[slot], ((ig + k) / NSLOT) & 1); if (p.prof) w_if += clock64() - t0_; }
+            tc_fence_after();
+#pragma unroll
+            for (int ii = 0; ii < G; ++ii) {
+              const int i = G * k + ii;
+              if (i >= NA_IN) continue;
+              const int r = y0 - 2 + i;
+              const uint32_t en = (r >= rlo && r <= rhi) ? 1u : 0u;
+              issue_row<C, R, G>(i, NA_OUT, seqA, tmem, r16 + slot * (GRP / 16) + ii * (ROW_BYTES / 16), ba16, en);
+            }
+            mma_commit(&in_empty[slot]);
+#pragma unroll
+            for (int ka = 0; ka < S::NGA_OUT; ++ka)
+              if (S::done_group(ka, NA_OUT) == k) mma_commit(&a_full[(qa + ka) % S::OGR]);
+            if (k == S::NGA_IN - 1) {   // groups whose completion falls past the last input group
+#pragma unroll
+              for (int ka = 0; ka < S::NGA_OUT; ++ka)
+                if (S::done_group(ka, NA_OUT) > k) mma_commit(&a_full[(qa + ka) % S::OGR]);
+            }
+          }
+          if (step >= LAG && step - LAG < S::NGA_OUT) {
+            // ---- conv_b, input group kb: t rows y0-1 + G*kb ... (SMEM t ring)
+            const int kb = step - LAG;
+            const uint32_t tslot = (tg + kb) & (NSLOT - 1);
+            if (kb < S::NGB_OUT) { const long long t0_ = clock64(); mbar_wait(&b_emptyacc[(qb + kb) % S::OGR], (((qb + kb) / S::OGR) & 1) ^ 1); if (p.prof) w_be += clock64() - t0_; }
+            { const long long t0_ = clock64(); mbar_wait(&t_full[tslot], ((tg + kb) / NSLOT) & 1); if (p.prof) w_tf += clock64() - t0_; }
+            tc_fence_after();
+#pragma unroll
+            for (int ii = 0; ii < G; ++ii) {
+              const int i = G * kb + ii;
+              if (i >= NA_OUT) continue;
+              const int tr = y0 - 1 + i;
+              const uint32_t en = (tr >= 0 && tr < p.Hr) ? 1u : 0u;
+              issue_row<C, R, G>(i, BR, seqB, tmem + S::COLB, t16 + tslot * (GRP / 16) + ii * (ROW_BYTES / 16), bb16,
+                                 en);
+            }
+            mma_commit(&t_empty[tslot]);
+#pragma unroll
+            for (int jb = 0; jb < S::NGB_OUT; ++jb)
+              if (S::done_group(jb, BR) == kb) mma_commit(&b_fullacc[(qb + jb) % S::OGR]);
+            if (kb == S::NGA_OUT - 1) {
+#pragma unroll
+              for (int jb = 0; jb < S::NGB_OUT; ++jb)
+                if (S::done_group(jb, BR) > kb) mma_commit(&b_fullacc[(qb + jb) % S::OGR]);
+            }
+          }
+        }
+        ig += S::NGA_IN;
+        tg += S::NGA_OUT;
+        qa += S::NGA_OUT;
+        qb += S::NGB_OUT;
+      }
+    }
+    __syncwarp();
+  } else {
+    // =============================== epilogues ===============================
+    const int quad = (warp - 2) >> 2;        // 0: t = relu(conv_a) -> SMEM; 1: r' = r + s*conv_b -> HBM
+    const int q4 = warp & 3;
+    const int m = 32 * q4 + lane;
+    const uint32_t lane_off = (uint32_t)(32 * q4) << 16;
+    const int words = p.bin_w / 32;
+    const size_t bin_px = (size_t)p.Hr * 128;
+    constexpr size_t PSTRIDE = 128 * 8;      // elements between planes of one row
+    uint32_t tg = 0, qa = 0, qb = 0;
+    for (uint32_t us = 0;; ++us) {
+      mbar_wait(&unit_full[us & 3], (us >> 2) & 1);
+      const int u = *(volatile int*)&unit_ring[us & 3];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&unit_empty[us & 3]);
+      if (u < 0) break;
+      const int bin = u / p.nbands, y0 = (u - bin * p.nbands) * BR;
+      const int nrows = min(BR, p.Hr - y0);
+      if (quad == 0) {
+        // ---- t rows y0-1 .. y0+32 into the SMEM t ring
+        const uint32_t seqA = qa * G;
+        for (int ka = 0; ka < S::NGA_OUT; ++ka) {
+          uint32_t occw[G];
+#pragma unroll
+          for (int jj = 0; jj < G; ++jj) {
+            const int tr = min(max(y0 - 1 + G * ka + jj, 0), p.Hr - 1);
+            occw[jj] = __ldg(p.mbits + ((size_t)bin * p.bin_h + tr) * words + m / 32);
+          }
+          const uint32_t tslot = (tg + ka) & (NSLOT - 1);
+          { const long long t0_ = clock64(); mbar_wait(&a_full[(qa + ka) % S::OGR], ((qa + ka) / S::OGR) & 1); if (p.prof) w_ea += clock64() - t0_; }
+          { const long long t0_ = clock64(); mbar_wait(&t_empty[tslot], (((tg + ka) / NSLOT) & 1) ^ 1); if (p.prof) w_te += clock64() - t0_; }
+          tc_fence_after();
+          uint8_t* trow0 = tring + tslot * GRP;
+#pragma unroll
+          for (int jj = 0; jj < G; ++jj) {
+            const int ja = G * ka + jj;
+            const uint32_t taddr = tmem + lane_off + ring_slot(seqA + (uint32_t)ja, Rm) * (uint32_t)C;
+            if (ja < NA_OUT) {
+              const bool occ = (occw[jj] >> (m & 31)) & 1u;
+              uint32_t r[C];
+#pragma unroll
+              for (int c = 0; c < C; c += 16) tmem_ld16(taddr + (uint32_t)c, r + c);
+              tmem_ld_wait();
+#pragma unroll
+              for (int g = 0; g < C / 8; ++g) {
+                float v[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[e] = fmaxf(__uint_as_float(r[8 * g + e]), 0.f);
+                *reinterpret_cast<uint4*>(trow0 + jj * ROW_BYTES + g * 2048 + m * 16) = pack8(v, occ);
+              }
+            }
+#pragma unroll
+            for (int c = 0; c < C; c += 16) tmem_st16(taddr + (uint32_t)c, bias_sm[0] + c);
+          }
+          tmem_st_wait();
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // t rows -> tensor-core reads
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&t_full[tslot]);
+            mbar_arrive(&a_empty[(qa + ka) % S::OGR]);
+          }
+        }
+      } else {
+        // ---- r' rows y0 .. y0+31 = r + res_scale * conv_b, masked, to HBM
+        const uint32_t seqB = qb * G;
+        for (int jb = 0; jb < S::NGB_OUT; ++jb) {
+          uint32_t occw[G];
+          uint4 sk[G][C / 8];
+#pragma unroll
+          for (int jj = 0; jj < G; ++jj) {
+            const int y = min(y0 + G * jb + jj, p.Hr - 1);
+            occw[jj] = __ldg(p.mbits + ((size_t)bin * p.bin_h + y) * words + m / 32);
+            const size_t act = (size_t)bin * bin_px * C + (size_t)y * (C / 8) * PSTRIDE + (size_t)m * 8;
+#pragma unroll
+            for (int g = 0; g < C / 8; ++g) sk[jj][g] = *reinterpret_cast<const uint4*>(p.in + act + g * PSTRIDE);
+          }
+          { const long long t0_ = clock64(); mbar_wait(&b_fullacc[(qb + jb) % S::OGR], ((qb + jb) / S::OGR) & 1); if (p.prof) w_eb += clock64() - t0_; }
+          tc_fence_after();
+#pragma unroll
+          for (int jj = 0; jj < G; ++jj) {
+            const int j = G * jb + jj;
+            const uint32_t taddr = tmem + lane_off + (uint32_t)S::COLB + ring_slot(seqB + (uint32_t)j, Rm) * (uint32_t)C;
+            if (j < nrows) {
+              const int y = y0 + j;
+              const bool occ = (occw[jj] >> (m & 31)) & 1u;
+              uint32_t r[C];
+#pragma unroll
+              for (int c = 0; c < C; c += 16) tmem_ld16(taddr + (uint32_t)c, r + c);
+              tmem_ld_wait();
+              __nv_bfloat16* o = p.out + (size_t)bin * bin_px * C + (size_t)y * (C / 8) * PSTRIDE + (size_t)m * 8;
+#pragma unroll
+              for (int g = 0; g < C / 8; ++g) {
+                float v[8];
+                const __nv_bfloat162* s2 = reinterpret_cast<const __nv_bfloat162*>(&sk[jj][g]);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 f = __bfloat1622float2(s2[e]);
+                  v[2 * e] = fmaf(p.res_scale, __uint_as_float(r[8 * g + 2 * e]), f.x);
+                  v[2 * e + 1] = fmaf(p.res_scale, __uint_as_float(r[8 * g + 2 * e + 1]), f.y);
+                }
+                *reinterpret_cast<uint4*>(o + g * PSTRIDE) = pack8(v, occ);
+              }
+            }
+#pragma unroll
+            for (int c = 0; c < C; c += 16) tmem_st16(taddr + (uint32_t)c, bias_sm[1] + c);
+          }
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&b_emptyacc[(qb + jb) % S::OGR]);
+        }
+      }
+      tg += S::NGA_OUT;
+      qa += S::NGA_OUT;
+      qb += S::NGB_OUT;
+    }
+  }
+  if (p.prof && lane == 0) {
+    const long long tot = clock64() - pstart;
+    if (warp == 1) {
+      atomicAdd(p.prof + 0, (unsigned long long)tot); atomicAdd(p.prof + 1, (unsigned long long)w_ae);
+      atomicAdd(p.prof + 2, (unsigned long long)w_if); atomicAdd(p.prof + 3, (unsigned long long)w_be);
+      atomicAdd(p.prof + 4, (unsigned long long)w_tf);
+    }
+    if (warp >= 2 && warp < 6) { atomicAdd(p.prof + 5, (unsigned long long)w_ea); atomicAdd(p.prof + 6, (unsigned long long)w_te); }
+    if (warp >= 6) atomicAdd(p.prof + 7, (unsigned long long)w_eb);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+}  // namespace rb
+}  // namespace tc
+
+// ---------------------------------------------------------------------------------- host side
+
+static uint16_t rb_bf16_bits(float f) {
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+
+// sliding-window B image of a C->C conv: per step st (dx-major, K-chunk pair), a block
+// [2 K-chunks][3*C rows][8] bf16; row g*C + co = kernel row g, output channel co.
+static void rb_pack(const std::vector<float>& w32, const ConvDesc& d, int C, std::vector<uint16_t>& img) {
+  const int KC = C / 16, NS = 3 * KC, N = 3 * C;
+  const size_t off = img.size();
+  img.resize(off + (size_t)NS * N * 16, 0);
+  for (int st = 0; st < NS; ++st)
+    for (int g = 0; g < 3; ++g)
+      for (int co = 0; co < C; ++co)
+        for (int k = 0; k < 16; ++k) {
+          const int dx = st / KC - 1, ci = 16 * (st % KC) + k;
+          const float v = w32[d.w_off + ((size_t)co * d.cin8 * 8 + ci) * 9 + g * 3 + (dx + 1)];
+          img[off + (size_t)st * N * 16 + (size_t)(k / 8) * N * 8 + (size_t)(g * C + co) * 8 + (k % 8)] = rb_bf16_bits(v);
+        }
+}
+
+bool resblock_tc_supported(const SRNet* net, int bin_w) {
+  const char* e = getenv("REGEN_NO_FUSED_RESBLOCK");
+  if (e && e[0] == '1') return false;
+  return net->use_tc && bin_w == 128 && (net->cfg.channels == 32 || net->cfg.channels == 16) &&
+         net->cfg.n_resblocks > 0 && !net->tc_weights.empty();
+}
+
+struct RbImages {
+  std::vector<size_t> off;   // byte offset of each resblock's [conv_a | conv_b] image pair
+  uint32_t b_bytes = 0;
+  uint8_t* d = nullptr;
+};
+
+static RbImages* rb_images(SRNet* net) {
+  if (net->rb_images) return (RbImages*)net->rb_images;
+  auto* im = new RbImages();
+  const int C = net->cfg.channels;
+  std::vector<uint16_t> all;
+  for (int b = 0; b < net->cfg.n_resblocks; ++b) {
+    const ConvDesc& ca = net->convs[1 + 2 * b];
+    const ConvDesc& cb = net->convs[2 + 2 * b];
+    im->off.push_back(all.size() * 2);
+    rb_pack(net->tc_weights, ca, C, all);
+    rb_pack(net->tc_weights, cb, C, all);
+  }
+  im->b_bytes = (uint32_t)((size_t)3 * (C / 16) * 3 * C * 16 * 2);
+  if (cudaMalloc(&im->d, all.size() * 2) != cudaSuccess ||
+      cudaMemcpy(im->d, all.data(), all.size() * 2, cudaMemcpyHostToDevice) != cudaSuccess) {
+    delete im;
+    return nullptr;
+  }
+  net->rb_images = im;
+  return im;
+}
+
+void resblock_tc_release(SRNet* net) {
+  if (!net->rb_images) return;
+  auto* im = (RbImages*)net->rb_images;
+  cudaFree(im->d);
+  delete im;
+  net->rb_images = nullptr;
+}
+
+regen_status resblock_tc_launch(const SRNet* cnet, int block, const void* in, void* out, const uint32_t* mbits,
+                                int max_bins, const int32_t* d_num_bins, int bin_w, int bin_h, int* counter,
+                                cudaStream_t s) {
+  using namespace tc::rb;
+  SRNet* net = const_cast<SRNet*>(cnet);
+  RbImages* im = rb_images(net);
+  REGEN_REQUIRE(im != nullptr, "resblock B images");
+  const int C = net->cfg.channels;
+  Params p;
+  memset(&p, 0, sizeof(p));
+  p.in = (const __nv_bfloat16*)in;
+  p.out = (__nv_bfloat16*)out;
+  p.bias_a = net->d_w32 + net->convs[1 + 2 * block].b_off;
+  p.bias_b = net->d_w32 + net->convs[2 + 2 * block].b_off;
+  p.mbits = mbits;
+  p.num_bins = d_num_bins;
+  p.wimg = im->d + im->off[block];
+  p.b_bytes = im->b_bytes;
+  p.Hr = bin_h;
+  p.bin_w = bin_w;
+  p.bin_h = bin_h;
+  p.max_bins = max_bins;
+  p.nbands = (bin_h + BR - 1) / BR;
+  p.res_scale = net->cfg.res_scale;
+  p.counter = counter;
+  void (*kern)(Params) = nullptr;
+  int G = 0;
+  if (C == 32) { kern = resblock_tc_kernel<32, 8, 2>; G = 2; }
+  if (C == 16) { kern = resblock_tc_kernel<16, 16, 4>; G = 4; }
+  REGEN_REQUIRE(kern != nullptr, "fused resblock: unsupported C=%d", C);
+  const size_t smem = 1024 + 2ull * NSLOT * G * (C / 8) * 128 * 16 + 2ull * p.b_bytes;
+  REGEN_REQUIRE(smem <= 227 * 1024, "fused resblock SMEM %zu", smem);
+  REGEN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  static int nsm = 0;
+  if (nsm == 0) {
+    int dev;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int grid = std::min(max_bins * p.nbands, nsm);
+  static unsigned long long* d_prof = nullptr;
+  const char* pe = getenv("REGEN_TC_PROF");
+  const bool prof = pe && pe[0] == '1';
+  if (prof) {
+    if (!d_prof) cudaMalloc(&d_prof, 8 * sizeof(unsigned long long));
+    cudaMemsetAsync(d_prof, 0, 8 * sizeof(unsigned long long), s);
+    p.prof = d_prof;
+  }
+  kern<<<grid, NTHREADS, smem, s>>>(p);
+  REGEN_LAUNCH_CHECK();
+  if (prof) {
+    unsigned long long h[8];
+    cudaMemcpyAsync(h, d_prof, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    const double g = grid;
+    fprintf(stderr, "[rb-prof] mma total %.0f | waits a_empty %.0f in_full %.0f b_empty %.0f t_full %.0f | epiA a_full %.0f "
+            "t_empty %.0f | epiB b_full %.0f (cycles/CTA)\n", h[0] / g, h[1] / g, h[2] / g, h[3] / g, h[4] / g,
+            h[5] / (4 * g), h[6] / (4 * g), h[7] / (4 * g));
+  }
+  return REGEN_OK;
+}
+
+}  // namespace regen
