@@ -194,6 +194,11 @@ REGEN_API regen_status regen_scatter_blend(const regen_geom* geom, const regen_p
 REGEN_API regen_status regen_workspace_size(int32_t which, const regen_geom* geom, const void* params, const void* sr,
                                   size_t* bytes);
 
+/* Number of kernels one regen_enhance_packed call launches for this SR handle and bin geometry
+ * (paint + gather + one per conv launch + the fold combine; memsets excluded). Host-only, no device
+ * work; lets benchmarks count launches without a profiler. Returns REGEN_E_INVALID on null args. */
+REGEN_API regen_status regen_enhance_kernel_count(const void* sr, const regen_pack_params* params, int32_t* count);
+
 /* Helpers. */
 REGEN_API int64_t regen_capacity_mbs(int32_t bin_w, int32_t bin_h, int32_t n_bins, int32_t mb);  /* floor(H*W*B/mb^2) */
 REGEN_API const char* regen_status_string(regen_status s);

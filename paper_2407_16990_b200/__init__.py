@@ -26,7 +26,7 @@ ST_REGION_OVERFLOW, ST_BOX_OVERFLOW, ST_FREELIST_OVERFLOW = 1, 2, 4
 
 EXPORTED = ["regen_select_mbs", "regen_pack_regions", "regen_sr_create", "regen_sr_destroy", "regen_stitch_bins",
             "regen_enhance_packed", "regen_scatter_blend", "regen_workspace_size", "regen_capacity_mbs",
-            "regen_status_string", "regen_last_error", "regen_abi_version"]
+            "regen_status_string", "regen_last_error", "regen_abi_version", "regen_enhance_kernel_count"]
 
 
 class Geom(ctypes.Structure):
@@ -79,13 +79,15 @@ def _load():
     lib.regen_enhance_packed.argtypes = [vp, P(Geom), P(PackParams), vp, vp, i64, vp, vp, vp, vp, vp, sz, vp]
     lib.regen_scatter_blend.argtypes = [P(Geom), P(PackParams), i32, vp, vp, vp, vp, i32, vp, i32, vp]
     lib.regen_workspace_size.argtypes = [i32, P(Geom), vp, vp, P(sz)]
+    lib.regen_enhance_kernel_count.argtypes = [vp, P(PackParams), P(i32)]
     lib.regen_capacity_mbs.argtypes = [i32, i32, i32, i32]
     lib.regen_capacity_mbs.restype = i64
     lib.regen_status_string.restype = ctypes.c_char_p
     lib.regen_last_error.restype = ctypes.c_char_p
     lib.regen_abi_version.restype = i32
     for name in ["regen_select_mbs", "regen_pack_regions", "regen_sr_create", "regen_sr_destroy",
-                 "regen_stitch_bins", "regen_enhance_packed", "regen_scatter_blend", "regen_workspace_size"]:
+                 "regen_stitch_bins", "regen_enhance_packed", "regen_scatter_blend", "regen_workspace_size",
+                 "regen_enhance_kernel_count"]:
         getattr(lib, name).restype = ctypes.c_int
     return lib
 
@@ -255,18 +257,16 @@ class Pipeline:
         self.enhance(frames, stream)
         return self.scatter(frames, out, stream)
 
-    def n_convs(self) -> int:
-        """Conv kernel launches per enhance call (a fused residual block is one launch)."""
-        c = self.sr.cfg
-        if c.n_resblocks == 0:
-            return 2
-        fused = (c.dtype == DTYPE_BF16 and c.channels in (16, 32) and self.pack.bin_w == 128
-                 and os.environ.get("REGEN_NO_FUSED_RESBLOCK", "0") != "1")
-        return 1 + (1 if fused else 2) * c.n_resblocks + 1 + (2 if c.scale == 4 else 1) + 1
+    def enhance_kernels(self) -> int:
+        """Kernels one enhance call launches (regen_enhance_kernel_count)."""
+        n = ctypes.c_int32(0)
+        _check(lib.regen_enhance_kernel_count(self.sr.handle, ctypes.byref(self.pack), ctypes.byref(n)),
+               "regen_enhance_kernel_count")
+        return int(n.value)
 
     def launches_per_step(self) -> int:
-        """Kernels libregen launches per run(): select 4, pack 7, enhance 2 + one per conv, scatter 1."""
-        return 4 + 7 + 2 + self.n_convs() + 1
+        """Kernels libregen launches per run(): select 4, pack 7, enhance (counted by the library), scatter 1."""
+        return 4 + 7 + self.enhance_kernels() + 1
 
     # ---- host-side views (sync), for tests and reporting
     def host_results(self) -> dict:

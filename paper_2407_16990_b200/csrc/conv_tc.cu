@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
   // up_column() — each chunk then writes whole HR pixels of CG channels for all sub-columns j.
   for (int n = threadIdx.x; n < 768; n += NTHREADS) {
     float b = 0.f;
-    if (ROLE == ROLE_UP) {
+    if constexpr (ROLE == ROLE_UP) {
       const int co = up_column<C, CP, PS>(n);
       if (co < p.cout) b = __ldg(p.bias + co);
     } else if (n < p.cout) {
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
               const int xl = x / p.res;
               const bool occ = (occw[jj][t] >> (xl & 31)) & 1u;
               const uint32_t taddr = tmem + lane_off + (uint32_t)((t * R + S::slot(j)) * CP);
-              if (ROLE == ROLE_TAIL) {
+              if constexpr (ROLE == ROLE_TAIL) {
                 uint32_t r[16];
                 tmem_ld16(taddr, r);
                 tmem_ld_wait();
@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
                 val.x = pack_bf16x2(occ ? __uint_as_float(r[0]) : 0.f, occ ? __uint_as_float(r[1]) : 0.f);
                 val.y = pack_bf16x2(occ ? __uint_as_float(r[2]) : 0.f, 0.f);
                 *reinterpret_cast<uint2*>(p.out + ((size_t)bin * bin_px + (size_t)y * p.Wr + x) * 4) = val;
-              } else if (ROLE == ROLE_UP) {
+              } else if constexpr (ROLE == ROLE_UP) {
                 // chunk = (sub-row i, channel group g): + bias, PixelShuffle(PS) into [bin][Y][C/8][X][8];
                 // per plane the PS sub-columns of a pixel are adjacent 16-B chunks (full sectors)
                 constexpr int CG = CP / PS, NG = C / CG;
@@ -634,6 +634,18 @@ static KernFn lookup(int role, int C, int CP, int R, int G, int T, int PS) {
   K(ROLE_UP, 64, 48, 8, 2, 1, 3)
   K(ROLE_UP, 64, 64, 8, 2, 1, 2)
   K(ROLE_UP, 64, 64, 4, 1, 2, 2)
+  K(ROLE_FOLD, 16, 80, 4, 1, 1, 1)
+  K(ROLE_FOLD, 16, 48, 8, 2, 1, 1)
+  K(ROLE_FOLD, 16, 48, 4, 1, 2, 1)
+  K(ROLE_FOLD, 32, 80, 4, 1, 1, 1)
+  K(ROLE_FOLD, 32, 48, 8, 2, 1, 1)
+  K(ROLE_FOLD, 32, 48, 4, 1, 2, 1)
+  K(ROLE_FOLD, 48, 80, 4, 1, 1, 1)
+  K(ROLE_FOLD, 48, 48, 8, 2, 1, 1)
+  K(ROLE_FOLD, 48, 48, 4, 1, 2, 1)
+  K(ROLE_FOLD, 64, 80, 4, 1, 1, 1)
+  K(ROLE_FOLD, 64, 48, 8, 2, 1, 1)
+  K(ROLE_FOLD, 64, 48, 4, 1, 2, 1)
 #undef K
   return nullptr;
 }

@@ -8,6 +8,7 @@
 // conv_simt      fp32 direct 3x3 conv (CUDA cores), the FP32 model path (C1) and the reference
 //                path for convs the tcgen05 kernel does not cover; same layout and epilogues.
 #include <math.h>
+#include <stdlib.h>
 
 #include <vector>
 
@@ -107,6 +108,7 @@ extern "C" regen_status regen_sr_create(const regen_sr_config* cfg, const float*
     for (int co = 0; co < d.cout; ++co) w32.push_back(h_weights[src + co]);
     src += d.cout;
   }
+  if (cfg->dtype == REGEN_DTYPE_BF16) fold_prepare(net, w32);   // appends the UP∘TAIL fold conv
   cudaError_t e = cudaMalloc(&net->d_w32, w32.size() * sizeof(float));
   if (e == cudaSuccess) e = cudaMemcpy(net->d_w32, w32.data(), w32.size() * sizeof(float), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
@@ -337,7 +339,7 @@ EnhanceBufs enhance_bufs(const SRNet* net, const regen_pack_params& p, void* bas
   EnhanceBufs e;
   e.map = c.take<int32_t>(px);
   e.mbits = c.take<uint32_t>((size_t)p.max_bins * p.bin_h * ((p.bin_w + 31) / 32));
-  e.counters = c.take<int32_t>(64);
+  e.counters = c.take<int32_t>(N_COUNTERS);
   e.x0 = c.take<uint8_t>(px * 8 * es);
   e.a0 = c.take<uint8_t>(px * C8 * 8 * es);
   if (net->cfg.n_resblocks > 0) {
@@ -359,6 +361,15 @@ static regen_status run_conv(const SRNet* net, const ConvDesc& cv, const void* i
     return conv_tc_launch(net, cv, in, out, skip, e.mbits, p.max_bins, d_num_bins, p.bin_w, p.bin_h,
                           e.counters + (&cv - net->convs.data()), s);
   return conv_simt_launch(net, cv, in, out, skip, e.map, p.max_bins, d_num_bins, p.bin_w, p.bin_h, s);
+}
+
+// the UP∘TAIL fold runs when the folded conv has a tcgen05 plan (REGEN_NO_FOLD=1 forces the literal
+// upsampler + tail, for A/B checks)
+static bool fold_enabled(const SRNet* net, int bin_w) {
+  if (net->fold_conv < 0 || !net->use_tc) return false;
+  const char* off = getenv("REGEN_NO_FOLD");
+  if (off && off[0] == '1') return false;
+  return conv_tc_supported(net, net->convs[net->fold_conv], bin_w);
 }
 
 static regen_status validate_pack(const regen_pack_params* p) {
@@ -420,6 +431,22 @@ extern "C" regen_status regen_stitch_bins(const regen_geom* geom, const regen_pa
                      d_lr_bins, (cudaStream_t)stream);
 }
 
+extern "C" regen_status regen_enhance_kernel_count(const void* sr, const regen_pack_params* p, int32_t* count) {
+  REGEN_REQUIRE(sr && p && count, "null argument");
+  const SRNet* net = (const SRNet*)sr;
+  const int nr = net->cfg.n_resblocks;
+  int n = 2;   // paint + gather
+  if (nr == 0) {
+    n += 2;
+  } else {
+    n += 1 + (resblock_tc_supported(net, p->bin_w) ? nr : 2 * nr) + 1;   // head, residual blocks, body
+    if (net->cfg.scale == 4) n += 1;                                      // first x2 stage
+    n += 2;                                                               // UP + TAIL, or FOLD + combine
+  }
+  *count = n;
+  return REGEN_OK;
+}
+
 extern "C" regen_status regen_enhance_packed(void* sr, const regen_geom* geom, const regen_pack_params* p,
                                              const uint8_t* d_frames, const regen_box* d_boxes, int64_t max_boxes,
                                              const int64_t* d_num_boxes, const int32_t* d_num_bins, void* d_hr_bins,
@@ -436,7 +463,7 @@ extern "C" regen_status regen_enhance_packed(void* sr, const regen_geom* geom, c
   REGEN_REQUIRE(d_ws && ws_bytes >= e.bytes, "workspace too small (%zu < %zu)", ws_bytes, e.bytes);
   e = enhance_bufs(net, *p, d_ws);
   cudaStream_t s = (cudaStream_t)stream;
-  REGEN_CUDA(cudaMemsetAsync(e.counters, 0, 64 * sizeof(int32_t), s));
+  REGEN_CUDA(cudaMemsetAsync(e.counters, 0, N_COUNTERS * sizeof(int32_t), s));
   st = stitch_into(*geom, *p, net->cfg.dtype, 0, d_frames, d_boxes, d_num_boxes, max_boxes, d_num_bins, e.map, e.x0, s,
                    e.mbits);
   if (st != REGEN_OK) return st;
@@ -454,7 +481,7 @@ extern "C" regen_status regen_enhance_packed(void* sr, const regen_geom* geom, c
     // fused residual blocks (t stays in SMEM), ping-pong a1 <-> a2
     for (int k = 0; k < net->cfg.n_resblocks && st == REGEN_OK; ++k) {
       void* o = (k & 1) ? e.a2 : e.a1;
-      st = resblock_tc_launch(net, k, r, o, e.mbits, p->max_bins, d_num_bins, p->bin_w, p->bin_h, e.counters + 32 + k, s);
+      st = resblock_tc_launch(net, k, r, o, e.mbits, p->max_bins, d_num_bins, p->bin_w, p->bin_h, e.counters + RB_COUNTER0 + k, s);
       r = o;
       i += 2;
     }
@@ -469,12 +496,19 @@ extern "C" regen_status regen_enhance_packed(void* sr, const regen_geom* geom, c
   }
   if (st == REGEN_OK) st = run_conv(net, cv[i++], r, body_out, e.a0, e, *p, d_num_bins, s);  // body + h
   if (st != REGEN_OK) return st;
-  if (net->cfg.scale == 4) {
+  const void* up_in = body_out;
+  if (net->cfg.scale == 4) {   // first x2 stage
     st = run_conv(net, cv[i++], body_out, e.u1, nullptr, e, *p, d_num_bins, s);
-    if (st == REGEN_OK) st = run_conv(net, cv[i++], e.u1, e.u, nullptr, e, *p, d_num_bins, s);
-  } else {
-    st = run_conv(net, cv[i++], body_out, e.u, nullptr, e, *p, d_num_bins, s);
+    up_in = e.u1;
   }
+  if (st != REGEN_OK) return st;
+  if (fold_enabled(net, p->bin_w)) {
+    // last upsampler + tail as the folded conv (partials in e.u) and the partial-sum combine
+    st = run_conv(net, cv[net->fold_conv], up_in, e.u, nullptr, e, *p, d_num_bins, s);
+    if (st == REGEN_OK) st = fold_combine_launch(net, e.u, d_hr_bins, e.mbits, p->max_bins, d_num_bins, p->bin_w, p->bin_h, s);
+    return st;
+  }
+  st = run_conv(net, cv[i++], up_in, e.u, nullptr, e, *p, d_num_bins, s);
   if (st == REGEN_OK) st = run_conv(net, cv[i++], e.u, d_hr_bins, nullptr, e, *p, d_num_bins, s);  // tail
   return st;
 }

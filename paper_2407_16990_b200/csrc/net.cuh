@@ -19,7 +19,8 @@ enum ConvRole : int {
   ROLE_UP = 4,       // -> conv, PixelShuffle(ps) into the next resolution
   ROLE_TAIL = 5,     // -> HR output [bin][y][x][4]
   ROLE_TINY0 = 6,    // x0 -> relu(conv)
-  ROLE_TINY1 = 7     // -> conv, PixelShuffle(scale) into the HR output
+  ROLE_TINY1 = 7,    // -> conv, PixelShuffle(scale) into the HR output
+  ROLE_FOLD = 8      // UP∘TAIL fold: conv C -> 3(p+2)^2 partial sums (upfold.cu)
 };
 
 struct ConvDesc {
@@ -45,13 +46,17 @@ struct SRNet {
   std::vector<float> tc_weights;   // host copy of the (rounded) weights for B-image packing
   int tc_bin_w = -1;             // bin width the B images were planned for
   void* rb_images = nullptr;     // fused-resblock B images (resblock_tc.cu)
+  int fold_conv = -1;            // index of the ROLE_FOLD conv in convs (-1: none)
 };
+
+constexpr int N_COUNTERS = 256, RB_COUNTER0 = 160;   // convs <= 2*64 + 6, residual blocks <= 64
 
 // enhance workspace layout
 struct EnhanceBufs {
   int32_t* map;      // [max_bins][bin_h][bin_w] box index covering the pixel, -1 outside boxes
   uint32_t* mbits;   // [max_bins][bin_h][ceil(bin_w/32)] occupancy bits (map >= 0)
-  int32_t* counters; // [64] per-conv dynamic scheduler counters, zeroed per call
+  int32_t* counters; // [N_COUNTERS] dynamic scheduler counters, zeroed per call: conv i at i,
+                     // fused residual block k at RB_COUNTER0 + k
   void* x0;          // [max_bins][bin_h][1][bin_w][8]
   void* a0;          // [max_bins][bin_h][C/8][bin_w][8]  (h)
   void* a1;          // (r)
@@ -71,6 +76,9 @@ bool conv_tc_supported(const SRNet* net, const ConvDesc& cv, int bin_w);
 regen_status conv_tc_prepare(SRNet* net);
 void conv_tc_release(SRNet* net);
 bool resblock_tc_supported(const SRNet* net, int bin_w);
+void fold_prepare(SRNet* net, std::vector<float>& w32);
+regen_status fold_combine_launch(const SRNet* net, const void* P, void* hr_bins, const uint32_t* mbits, int max_bins,
+                                 const int32_t* d_num_bins, int bin_w, int bin_h, cudaStream_t s);
 void resblock_tc_release(SRNet* net);
 regen_status resblock_tc_launch(const SRNet* net, int block, const void* in, void* out, const uint32_t* mbits,
                                 int max_bins, const int32_t* d_num_bins, int bin_w, int bin_h, int* counter,

@@ -216,3 +216,15 @@ def test_sr_tensor_core_matches_simt_path():
     with REGEN_FORCE_SIMT=1 is not needed: compare both against the oracle on a shared box set)."""
     wl = synth.small(synth.CONFIGS["c2"], F=2)
     _check_pixels(wl, seed=9, box_sample=lambda n: range(1, n, max(1, n // 5)))
+
+
+@pytest.mark.parametrize("s,C", [(3, 32), (2, 32), (4, 16), (3, 64)])
+def test_upsampler_tail_fold_matches_oracle_and_literal_path(s, C, monkeypatch):
+    """The UP∘TAIL fold (upfold.cu) and the literal upsampler + tail both stay within the
+    bf16 tolerance of the oracle on the same boxes (REGEN_NO_FOLD=1 selects the literal path)."""
+    wl = dataclasses.replace(synth.small(synth.CONFIGS["c2"], F=1), sr=synth.SRConfig(s, C, 1, 1.0, True))
+    sample = lambda n: range(0, n, max(1, n // 8))  # noqa: E731
+    worst_fold = _check_pixels(wl, seed=11, kind="noisy", box_sample=sample)
+    monkeypatch.setenv("REGEN_NO_FOLD", "1")
+    worst_lit = _check_pixels(wl, seed=11, kind="noisy", box_sample=sample)
+    assert worst_fold <= TOL[True] and worst_lit <= TOL[True]
