@@ -9,7 +9,7 @@
 //   writes each t row into an SMEM ring in the UMMA operand layout (generic-proxy stores + proxy fence);
 //   conv_b consumes those t rows from SMEM into TMEM ring B; epilogue quad B (warps 6-9) adds the
 //   residual (r, prefetched from HBM/L2) and stores r'.
-// One thread (warp 1) issues both convs' MMAs, interleaving conv_b group k with conv_a group k+LAG.
+// Two issuing threads: warp 1 issues conv_a, warp 10 conv_b (each waits only on its own inputs).
 // Synchronisation is per group of G rows: r ring (in_full/in_empty), TMEM ring A and B
 // (acc*_full/acc*_empty), t ring (t_full by quad A, t_empty by tcgen05.commit). TMEM columns are
 // computed at run time from the per-CTA row sequence (no branches in the MMA stream).
@@ -26,12 +26,11 @@ namespace tc {
 
 namespace rb {
 
-constexpr int NTHREADS = 320;
+constexpr int NTHREADS = 352;   // warp 0 producer, 1 conv_a MMAs, 2-9 epilogues, 10 conv_b MMAs
 constexpr int BR = 32;        // output rows per unit
 constexpr int NA_OUT = BR + 2;   // t rows per unit
 constexpr int NA_IN = BR + 4;    // r rows per unit
 constexpr int NSLOT = 4;      // r-ring and t-ring groups (power of two)
-constexpr int LAG = 3;        // conv_b group k is issued after conv_a group k + LAG
 
 struct Params {
   const __nv_bfloat16* in;    // r
@@ -46,6 +45,7 @@ struct Params {
   float res_scale;
   int* counter;
   unsigned long long* prof;   // REGEN_TC_PROF=1: wait-time counters
+  int dbg;                    // REGEN_RB_DBG bits (timing experiments only): 1 no epilogue work, 2 no row loads, 4 no MMAs
 };
 
 template <int C, int R, int G>
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
       mbar_init(&b_fullacc[i], 1); mbar_init(&b_emptyacc[i], 4);
     }
     mbar_init(&w_full, 1);
-    for (int i = 0; i < 4; ++i) { mbar_init(&unit_full[i], 1); mbar_init(&unit_empty[i], 9); }
+    for (int i = 0; i < 4; ++i) { mbar_init(&unit_full[i], 1); mbar_init(&unit_empty[i], 10); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
   // arm both accumulator rings with their biases
-  if (warp >= 2) {
+  if (warp >= 2 && warp < 10) {
     const int quad = (warp - 2) >> 2, q4 = warp & 3;
     for (int s = 0; s < R; ++s)
 #pragma unroll
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
           mbar_wait(&in_empty[slot], ((ig / NSLOT) & 1) ^ 1);
           const int g0 = y0 - 2 + G * k;
           const int a = max(g0, rlo), b = min(g0 + G - 1, rhi);
-          if (a <= b) {
+          if (a <= b && !(p.dbg & 2)) {
             mbar_expect_tx(&in_full[slot], (uint32_t)(b - a + 1) * ROW_BYTES);
             bulk_g2s(rring + slot * GRP + (uint32_t)(a - g0) * ROW_BYTES,
                      p.in + ((size_t)bin * p.Hr + a) * (ROW_BYTES / 2), (uint32_t)(b - a + 1) * ROW_BYTES,
@@ -191,9 +191,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
         }
       }
     }
-  } else if (warp == 1) {
-    // =============================== MMA issuer (both convs) ===============================
+  } else if (warp == 1 || warp == 10) {
+    // =============================== MMA issuers: conv_a (warp 1), conv_b (warp 10) ===============
+    // Two issuing threads, so a conv_b wait for a t row never holds back conv_a's MMAs (tcgen05.commit
+    // tracks the MMAs of the committing thread only).
     if (elect_one()) {
+      const bool conv_a = warp == 1;
       uint32_t ig = 0, tg = 0;      // r-ring groups consumed, t-ring groups consumed
       uint32_t qa = 0, qb = 0;      // accumulator group sequences (ring A, ring B)
       const uint32_t r16 = smem_u32(rring) >> 4, t16 = smem_u32(tring) >> 4;
@@ -207,12 +210,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
         const int bin = u / p.nbands, y0 = (u - bin * p.nbands) * BR;
         const int y1 = min(p.Hr, y0 + BR);
         const int rlo = max(y0 - 2, 0), rhi = min(y1 + 1, p.Hr - 1);
-        const uint32_t seqA = qa * G, seqB = qb * G;
+        if (conv_a) {
+          const uint32_t seqA = qa * G;
 #pragma unroll
-        for (int step = 0; step < S::NGA_IN + LAG; ++step) {
-          if (step < S::NGA_IN) {
+          for (int k = 0; k < S::NGA_IN; ++k) {
             // ---- conv_a, input group k: r rows y0-2 + G*k ...
-            const int k = step;
             const uint32_t slot = (ig + k) & (NSLOT - 1);
             if (k < S::NGA_OUT) { const long long t0_ = clock64(); mbar_wait(&a_empty[(qa + k) % S::OGR], (((qa + k) / S::OGR) & 1) ^ 1); if (p.prof) w_ae += clock64() - t0_; }
             { const long long t0_ = clock64(); mbar_wait(&in_full[slot], ((ig + k) / NSLOT) & 1); if (p.prof) w_if += clock64() - t0_; }
@@ -222,7 +224,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
               const int i = G * k + ii;
               if (i >= NA_IN) continue;
               const int r = y0 - 2 + i;
-              const uint32_t en = (r >= rlo && r <= rhi) ? 1u : 0u;
+              const uint32_t en = (r >= rlo && r <= rhi && !(p.dbg & 4)) ? 1u : 0u;
               issue_row<C, R, G>(i, NA_OUT, seqA, tmem, r16 + slot * (GRP / 16) + ii * (ROW_BYTES / 16), ba16, en);
             }
             mma_commit(&in_empty[slot]);
@@ -235,9 +237,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
                 if (S::done_group(ka, NA_OUT) > k) mma_commit(&a_full[(qa + ka) % S::OGR]);
             }
           }
-          if (step >= LAG && step - LAG < S::NGA_OUT) {
+        } else {
+          const uint32_t seqB = qb * G;
+#pragma unroll
+          for (int kb = 0; kb < S::NGA_OUT; ++kb) {
             // ---- conv_b, input group kb: t rows y0-1 + G*kb ... (SMEM t ring)
-            const int kb = step - LAG;
             const uint32_t tslot = (tg + kb) & (NSLOT - 1);
             if (kb < S::NGB_OUT) { const long long t0_ = clock64(); mbar_wait(&b_emptyacc[(qb + kb) % S::OGR], (((qb + kb) / S::OGR) & 1) ^ 1); if (p.prof) w_be += clock64() - t0_; }
             { const long long t0_ = clock64(); mbar_wait(&t_full[tslot], ((tg + kb) / NSLOT) & 1); if (p.prof) w_tf += clock64() - t0_; }
@@ -247,7 +251,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
               const int i = G * kb + ii;
               if (i >= NA_OUT) continue;
               const int tr = y0 - 1 + i;
-              const uint32_t en = (tr >= 0 && tr < p.Hr) ? 1u : 0u;
+              const uint32_t en = (tr >= 0 && tr < p.Hr && !(p.dbg & 4)) ? 1u : 0u;
               issue_row<C, R, G>(i, BR, seqB, tmem + S::COLB, t16 + tslot * (GRP / 16) + ii * (ROW_BYTES / 16), bb16,
                                  en);
             }
@@ -306,7 +310,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
           for (int jj = 0; jj < G; ++jj) {
             const int ja = G * ka + jj;
             const uint32_t taddr = tmem + lane_off + ring_slot(seqA + (uint32_t)ja, Rm) * (uint32_t)C;
-            if (ja < NA_OUT) {
+            if (ja < NA_OUT && !(p.dbg & 1)) {
               const bool occ = (occw[jj] >> (m & 31)) & 1u;
               uint32_t r[C];
 #pragma unroll
@@ -344,7 +348,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
             occw[jj] = __ldg(p.mbits + ((size_t)bin * p.bin_h + y) * words + m / 32);
             const size_t act = (size_t)bin * bin_px * C + (size_t)y * (C / 8) * PSTRIDE + (size_t)m * 8;
 #pragma unroll
-            for (int g = 0; g < C / 8; ++g) sk[jj][g] = *reinterpret_cast<const uint4*>(p.in + act + g * PSTRIDE);
+            for (int g = 0; g < C / 8; ++g)
+              sk[jj][g] = (p.dbg & 1) ? make_uint4(0, 0, 0, 0) : *reinterpret_cast<const uint4*>(p.in + act + g * PSTRIDE);
           }
           { const long long t0_ = clock64(); mbar_wait(&b_fullacc[(qb + jb) % S::OGR], ((qb + jb) / S::OGR) & 1); if (p.prof) w_eb += clock64() - t0_; }
           tc_fence_after();
@@ -352,7 +357,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
           for (int jj = 0; jj < G; ++jj) {
             const int j = G * jb + jj;
             const uint32_t taddr = tmem + lane_off + (uint32_t)S::COLB + ring_slot(seqB + (uint32_t)j, Rm) * (uint32_t)C;
-            if (j < nrows) {
+            if (j < nrows && !(p.dbg & 1)) {
               const int y = y0 + j;
               const bool occ = (occw[jj] >> (m & 31)) & 1u;
               uint32_t r[C];
@@ -391,9 +396,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
     const long long tot = clock64() - pstart;
     if (warp == 1) {
       atomicAdd(p.prof + 0, (unsigned long long)tot); atomicAdd(p.prof + 1, (unsigned long long)w_ae);
-      atomicAdd(p.prof + 2, (unsigned long long)w_if); atomicAdd(p.prof + 3, (unsigned long long)w_be);
-      atomicAdd(p.prof + 4, (unsigned long long)w_tf);
+      atomicAdd(p.prof + 2, (unsigned long long)w_if);
     }
+    if (warp == 10) { atomicAdd(p.prof + 3, (unsigned long long)w_be); atomicAdd(p.prof + 4, (unsigned long long)w_tf); }
     if (warp >= 2 && warp < 6) { atomicAdd(p.prof + 5, (unsigned long long)w_ea); atomicAdd(p.prof + 6, (unsigned long long)w_te); }
     if (warp >= 6) atomicAdd(p.prof + 7, (unsigned long long)w_eb);
   }
@@ -498,6 +503,10 @@ regen_status resblock_tc_launch(const SRNet* cnet, int block, const void* in, vo
   p.nbands = (bin_h + BR - 1) / BR;
   p.res_scale = net->cfg.res_scale;
   p.counter = counter;
+  {
+    const char* dbg = getenv("REGEN_RB_DBG");
+    p.dbg = dbg ? atoi(dbg) : 0;
+  }
   void (*kern)(Params) = nullptr;
   int G = 0;
   if (C == 32) { kern = resblock_tc_kernel<32, 8, 2>; G = 2; }
