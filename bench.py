@@ -262,8 +262,7 @@ def main() -> None:
                 front_done[k % 2].record(s_front)
             with torch.cuda.stream(s_back):
                 s_back.wait_event(front_done[k % 2])
-                q.enhance(fr, stream=s_back)
-                q.scatter(fr, stream=s_back)
+                q.enhance_scatter(fr, stream=s_back)
                 back_done[k % 2].record(s_back)
 
     for _ in range(args.warmup):

@@ -50,7 +50,8 @@ enum { REGEN_MODE_TOPK = 0, REGEN_MODE_THRESHOLD = 1 };
 enum { REGEN_SCOPE_GLOBAL = 0, REGEN_SCOPE_PER_STREAM = 1, REGEN_SCOPE_PER_FRAME = 2 };
 enum { REGEN_ORDER_DENSITY = 0, REGEN_ORDER_AREA = 1 };
 enum { REGEN_DTYPE_BF16 = 0, REGEN_DTYPE_FP32 = 1 };
-enum { REGEN_CALL_SELECT = 0, REGEN_CALL_PACK = 1, REGEN_CALL_ENHANCE = 2, REGEN_CALL_SCATTER = 3 };
+enum { REGEN_CALL_SELECT = 0, REGEN_CALL_PACK = 1, REGEN_CALL_ENHANCE = 2, REGEN_CALL_SCATTER = 3,
+       REGEN_CALL_ENHANCE_SCATTER = 4 };
 
 /* asynchronous status bits (*d_status) */
 enum {
@@ -188,6 +189,22 @@ REGEN_API regen_status regen_scatter_blend(const regen_geom* geom, const regen_p
                                  const uint8_t* d_frames, const regen_box* d_boxes,
                                  const int32_t* d_mb_owner, const void* d_hr_bins, int32_t hr_dtype,
                                  void* d_out, int32_t out_dtype, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * a6+a7+a8 in one call: the HR frames d_out (as regen_scatter_blend) from the packed boxes, equal
+ * bit for bit to regen_enhance_packed followed by regen_scatter_blend with hr_dtype = the model
+ * dtype. When the network's last upsampler + tail run folded (BF16 tensor-core path)
+ * the HR bins are never formed: the fold's combine pass writes each owned selected MB's HR pixels
+ * straight into d_out and the scatter pass writes the bilinear pixels only (the paper's paste-back,
+ * P:771, without the HR-bin round trip). Otherwise the two calls run back to back with the HR bins
+ * in the workspace. Workspace: regen_workspace_size(REGEN_CALL_ENHANCE_SCATTER, geom, &pack_params,
+ * sr, &bytes). Argument errors as regen_enhance_packed / regen_scatter_blend.
+ * ------------------------------------------------------------------------------------------- */
+REGEN_API regen_status regen_enhance_scatter(void* sr, const regen_geom* geom, const regen_pack_params* params,
+                                   const uint8_t* d_frames, const regen_box* d_boxes, int64_t max_boxes,
+                                   const int64_t* d_num_boxes, const int32_t* d_num_bins,
+                                   const int32_t* d_mb_owner, void* d_out, int32_t out_dtype,
+                                   int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream);
 
 /* Workspace bytes for a call (which = REGEN_CALL_*; params = the call's params struct;
  * sr = SR handle for ENHANCE, else NULL). */

@@ -21,12 +21,13 @@ MODE_TOPK, MODE_THRESHOLD = 0, 1
 SCOPE_GLOBAL, SCOPE_PER_STREAM, SCOPE_PER_FRAME = 0, 1, 2
 ORDER_DENSITY, ORDER_AREA = 0, 1
 DTYPE_BF16, DTYPE_FP32 = 0, 1
-CALL_SELECT, CALL_PACK, CALL_ENHANCE, CALL_SCATTER = 0, 1, 2, 3
+CALL_SELECT, CALL_PACK, CALL_ENHANCE, CALL_SCATTER, CALL_ENHANCE_SCATTER = 0, 1, 2, 3, 4
 ST_REGION_OVERFLOW, ST_BOX_OVERFLOW, ST_FREELIST_OVERFLOW = 1, 2, 4
 
 EXPORTED = ["regen_select_mbs", "regen_pack_regions", "regen_sr_create", "regen_sr_destroy", "regen_stitch_bins",
             "regen_enhance_packed", "regen_scatter_blend", "regen_workspace_size", "regen_capacity_mbs",
-            "regen_status_string", "regen_last_error", "regen_abi_version", "regen_enhance_kernel_count"]
+            "regen_status_string", "regen_last_error", "regen_abi_version", "regen_enhance_kernel_count",
+            "regen_enhance_scatter"]
 
 
 class Geom(ctypes.Structure):
@@ -78,6 +79,8 @@ def _load():
     lib.regen_stitch_bins.argtypes = [P(Geom), P(PackParams), i32, vp, vp, i64, vp, vp, vp, vp, sz, vp]
     lib.regen_enhance_packed.argtypes = [vp, P(Geom), P(PackParams), vp, vp, i64, vp, vp, vp, vp, vp, sz, vp]
     lib.regen_scatter_blend.argtypes = [P(Geom), P(PackParams), i32, vp, vp, vp, vp, i32, vp, i32, vp]
+    lib.regen_enhance_scatter.argtypes = [vp, P(Geom), P(PackParams), vp, vp, i64, vp, vp, vp, vp, i32, vp, vp, sz,
+                                          vp]
     lib.regen_workspace_size.argtypes = [i32, P(Geom), vp, vp, P(sz)]
     lib.regen_enhance_kernel_count.argtypes = [vp, P(PackParams), P(i32)]
     lib.regen_capacity_mbs.argtypes = [i32, i32, i32, i32]
@@ -87,7 +90,7 @@ def _load():
     lib.regen_abi_version.restype = i32
     for name in ["regen_select_mbs", "regen_pack_regions", "regen_sr_create", "regen_sr_destroy",
                  "regen_stitch_bins", "regen_enhance_packed", "regen_scatter_blend", "regen_workspace_size",
-                 "regen_enhance_kernel_count"]:
+                 "regen_enhance_kernel_count", "regen_enhance_scatter"]:
         getattr(lib, name).restype = ctypes.c_int
     return lib
 
@@ -155,6 +158,13 @@ def enhance_packed(sr, geom, params, frames, boxes, max_boxes, num_boxes, num_bi
            "regen_enhance_packed")
 
 
+def enhance_scatter(sr, geom, params, frames, boxes, max_boxes, num_boxes, num_bins, mb_owner, out, out_dtype, status,
+                    ws, stream=None):
+    _check(lib.regen_enhance_scatter(sr.handle, ctypes.byref(geom), ctypes.byref(params), _ptr(frames), _ptr(boxes),
+                                     max_boxes, _ptr(num_boxes), _ptr(num_bins), _ptr(mb_owner), _ptr(out), out_dtype,
+                                     _ptr(status), _ptr(ws), ws.numel(), _stream(stream)), "regen_enhance_scatter")
+
+
 def scatter_blend(geom, params, scale, frames, boxes, mb_owner, hr_bins, hr_dtype, out, out_dtype, stream=None):
     _check(lib.regen_scatter_blend(ctypes.byref(geom), ctypes.byref(params), scale, _ptr(frames), _ptr(boxes),
                                    _ptr(mb_owner), _ptr(hr_bins), hr_dtype, _ptr(out), out_dtype, _stream(stream)),
@@ -214,14 +224,23 @@ class Pipeline:
         self.order = torch.empty(self.max_boxes, dtype=i32, device=dev)
         self.owner = torch.empty(self.n_mbs, dtype=i32, device=dev)
         ws = max(workspace_size(CALL_SELECT, self.geom), workspace_size(CALL_PACK, self.geom),
-                 workspace_size(CALL_ENHANCE, self.geom, self.pack, self.sr.handle))
+                 workspace_size(CALL_ENHANCE, self.geom, self.pack, self.sr.handle),
+                 workspace_size(CALL_ENHANCE_SCATTER, self.geom, self.pack, self.sr.handle))
         self.ws = torch.empty(ws, dtype=u8, device=dev)
-        hr_t = torch.bfloat16 if bf16 else torch.float32
         self.hr_dtype = DTYPE_BF16 if bf16 else DTYPE_FP32
-        self.hr_bins = torch.empty((max_bins, scale * bin_h, scale * bin_w, 4), dtype=hr_t, device=dev)
+        self._hr_shape = (max_bins, scale * bin_h, scale * bin_w, 4)
+        self._hr_bins = None   # allocated on first use of the separate enhance/scatter calls
         self.out_dtype = (DTYPE_BF16 if bf16 else DTYPE_FP32) if out_dtype is None else out_dtype
         self.out = torch.empty((S, F, scale * H, scale * W, 3),
                                dtype=torch.bfloat16 if self.out_dtype == DTYPE_BF16 else torch.float32, device=dev)
+
+    @property
+    def hr_bins(self):
+        if self._hr_bins is None:
+            t = self.torch
+            self._hr_bins = t.empty(self._hr_shape, dtype=t.bfloat16 if self.hr_dtype == DTYPE_BF16 else t.float32,
+                                    device=self.out.device)
+        return self._hr_bins
 
     @property
     def num_regions_t(self):
@@ -251,9 +270,19 @@ class Pipeline:
                       out, self.out_dtype, stream)
         return out
 
-    def run(self, importance, frames, out=None, stream=None):
+    def enhance_scatter(self, frames, out=None, stream=None):
+        """a6-a8 in one call (regen_enhance_scatter): HR frames without the HR-bin round trip."""
+        out = self.out if out is None else out
+        enhance_scatter(self.sr, self.geom, self.pack, frames, self.boxes, self.max_boxes, self.counts[1:2],
+                        self.num_bins, self.owner, out, self.out_dtype, self.status, self.ws, stream)
+        return out
+
+    def run(self, importance, frames, out=None, stream=None, fused=True):
+        """select -> pack -> enhance -> scatter; fused=True uses regen_enhance_scatter for the last two."""
         self.select(importance, stream)
         self.pack_step(importance, stream)
+        if fused:
+            return self.enhance_scatter(frames, out, stream)
         self.enhance(frames, stream)
         return self.scatter(frames, out, stream)
 

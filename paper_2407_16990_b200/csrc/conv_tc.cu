@@ -59,6 +59,7 @@ struct Params {
   float res_scale;
   unsigned long long* prof; // optional wait-time counters (REGEN_TC_PROF=1), else null
   int* counter;             // dynamic unit scheduler (zeroed before the launch)
+  int reverse;              // hand out units last-to-first (L2 reuse along a conv chain)
 };
 
 // ------------------------------------------------------------------------------- compile-time shape
@@ -208,6 +209,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
       for (uint32_t us = 0;; ++us) {
         int u = atomicAdd(p.counter, 1);
         if (u >= total_units) u = -1;
+        else if (p.reverse) u = total_units - 1 - u;
         mbar_wait(&unit_empty[us & 3], ((us >> 2) & 1) ^ 1);
         unit_ring[us & 3] = u;
         mbar_arrive(&unit_full[us & 3]);
@@ -733,7 +735,7 @@ bool conv_tc_supported(const SRNet* net, const ConvDesc& cv, int bin_w) {
 
 regen_status conv_tc_launch(const SRNet* net, const ConvDesc& cv, const void* in, void* out, const void* skip,
                             const uint32_t* mbits, int max_bins, const int32_t* d_num_bins, int bin_w, int bin_h,
-                            int* counter, cudaStream_t s) {
+                            int* counter, cudaStream_t s, int reverse) {
   using namespace tc;
   const Plan* pl = get_plan(const_cast<SRNet*>(net), cv, bin_w);
   REGEN_REQUIRE(pl != nullptr, "no tcgen05 plan for conv");
@@ -759,6 +761,7 @@ regen_status conv_tc_launch(const SRNet* net, const ConvDesc& cv, const void* in
   p.out_c8 = cv.role == ROLE_UP ? net->cfg.channels / 8 : (cv.cout + 7) / 8;
   p.res_scale = cv.role == ROLE_RES_B ? net->cfg.res_scale : 1.0f;
   p.counter = counter;
+  p.reverse = reverse;
   const int cin8 = cv.cin == 3 ? 1 : cv.cin / 8;
   const uint32_t grp_bytes = (uint32_t)cin8 * p.Wr * 16 * pl->G;
   // deepest input ring that fits (row loads are latency-bound: more rows in flight per SM)

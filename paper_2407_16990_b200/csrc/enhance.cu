@@ -144,17 +144,30 @@ namespace regen {
 
 // ------------------------------------------------------------------------------------ stitch
 
+struct OwnArgs {          // optional: mark bin pixels whose source MB is owned by their box
+  const int32_t* owner;  // [S][F][GH][GW], null: skip
+  uint8_t* own8;
+  int F, GH, GW, mb;
+};
+
 __global__ void paint_kernel(const regen_box* boxes, const int64_t* num_boxes, int64_t max_boxes, int32_t* map,
-                             int bin_w, int bin_h) {
+                             int bin_w, int bin_h, OwnArgs oa) {
   const int64_t b = blockIdx.x;
   if (b >= min(*num_boxes, max_boxes)) return;
   const regen_box bx = boxes[b];
   if (bx.bin < 0) return;
   const int fw = bx.rotated ? bx.h : bx.w, fh = bx.rotated ? bx.w : bx.h;
   int32_t* m = map + (int64_t)bx.bin * bin_w * bin_h;
+  const int32_t* ow = oa.owner ? oa.owner + ((size_t)bx.stream * oa.F + bx.frame) * oa.GH * oa.GW : nullptr;
   for (int i = threadIdx.x; i < fw * fh; i += blockDim.x) {
     const int q = i / fw, p = i - q * fw;
-    m[(bx.by + q) * bin_w + bx.bx + p] = (int32_t)b;
+    const size_t px = (size_t)(bx.by + q) * bin_w + bx.bx + p;
+    m[px] = (int32_t)b;
+    if (ow) {
+      const int sx = bx.rotated ? bx.x0 + q : bx.x0 + p;
+      const int sy = bx.rotated ? bx.y0 + bx.h - 1 - p : bx.y0 + q;
+      oa.own8[(size_t)bx.bin * bin_w * bin_h + px] = ow[(sy / oa.mb) * oa.GW + sx / oa.mb] == (int32_t)b;
+    }
   }
 }
 
@@ -339,6 +352,7 @@ EnhanceBufs enhance_bufs(const SRNet* net, const regen_pack_params& p, void* bas
   EnhanceBufs e;
   e.map = c.take<int32_t>(px);
   e.mbits = c.take<uint32_t>((size_t)p.max_bins * p.bin_h * ((p.bin_w + 31) / 32));
+  e.own8 = c.take<uint8_t>(px);
   e.counters = c.take<int32_t>(N_COUNTERS);
   e.x0 = c.take<uint8_t>(px * 8 * es);
   e.a0 = c.take<uint8_t>(px * C8 * 8 * es);
@@ -354,12 +368,14 @@ EnhanceBufs enhance_bufs(const SRNet* net, const regen_pack_params& p, void* bas
   return e;
 }
 
+// `order` alternates along the conv chain: a conv hands out its units in the reverse order of the one
+// before it, so it starts on the bins its producer wrote last (still in L2).
 static regen_status run_conv(const SRNet* net, const ConvDesc& cv, const void* in, void* out, const void* skip,
                              const EnhanceBufs& e, const regen_pack_params& p, const int32_t* d_num_bins,
-                             cudaStream_t s) {
+                             cudaStream_t s, int order = 0) {
   if (net->use_tc && conv_tc_supported(net, cv, p.bin_w))
     return conv_tc_launch(net, cv, in, out, skip, e.mbits, p.max_bins, d_num_bins, p.bin_w, p.bin_h,
-                          e.counters + (&cv - net->convs.data()), s);
+                          e.counters + (&cv - net->convs.data()), s, order & 1);
   return conv_simt_launch(net, cv, in, out, skip, e.map, p.max_bins, d_num_bins, p.bin_w, p.bin_h, s);
 }
 
@@ -386,9 +402,17 @@ namespace regen {
 regen_status stitch_into(const regen_geom& g, const regen_pack_params& p, int dtype, int layout,
                          const uint8_t* d_frames, const regen_box* d_boxes, const int64_t* d_num_boxes,
                          int64_t max_boxes, const int32_t* d_num_bins, int32_t* map, void* out, cudaStream_t s,
-                         uint32_t* mbits = nullptr) {
+                         uint32_t* mbits = nullptr, const int32_t* owner = nullptr, uint8_t* own8 = nullptr) {
   REGEN_CUDA(cudaMemsetAsync(map, 0xFF, (size_t)p.max_bins * p.bin_w * p.bin_h * 4, s));
-  paint_kernel<<<(unsigned)max_boxes, 256, 0, s>>>(d_boxes, d_num_boxes, max_boxes, map, p.bin_w, p.bin_h);
+  OwnArgs oa;
+  oa.owner = owner;
+  oa.own8 = own8;
+  oa.F = g.F;
+  oa.GH = grid_h(g);
+  oa.GW = grid_w(g);
+  oa.mb = g.mb;
+  if (owner) REGEN_CUDA(cudaMemsetAsync(own8, 0, (size_t)p.max_bins * p.bin_w * p.bin_h, s));
+  paint_kernel<<<(unsigned)max_boxes, 256, 0, s>>>(d_boxes, d_num_boxes, max_boxes, map, p.bin_w, p.bin_h, oa);
   REGEN_LAUNCH_CHECK();
   dim3 grid((p.bin_w + 127) / 128, p.bin_h, p.max_bins);
   if (dtype == REGEN_DTYPE_BF16) {
@@ -447,6 +471,86 @@ extern "C" regen_status regen_enhance_kernel_count(const void* sr, const regen_p
   return REGEN_OK;
 }
 
+namespace regen {
+
+// stitch + SR of the packed batch; the HR result goes to hr_bins, or (fa != null, fold path only)
+// straight into the HR frames for owned MBs
+static regen_status enhance_run(const SRNet* net, const regen_geom* geom, const regen_pack_params* p,
+                                const uint8_t* d_frames, const regen_box* d_boxes, int64_t max_boxes,
+                                const int64_t* d_num_boxes, const int32_t* d_num_bins, void* d_hr_bins,
+                                const EnhanceBufs& e, cudaStream_t s, FoldFrameArgs* fa) {
+  REGEN_CUDA(cudaMemsetAsync(e.counters, 0, N_COUNTERS * sizeof(int32_t), s));
+  regen_status st = stitch_into(*geom, *p, net->cfg.dtype, 0, d_frames, d_boxes, d_num_boxes, max_boxes, d_num_bins,
+                                e.map, e.x0, s, e.mbits, fa ? fa->owner : nullptr, e.own8);
+  if (st != REGEN_OK) return st;
+  const auto& cv = net->convs;
+  if (net->cfg.n_resblocks == 0) {
+    st = run_conv(net, cv[0], e.x0, e.a0, nullptr, e, *p, d_num_bins, s);
+    if (st == REGEN_OK) st = run_conv(net, cv[1], e.a0, d_hr_bins, nullptr, e, *p, d_num_bins, s);
+    return st;
+  }
+  size_t i = 0;
+  int ord = 0;   // unit order of the next conv launch (alternating, see run_conv)
+  st = run_conv(net, cv[i++], e.x0, e.a0, nullptr, e, *p, d_num_bins, s, ord++);     // head -> h
+  const void* r = e.a0;
+  void* body_out = e.a2;
+  if (resblock_tc_supported(net, p->bin_w)) {
+    // fused residual blocks (t stays in SMEM), ping-pong a1 <-> a2
+    for (int k = 0; k < net->cfg.n_resblocks && st == REGEN_OK; ++k) {
+      void* o = (k & 1) ? e.a2 : e.a1;
+      st = resblock_tc_launch(net, k, r, o, e.mbits, p->max_bins, d_num_bins, p->bin_w, p->bin_h,
+                              e.counters + RB_COUNTER0 + k, s, (ord++) & 1);
+      r = o;
+      i += 2;
+    }
+    body_out = (r == e.a1) ? e.a2 : e.a1;
+  } else {
+    for (int k = 0; k < net->cfg.n_resblocks && st == REGEN_OK; ++k) {
+      st = run_conv(net, cv[i++], r, e.a2, nullptr, e, *p, d_num_bins, s, ord++);      // t = relu(conv(r))
+      if (st != REGEN_OK) break;
+      st = run_conv(net, cv[i++], e.a2, e.a1, r, e, *p, d_num_bins, s, ord++);         // r' = r + s*conv(t)
+      r = e.a1;
+    }
+  }
+  if (st == REGEN_OK) st = run_conv(net, cv[i++], r, body_out, e.a0, e, *p, d_num_bins, s, ord++);  // body + h
+  if (st != REGEN_OK) return st;
+  const void* up_in = body_out;
+  if (net->cfg.scale == 4) {   // first x2 stage
+    st = run_conv(net, cv[i++], body_out, e.u1, nullptr, e, *p, d_num_bins, s, ord++);
+    up_in = e.u1;
+  }
+  if (st != REGEN_OK) return st;
+  if (fold_enabled(net, p->bin_w)) {
+    // last upsampler + tail as the folded conv (partials in e.u) and the partial-sum combine
+    st = run_conv(net, cv[net->fold_conv], up_in, e.u, nullptr, e, *p, d_num_bins, s, ord++);
+    if (fa) {
+      fa->map = e.map;
+      fa->own8 = e.own8;
+    }
+    if (st == REGEN_OK)
+      st = fold_combine_launch(net, e.u, d_hr_bins, e.mbits, p->max_bins, d_num_bins, p->bin_w, p->bin_h, s, fa);
+    return st;
+  }
+  REGEN_REQUIRE(fa == nullptr, "frame output needs the fold path");
+  st = run_conv(net, cv[i++], up_in, e.u, nullptr, e, *p, d_num_bins, s, ord++);
+  if (st == REGEN_OK) st = run_conv(net, cv[i++], e.u, d_hr_bins, nullptr, e, *p, d_num_bins, s, ord++);  // tail
+  return st;
+}
+
+static size_t hr_bins_bytes(const SRNet* net, const regen_pack_params& p) {
+  const size_t es = net->cfg.dtype == REGEN_DTYPE_BF16 ? 2 : 4;
+  const size_t s = (size_t)net->cfg.scale;
+  return (size_t)p.max_bins * s * s * p.bin_w * p.bin_h * 4 * es;
+}
+
+// workspace of regen_enhance_scatter: the enhance buffers, plus the HR bins when the fold is off
+size_t enhance_scatter_ws_bytes(const SRNet* net, const regen_pack_params& p) {
+  const size_t e = (enhance_bufs(net, p, nullptr).bytes + 255) / 256 * 256;
+  return fold_enabled(net, p.bin_w) ? e : e + hr_bins_bytes(net, p) + 256;
+}
+
+}  // namespace regen
+
 extern "C" regen_status regen_enhance_packed(void* sr, const regen_geom* geom, const regen_pack_params* p,
                                              const uint8_t* d_frames, const regen_box* d_boxes, int64_t max_boxes,
                                              const int64_t* d_num_boxes, const int32_t* d_num_bins, void* d_hr_bins,
@@ -462,53 +566,46 @@ extern "C" regen_status regen_enhance_packed(void* sr, const regen_geom* geom, c
   EnhanceBufs e = enhance_bufs(net, *p, nullptr);
   REGEN_REQUIRE(d_ws && ws_bytes >= e.bytes, "workspace too small (%zu < %zu)", ws_bytes, e.bytes);
   e = enhance_bufs(net, *p, d_ws);
+  return enhance_run(net, geom, p, d_frames, d_boxes, max_boxes, d_num_boxes, d_num_bins, d_hr_bins, e,
+                     (cudaStream_t)stream, nullptr);
+}
+
+extern "C" regen_status regen_enhance_scatter(void* sr, const regen_geom* geom, const regen_pack_params* p,
+                                              const uint8_t* d_frames, const regen_box* d_boxes, int64_t max_boxes,
+                                              const int64_t* d_num_boxes, const int32_t* d_num_bins,
+                                              const int32_t* d_mb_owner, void* d_out, int32_t out_dtype,
+                                              int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream) {
+  REGEN_REQUIRE(sr != nullptr, "null SR handle");
+  regen_status st = validate_geom(geom);
+  if (st != REGEN_OK) return st;
+  st = validate_pack(p);
+  if (st != REGEN_OK) return st;
+  REGEN_REQUIRE(d_frames && d_boxes && d_num_boxes && d_num_bins && d_mb_owner && d_out && d_status,
+                "null device pointer");
+  REGEN_REQUIRE(max_boxes >= 1 && max_boxes < (1ll << 31), "bad max_boxes");
+  REGEN_REQUIRE(out_dtype == REGEN_DTYPE_BF16 || out_dtype == REGEN_DTYPE_FP32, "bad out dtype");
+  const SRNet* net = (const SRNet*)sr;
+  REGEN_REQUIRE(net->cfg.scale >= 2, "scale must be >= 2");
+  const size_t need = enhance_scatter_ws_bytes(net, *p);
+  REGEN_REQUIRE(d_ws && ws_bytes >= need, "workspace too small (%zu < %zu)", ws_bytes, need);
+  EnhanceBufs e = enhance_bufs(net, *p, d_ws);
   cudaStream_t s = (cudaStream_t)stream;
-  REGEN_CUDA(cudaMemsetAsync(e.counters, 0, N_COUNTERS * sizeof(int32_t), s));
-  st = stitch_into(*geom, *p, net->cfg.dtype, 0, d_frames, d_boxes, d_num_boxes, max_boxes, d_num_bins, e.map, e.x0, s,
-                   e.mbits);
-  if (st != REGEN_OK) return st;
-  const auto& cv = net->convs;
-  if (net->cfg.n_resblocks == 0) {
-    st = run_conv(net, cv[0], e.x0, e.a0, nullptr, e, *p, d_num_bins, s);
-    if (st == REGEN_OK) st = run_conv(net, cv[1], e.a0, d_hr_bins, nullptr, e, *p, d_num_bins, s);
-    return st;
-  }
-  size_t i = 0;
-  st = run_conv(net, cv[i++], e.x0, e.a0, nullptr, e, *p, d_num_bins, s);            // head -> h
-  const void* r = e.a0;
-  void* body_out = e.a2;
-  if (resblock_tc_supported(net, p->bin_w)) {
-    // fused residual blocks (t stays in SMEM), ping-pong a1 <-> a2
-    for (int k = 0; k < net->cfg.n_resblocks && st == REGEN_OK; ++k) {
-      void* o = (k & 1) ? e.a2 : e.a1;
-      st = resblock_tc_launch(net, k, r, o, e.mbits, p->max_bins, d_num_bins, p->bin_w, p->bin_h, e.counters + RB_COUNTER0 + k, s);
-      r = o;
-      i += 2;
-    }
-    body_out = (r == e.a1) ? e.a2 : e.a1;
-  } else {
-    for (int k = 0; k < net->cfg.n_resblocks && st == REGEN_OK; ++k) {
-      st = run_conv(net, cv[i++], r, e.a2, nullptr, e, *p, d_num_bins, s);             // t = relu(conv(r))
-      if (st != REGEN_OK) break;
-      st = run_conv(net, cv[i++], e.a2, e.a1, r, e, *p, d_num_bins, s);                // r' = r + s*conv(t)
-      r = e.a1;
-    }
-  }
-  if (st == REGEN_OK) st = run_conv(net, cv[i++], r, body_out, e.a0, e, *p, d_num_bins, s);  // body + h
-  if (st != REGEN_OK) return st;
-  const void* up_in = body_out;
-  if (net->cfg.scale == 4) {   // first x2 stage
-    st = run_conv(net, cv[i++], body_out, e.u1, nullptr, e, *p, d_num_bins, s);
-    up_in = e.u1;
-  }
-  if (st != REGEN_OK) return st;
   if (fold_enabled(net, p->bin_w)) {
-    // last upsampler + tail as the folded conv (partials in e.u) and the partial-sum combine
-    st = run_conv(net, cv[net->fold_conv], up_in, e.u, nullptr, e, *p, d_num_bins, s);
-    if (st == REGEN_OK) st = fold_combine_launch(net, e.u, d_hr_bins, e.mbits, p->max_bins, d_num_bins, p->bin_w, p->bin_h, s);
-    return st;
+    FoldFrameArgs fa;
+    fa.geom = *geom;
+    fa.map = nullptr;
+    fa.boxes = d_boxes;
+    fa.owner = d_mb_owner;
+    fa.out = d_out;
+    fa.out_dtype = out_dtype;
+    st = enhance_run(net, geom, p, d_frames, d_boxes, max_boxes, d_num_boxes, d_num_bins, nullptr, e, s, &fa);
+    if (st != REGEN_OK) return st;
+    return scatter_launch(*geom, *p, net->cfg.scale, d_frames, d_boxes, d_mb_owner, nullptr, net->cfg.dtype, d_out,
+                          out_dtype, true, s);
   }
-  st = run_conv(net, cv[i++], up_in, e.u, nullptr, e, *p, d_num_bins, s);
-  if (st == REGEN_OK) st = run_conv(net, cv[i++], e.u, d_hr_bins, nullptr, e, *p, d_num_bins, s);  // tail
-  return st;
+  void* hr = (uint8_t*)d_ws + (e.bytes + 255) / 256 * 256;
+  st = enhance_run(net, geom, p, d_frames, d_boxes, max_boxes, d_num_boxes, d_num_bins, hr, e, s, nullptr);
+  if (st != REGEN_OK) return st;
+  return scatter_launch(*geom, *p, net->cfg.scale, d_frames, d_boxes, d_mb_owner, hr, net->cfg.dtype, d_out, out_dtype,
+                        false, s);
 }

@@ -55,6 +55,8 @@ constexpr int N_COUNTERS = 256, RB_COUNTER0 = 160;   // convs <= 2*64 + 6, resid
 struct EnhanceBufs {
   int32_t* map;      // [max_bins][bin_h][bin_w] box index covering the pixel, -1 outside boxes
   uint32_t* mbits;   // [max_bins][bin_h][ceil(bin_w/32)] occupancy bits (map >= 0)
+  uint8_t* own8;     // [max_bins][bin_h][bin_w] 1 where the pixel's source MB is owned by its box
+                     // (written by paint only when the owner grid is given: regen_enhance_scatter)
   int32_t* counters; // [N_COUNTERS] dynamic scheduler counters, zeroed per call: conv i at i,
                      // fused residual block k at RB_COUNTER0 + k
   void* x0;          // [max_bins][bin_h][1][bin_w][8]
@@ -77,14 +79,28 @@ regen_status conv_tc_prepare(SRNet* net);
 void conv_tc_release(SRNet* net);
 bool resblock_tc_supported(const SRNet* net, int bin_w);
 void fold_prepare(SRNet* net, std::vector<float>& w32);
+// frame-output mode of the fold combine (regen_enhance_scatter)
+struct FoldFrameArgs {
+  regen_geom geom;
+  const int32_t* map;
+  const uint8_t* own8;
+  const regen_box* boxes;
+  const int32_t* owner;
+  void* out;
+  int out_dtype;
+};
 regen_status fold_combine_launch(const SRNet* net, const void* P, void* hr_bins, const uint32_t* mbits, int max_bins,
-                                 const int32_t* d_num_bins, int bin_w, int bin_h, cudaStream_t s);
+                                 const int32_t* d_num_bins, int bin_w, int bin_h, cudaStream_t s,
+                                 const FoldFrameArgs* fa = nullptr);
+regen_status scatter_launch(const regen_geom& g, const regen_pack_params& p, int scale, const uint8_t* d_frames,
+                            const regen_box* d_boxes, const int32_t* d_mb_owner, const void* d_hr_bins, int hr_dtype,
+                            void* d_out, int out_dtype, bool skip_owned, cudaStream_t s);
 void resblock_tc_release(SRNet* net);
 regen_status resblock_tc_launch(const SRNet* net, int block, const void* in, void* out, const uint32_t* mbits,
                                 int max_bins, const int32_t* d_num_bins, int bin_w, int bin_h, int* counter,
-                                cudaStream_t s);
+                                cudaStream_t s, int reverse = 0);
 regen_status conv_tc_launch(const SRNet* net, const ConvDesc& cv, const void* in, void* out, const void* skip,
                             const uint32_t* mbits, int max_bins, const int32_t* d_num_bins, int bin_w, int bin_h,
-                            int* counter, cudaStream_t s);
+                            int* counter, cudaStream_t s, int reverse = 0);
 
 }  // namespace regen

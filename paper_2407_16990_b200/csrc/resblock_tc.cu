@@ -45,6 +45,7 @@ struct Params {
   float res_scale;
   int* counter;
   unsigned long long* prof;   // REGEN_TC_PROF=1: wait-time counters
+  int reverse;                // hand out units last-to-first (L2 reuse along the chain)
   int dbg;                    // REGEN_RB_DBG bits (timing experiments only): 1 no epilogue work, 2 no row loads, 4 no MMAs
 };
 
@@ -168,6 +169,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
       for (uint32_t us = 0;; ++us) {
         int u = atomicAdd(p.counter, 1);
         if (u >= total_units) u = -1;
+        else if (p.reverse) u = total_units - 1 - u;
         mbar_wait(&unit_empty[us & 3], ((us >> 2) & 1) ^ 1);
         unit_ring[us & 3] = u;
         mbar_arrive(&unit_full[us & 3]);
@@ -480,7 +482,7 @@ void resblock_tc_release(SRNet* net) {
 
 regen_status resblock_tc_launch(const SRNet* cnet, int block, const void* in, void* out, const uint32_t* mbits,
                                 int max_bins, const int32_t* d_num_bins, int bin_w, int bin_h, int* counter,
-                                cudaStream_t s) {
+                                cudaStream_t s, int reverse) {
   using namespace tc::rb;
   SRNet* net = const_cast<SRNet*>(cnet);
   RbImages* im = rb_images(net);
@@ -503,6 +505,7 @@ regen_status resblock_tc_launch(const SRNet* cnet, int block, const void* in, vo
   p.nbands = (bin_h + BR - 1) / BR;
   p.res_scale = net->cfg.res_scale;
   p.counter = counter;
+  p.reverse = reverse;
   {
     const char* dbg = getenv("REGEN_RB_DBG");
     p.dbg = dbg ? atoi(dbg) : 0;

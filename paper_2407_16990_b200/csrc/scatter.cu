@@ -1,9 +1,8 @@
 // a8: scatter-and-blend, eq. P:461-464 "SR(MB_s) + IN(unselected MBs)", "stitching them
-// back to bi-linear-interpolated non-regions". One thread writes 8 consecutive HR pixels (24
-// channels) of one output row: either the bilinear value (D10: half-pixel centres, edge clamp,
-// fp32) or, inside the HR square of an owned selected MB, the box's HR bin pixel (un-rotated, D7).
-// Every HR pixel is written exactly once; stores are 16-B vectors (bf16) / 32-B (fp32).
-#include "common.cuh"
+// back to bi-linear-interpolated non-regions". Every HR pixel is written exactly once: the bilinear
+// value (D10: half-pixel centres, edge clamp, fp32) or, inside the HR square of an owned selected MB,
+// the box's HR bin pixel (un-rotated, D7). Stores are 16-B vectors (bf16) / 32-B (fp32).
+#include "net.cuh"
 
 namespace regen {
 
@@ -14,6 +13,11 @@ __device__ __forceinline__ float ld_hr<float>(const float* p) { return *p; }
 template <>
 __device__ __forceinline__ float ld_hr<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(*p); }
 
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
 struct ScatterArgs {
   const uint8_t* frames;
   const regen_box* boxes;
@@ -22,106 +26,179 @@ struct ScatterArgs {
   void* out;
   int W, H, OW, OH, GW, GH, mb, s, bin_w, bin_h;
   float inv_s;
+  int skip_owned;   // regen_enhance_scatter: owned MBs were written by the fold combine
 };
 
-template <typename TH, typename TO>
-__global__ void __launch_bounds__(128) scatter_kernel(ScatterArgs a) {
-  const int64_t sf = blockIdx.z;
-  const int Y = blockIdx.y;
-  const int X0 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
-  // separable bilinear (D10): the block first interpolates the LR row pair vertically for the LR
-  // columns its 8*128 HR pixels touch, into SMEM
-  __shared__ float vrow[3 * (8 * 128 / 2 + 4)];
-  const int Xb = blockIdx.x * blockDim.x * 8;
-  const int xa_blk = min((int)fmaxf(((float)Xb + 0.5f) * a.inv_s - 0.5f, 0.0f), a.W - 1);
-  const int xb_blk = min((int)fmaxf(((float)min(Xb + 8 * (int)blockDim.x, a.OW) - 0.5f) * a.inv_s - 0.5f, 0.0f) + 1, a.W - 1);
-  {
-    const uint8_t* img = a.frames + sf * (int64_t)a.H * a.W * 3;
-    const float sy = fmaxf(((float)Y + 0.5f) * a.inv_s - 0.5f, 0.0f);
-    const int yl0 = min((int)sy, a.H - 1);
+// One CTA per (frame, LR row y) writes the S HR rows S*y .. S*y+S-1:
+//   1. vertical pass of the S rows from the LR frame (L2-resident) -> SMEM [S][W] float4, and the
+//      owner row of their MB row -> SMEM
+//   2. horizontal pass: a thread per (HR row, pair of LR columns) computes their 2*S HR pixels
+//      (6*S values, a whole number of 32-bit words, consecutive threads -> consecutive words: no
+//      bank conflicts) into an SMEM copy of the output rows. D10 weights per sub-pixel phase are
+//      compile-time: HR pixel X = S*x + j samples src = x + (j + 0.5)/S - 0.5, i.e. columns
+//      (x-1, x) or (x, x+1) with a fixed fraction, clamped at the edges exactly as the oracle.
+//   3. copy-out in coalesced 16-B chunks (an MB's HR square is a whole number of chunks), skipping
+//      the chunks of owned MBs; those get the owner box's HR bin pixels (SKIP = false) or nothing
+//      (SKIP: regen_enhance_scatter wrote them already).
+constexpr int SC_THREADS = 256;
+
+template <int S>
+struct Phase {   // sub-pixel phase j: source offset d (-1 or 0) and fraction
+  __host__ __device__ static constexpr int d(int j) { return 2 * j + 1 < S ? -1 : 0; }
+  __host__ __device__ static constexpr float f(int j) {
+    return 2 * j + 1 < S ? (float)(1.0 + ((j + 0.5) / S - 0.5)) : (float)((j + 0.5) / S - 0.5);
+  }
+};
+
+template <typename TO>
+__device__ __forceinline__ void put2(uint32_t* w, int k, float a, float b);
+template <>
+__device__ __forceinline__ void put2<__nv_bfloat16>(uint32_t* w, int k, float a, float b) { w[k] = pack_bf16(a, b); }
+template <>
+__device__ __forceinline__ void put2<float>(uint32_t* w, int k, float a, float b) {
+  w[2 * k] = __float_as_uint(a);
+  w[2 * k + 1] = __float_as_uint(b);
+}
+
+template <int S, typename TH, typename TO, bool SKIP>
+__global__ void __launch_bounds__(SC_THREADS) scatter_rows_kernel(ScatterArgs a) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int64_t sf = blockIdx.y;
+  const int y = blockIdx.x;
+  const int W = a.W, W3 = W * 3;
+  const int npair = (W + 1) / 2;
+  constexpr int WPP = 3 * S * (int)sizeof(TO) / 2;                            // 32-bit words per column pair
+  const int row_words = (npair * WPP + 3) / 4 * 4;                            // staging row (16-B multiple)
+  float4* vr = reinterpret_cast<float4*>(sm);                                 // [S][W]
+  uint32_t* orow = reinterpret_cast<uint32_t*>(vr + S * W);                   // [S][row_words]
+  int32_t* own = reinterpret_cast<int32_t*>(orow + S * row_words);            // [GW]
+  const uint8_t* img = a.frames + sf * (int64_t)a.H * W3;
+  const int my = y / a.mb;   // MB row of all S HR rows
+  for (int j = threadIdx.x; j < a.GW; j += SC_THREADS) own[j] = a.owner[(sf * a.GH + my) * a.GW + j];
+  // ---- 1. vertical pass (D10) for the S rows
+#pragma unroll
+  for (int i = 0; i < S; ++i) {
+    int yl0 = y + Phase<S>::d(i);
+    float ly = Phase<S>::f(i);
+    if (yl0 < 0) { yl0 = 0; ly = 0.f; }
     const int yl1 = min(yl0 + 1, a.H - 1);
-    const float ly = sy - (float)yl0;
-    const uint8_t* r0 = img + ((size_t)yl0 * a.W + xa_blk) * 3;
-    const uint8_t* r1 = img + ((size_t)yl1 * a.W + xa_blk) * 3;
-    const int n = (xb_blk - xa_blk + 1) * 3;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const float p0 = (float)r0[i], p1 = (float)r1[i];
-      vrow[i] = fmaf(ly, p1 - p0, p0);
+    if (yl1 == yl0) ly = 0.f;
+    const uint8_t* r0 = img + (size_t)yl0 * W3;
+    const uint8_t* r1 = img + (size_t)yl1 * W3;
+    for (int x = threadIdx.x; x < W; x += SC_THREADS) {
+      float4 v;
+      float p0 = (float)__ldg(r0 + 3 * x), p1 = (float)__ldg(r1 + 3 * x);
+      v.x = fmaf(ly, p1 - p0, p0);
+      p0 = (float)__ldg(r0 + 3 * x + 1); p1 = (float)__ldg(r1 + 3 * x + 1);
+      v.y = fmaf(ly, p1 - p0, p0);
+      p0 = (float)__ldg(r0 + 3 * x + 2); p1 = (float)__ldg(r1 + 3 * x + 2);
+      v.z = fmaf(ly, p1 - p0, p0);
+      v.w = 0.f;
+      vr[i * W + x] = v;
     }
   }
   __syncthreads();
-  if (X0 >= a.OW) return;
-  float o[24];
-  // the 8 pixels lie in one MB column (16*s is a multiple of 8), so one owner lookup serves them all
-  const int32_t b = a.owner[(sf * a.GH + Y / (a.mb * a.s)) * a.GW + X0 / (a.mb * a.s)];
-  if (b >= 0) {
-    const regen_box* bp = a.boxes + b;
-    const int x0 = bp->x0, y0 = bp->y0, hh = bp->h, bin = bp->bin, bbx = bp->bx, bby = bp->by, rot = bp->rotated;
-    const int HW = a.s * a.bin_w, HH = a.s * a.bin_h;
-    const int u0 = X0 - a.s * x0, v = Y - a.s * y0;
-    const TH* hb = (const TH*)a.hr + (size_t)bin * HH * HW * 4;
-    // 8 B per pixel (4 channels); one 8-B load per pixel
-    const TH* src = !rot ? hb + ((size_t)(a.s * bby + v) * HW + a.s * bbx + u0) * 4
-                         : hb + ((size_t)(a.s * bby + u0) * HW + a.s * bbx + (a.s * hh - 1 - v)) * 4;
-    const size_t step = !rot ? 4 : (size_t)HW * 4;   // rotated 90 deg CW: box-local (u, v) <- bin (s*h-1-v, u)
-    if (sizeof(TH) == 2) {
-      uint2 q[8];
+  // ---- 2. horizontal pass into the SMEM output rows
 #pragma unroll
-      for (int k = 0; k < 8; ++k) q[k] = *reinterpret_cast<const uint2*>(src + (size_t)k * step);
+  for (int i = 0; i < S; ++i) {
+    const float4* vrow = vr + i * W;
+    uint32_t* orw = orow + i * row_words;
+    for (int t = threadIdx.x; t < npair; t += SC_THREADS) {
+      const int x0 = 2 * t;
+      float4 v[4];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const float2 f01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&q[k].x));
-        const float2 f23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&q[k].y));
-        o[3 * k] = f01.x;
-        o[3 * k + 1] = f01.y;
-        o[3 * k + 2] = f23.x;
+      for (int q = 0; q < 4; ++q) v[q] = vrow[min(max(x0 - 1 + q, 0), W - 1)];
+      float o[6 * S];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int x = x0 + q;
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+          float4 A, B;
+          float lx = Phase<S>::f(j);
+          if (Phase<S>::d(j) < 0) {
+            A = v[q]; B = v[q + 1];
+            if (x == 0) { lx = 0.f; A = v[q + 1]; }   // src < 0 clamps to column 0
+          } else {
+            A = v[q + 1]; B = v[q + 2];
+            if (x >= W - 1) lx = 0.f;                 // last column: i1 = i0
+          }
+          const int e = 3 * (q * S + j);
+          o[e] = fmaf(lx, B.x - A.x, A.x) * (1.0f / 255.0f);
+          o[e + 1] = fmaf(lx, B.y - A.y, A.y) * (1.0f / 255.0f);
+          o[e + 2] = fmaf(lx, B.z - A.z, A.z) * (1.0f / 255.0f);
+        }
       }
-    } else {
+      uint32_t w[WPP];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const float4 f = *reinterpret_cast<const float4*>(src + (size_t)k * step);
-        o[3 * k] = f.x;
-        o[3 * k + 1] = f.y;
-        o[3 * k + 2] = f.z;
-      }
-    }
-  } else {
-    // horizontal pass over the block's vertically interpolated LR row segment (SMEM)
+      for (int k = 0; k < 3 * S; ++k) put2<TO>(w, k, o[2 * k], o[2 * k + 1]);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float sx = fmaxf(((float)(X0 + k) + 0.5f) * a.inv_s - 0.5f, 0.0f);
-      const int xl0 = min((int)sx, a.W - 1);
-      const int xl1 = min(xl0 + 1, a.W - 1);
-      const float lx = sx - (float)xl0;
-      const float* v0 = vrow + 3 * (xl0 - xa_blk);
-      const float* v1 = vrow + 3 * (xl1 - xa_blk);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) o[3 * k + c] = fmaf(lx, v1[c] - v0[c], v0[c]) * (1.0f / 255.0f);
+      for (int k = 0; k < WPP; ++k) orw[t * WPP + k] = w[k];
     }
   }
-  TO* dst = (TO*)a.out + ((sf * a.OH + Y) * (int64_t)a.OW + X0) * 3;
-  if (X0 + 8 <= a.OW && ((((uintptr_t)dst) & 15) == 0)) {
-    if (sizeof(TO) == 2) {
-      uint4 v[3];
-      uint32_t* w = (uint32_t*)v;
+  __syncthreads();
+  // ---- 3. copy-out
+  constexpr int MB_BYTES = 16 * S * 3 * (int)sizeof(TO);     // HR width of an MB in bytes (mb = 16)
+  static_assert(MB_BYTES % 16 == 0, "MB squares must be whole 16-B chunks");
+  const int row_bytes = a.OW * 3 * (int)sizeof(TO);
+  const int n16 = row_bytes / 16;
 #pragma unroll
-      for (int i = 0; i < 12; ++i) {
-        __nv_bfloat162 h = __floats2bfloat162_rn(o[2 * i], o[2 * i + 1]);
-        w[i] = *(uint32_t*)&h;
+  for (int i = 0; i < S; ++i) {
+    const int Y = y * S + i;
+    uint8_t* drow = (uint8_t*)a.out + ((sf * a.OH + Y) * (int64_t)a.OW) * 3 * sizeof(TO);
+    const uint8_t* srow = reinterpret_cast<const uint8_t*>(orow + i * row_words);
+    if ((((uintptr_t)drow) & 15) == 0) {
+      for (int c = threadIdx.x; c < n16; c += SC_THREADS) {
+        if (own[(c * 16) / MB_BYTES] >= 0) continue;
+        *reinterpret_cast<uint4*>(drow + 16 * c) = *reinterpret_cast<const uint4*>(srow + 16 * c);
       }
-      uint4* d = (uint4*)dst;
-      d[0] = v[0]; d[1] = v[1]; d[2] = v[2];
+      for (int c = n16 * 16 + threadIdx.x; c < row_bytes; c += SC_THREADS)
+        if (own[c / MB_BYTES] < 0) drow[c] = srow[c];
     } else {
-      float4* d = (float4*)dst;
-#pragma unroll
-      for (int i = 0; i < 6; ++i) d[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+      for (int c = threadIdx.x; c < row_bytes / 2; c += SC_THREADS)
+        if (own[(2 * c) / MB_BYTES] < 0) reinterpret_cast<uint16_t*>(drow)[c] = reinterpret_cast<const uint16_t*>(srow)[c];
     }
-  } else {
-    for (int k = 0; k < 8 && X0 + k < a.OW; ++k)
-      for (int c = 0; c < 3; ++c) {
-        if (sizeof(TO) == 2) ((__nv_bfloat16*)dst)[3 * k + c] = __float2bfloat16_rn(o[3 * k + c]);
-        else ((float*)dst)[3 * k + c] = o[3 * k + c];
+  }
+  if (SKIP) return;
+  // ---- owned MBs: the box's HR bin pixels (un-rotated, D7), 8 pixels per thread
+  const int HW = S * a.bin_w, HH = S * a.bin_h;
+  const int nchunk = (a.OW + 7) / 8;
+  for (int t = threadIdx.x; t < S * nchunk; t += SC_THREADS) {
+    const int i = t / nchunk, c = t - i * nchunk;
+    const int Y = y * S + i;
+    const int X0 = c * 8;
+    const int32_t b = own[X0 / (16 * S)];   // the 8 pixels lie in one MB column (16*S is a multiple of 8)
+    if (b < 0) continue;
+    const regen_box* bp = a.boxes + b;
+    const int x0 = bp->x0, y0 = bp->y0, hh = bp->h, bin = bp->bin, bbx = bp->bx, bby = bp->by, rot = bp->rotated;
+    const int u0 = X0 - S * x0, v = Y - S * y0;
+    const TH* hb = (const TH*)a.hr + (size_t)bin * HH * HW * 4;
+    // rotated 90 deg CW: box-local (u, v) <- bin (S*h-1-v, u)
+    const TH* src = !rot ? hb + ((size_t)(S * bby + v) * HW + S * bbx + u0) * 4
+                         : hb + ((size_t)(S * bby + u0) * HW + S * bbx + (S * hh - 1 - v)) * 4;
+    const size_t step = !rot ? 4 : (size_t)HW * 4;
+    TO* dst = (TO*)a.out + ((sf * a.OH + Y) * (int64_t)a.OW + X0) * 3;
+    for (int k = 0; k < 8 && X0 + k < a.OW; ++k) {
+      float f0, f1, f2;
+      if (sizeof(TH) == 2) {
+        const uint2 q = *reinterpret_cast<const uint2*>(src + (size_t)k * step);
+        const float2 f01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&q.x));
+        const float2 f23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&q.y));
+        f0 = f01.x; f1 = f01.y; f2 = f23.x;
+      } else {
+        const float4 f = *reinterpret_cast<const float4*>(src + (size_t)k * step);
+        f0 = f.x; f1 = f.y; f2 = f.z;
       }
+      if (sizeof(TO) == 2) {
+        ((__nv_bfloat16*)dst)[3 * k] = __float2bfloat16_rn(f0);
+        ((__nv_bfloat16*)dst)[3 * k + 1] = __float2bfloat16_rn(f1);
+        ((__nv_bfloat16*)dst)[3 * k + 2] = __float2bfloat16_rn(f2);
+      } else {
+        ((float*)dst)[3 * k] = f0;
+        ((float*)dst)[3 * k + 1] = f1;
+        ((float*)dst)[3 * k + 2] = f2;
+      }
+    }
   }
 }
 
@@ -129,18 +206,11 @@ __global__ void __launch_bounds__(128) scatter_kernel(ScatterArgs a) {
 
 using namespace regen;
 
-extern "C" regen_status regen_scatter_blend(const regen_geom* geom, const regen_pack_params* p, int32_t scale,
-                                            const uint8_t* d_frames, const regen_box* d_boxes,
-                                            const int32_t* d_mb_owner, const void* d_hr_bins, int32_t hr_dtype,
-                                            void* d_out, int32_t out_dtype, void* stream) {
-  regen_status st = validate_geom(geom);
-  if (st != REGEN_OK) return st;
-  REGEN_REQUIRE(p != nullptr, "pack params null");
-  REGEN_REQUIRE(scale >= 2 && scale <= 8, "scale must be in [2, 8]");
-  REGEN_REQUIRE(hr_dtype == REGEN_DTYPE_BF16 || hr_dtype == REGEN_DTYPE_FP32, "bad hr dtype");
-  REGEN_REQUIRE(out_dtype == REGEN_DTYPE_BF16 || out_dtype == REGEN_DTYPE_FP32, "bad out dtype");
-  REGEN_REQUIRE(d_frames && d_boxes && d_mb_owner && d_hr_bins && d_out, "null device pointer");
-  const regen_geom g = *geom;
+namespace regen {
+
+regen_status scatter_launch(const regen_geom& g, const regen_pack_params& p, int scale, const uint8_t* d_frames,
+                            const regen_box* d_boxes, const int32_t* d_mb_owner, const void* d_hr_bins, int hr_dtype,
+                            void* d_out, int out_dtype, bool skip_owned, cudaStream_t s) {
   ScatterArgs a;
   a.frames = d_frames;
   a.boxes = d_boxes;
@@ -155,18 +225,54 @@ extern "C" regen_status regen_scatter_blend(const regen_geom* geom, const regen_
   a.GH = grid_h(g);
   a.mb = g.mb;
   a.s = scale;
-  a.bin_w = p->bin_w;
-  a.bin_h = p->bin_h;
+  a.bin_w = p.bin_w;
+  a.bin_h = p.bin_h;
   a.inv_s = 1.0f / (float)scale;
-  dim3 grid((unsigned)((a.OW + 8 * 128 - 1) / (8 * 128)), (unsigned)a.OH, (unsigned)n_frames(g));
-  cudaStream_t s = (cudaStream_t)stream;
-  if (hr_dtype == REGEN_DTYPE_BF16) {
-    if (out_dtype == REGEN_DTYPE_BF16) scatter_kernel<__nv_bfloat16, __nv_bfloat16><<<grid, 128, 0, s>>>(a);
-    else scatter_kernel<__nv_bfloat16, float><<<grid, 128, 0, s>>>(a);
-  } else {
-    if (out_dtype == REGEN_DTYPE_BF16) scatter_kernel<float, __nv_bfloat16><<<grid, 128, 0, s>>>(a);
-    else scatter_kernel<float, float><<<grid, 128, 0, s>>>(a);
+  a.skip_owned = skip_owned ? 1 : 0;
+  dim3 grid((unsigned)g.frame_h, (unsigned)n_frames(g));
+  REGEN_REQUIRE(g.mb == 16, "scatter expects 16-pixel MBs");
+  REGEN_REQUIRE(scale == 2 || scale == 3 || scale == 4, "scatter scale must be 2, 3 or 4");
+  const size_t es = out_dtype == REGEN_DTYPE_BF16 ? 2 : 4;
+  const size_t npair = ((size_t)g.frame_w + 1) / 2;
+  const size_t row_words = (npair * 3 * scale * es / 2 + 3) / 4 * 4;
+  const size_t smem = (size_t)g.frame_w * 16 * scale + (size_t)scale * row_words * 4 + (size_t)a.GW * 4 + 16;
+  REGEN_REQUIRE(smem <= 200 * 1024, "frame too wide for the scatter kernel (%zu B SMEM)", smem);
+  auto go = [&](auto kern) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, SC_THREADS, smem, s>>>(a);
+  };
+  const bool bf_hr = hr_dtype == REGEN_DTYPE_BF16, bf_out = out_dtype == REGEN_DTYPE_BF16;
+  using bf = __nv_bfloat16;
+#define SC_DISPATCH(S_)                                                              \
+  if (skip_owned) {                                                                  \
+    if (bf_out) go(scatter_rows_kernel<S_, bf, bf, true>);                           \
+    else go(scatter_rows_kernel<S_, bf, float, true>);                               \
+  } else if (bf_hr) {                                                                \
+    if (bf_out) go(scatter_rows_kernel<S_, bf, bf, false>);                          \
+    else go(scatter_rows_kernel<S_, bf, float, false>);                              \
+  } else {                                                                           \
+    if (bf_out) go(scatter_rows_kernel<S_, float, bf, false>);                       \
+    else go(scatter_rows_kernel<S_, float, float, false>);                           \
   }
+  if (scale == 2) { SC_DISPATCH(2) } else if (scale == 3) { SC_DISPATCH(3) } else { SC_DISPATCH(4) }
+#undef SC_DISPATCH
   REGEN_LAUNCH_CHECK();
   return REGEN_OK;
+}
+
+}  // namespace regen
+
+extern "C" regen_status regen_scatter_blend(const regen_geom* geom, const regen_pack_params* p, int32_t scale,
+                                            const uint8_t* d_frames, const regen_box* d_boxes,
+                                            const int32_t* d_mb_owner, const void* d_hr_bins, int32_t hr_dtype,
+                                            void* d_out, int32_t out_dtype, void* stream) {
+  regen_status st = validate_geom(geom);
+  if (st != REGEN_OK) return st;
+  REGEN_REQUIRE(p != nullptr, "pack params null");
+  REGEN_REQUIRE(scale >= 2 && scale <= 4, "scale must be 2, 3 or 4");
+  REGEN_REQUIRE(hr_dtype == REGEN_DTYPE_BF16 || hr_dtype == REGEN_DTYPE_FP32, "bad hr dtype");
+  REGEN_REQUIRE(out_dtype == REGEN_DTYPE_BF16 || out_dtype == REGEN_DTYPE_FP32, "bad out dtype");
+  REGEN_REQUIRE(d_frames && d_boxes && d_mb_owner && d_hr_bins && d_out, "null device pointer");
+  return scatter_launch(*geom, *p, scale, d_frames, d_boxes, d_mb_owner, d_hr_bins, hr_dtype, d_out, out_dtype, false,
+                        (cudaStream_t)stream);
 }

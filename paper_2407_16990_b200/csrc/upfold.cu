@@ -43,18 +43,41 @@ __host__ __device__ constexpr int block_off(int ny, int nx, int p) {
 }
 __host__ __device__ constexpr int n_channels(int p) { return 3 * (p + 2) * (p + 2); }
 
-template <int PS, typename TO>
-__global__ void __launch_bounds__(128) combine_kernel(const __nv_bfloat16* P, TO* out, const uint32_t* mbits,
+// Where the combined HR pixels go. BINS: the HR bin layout [bin][PS*Hr][PS*Wr][4] of
+// regen_enhance_packed. FRAME (regen_enhance_scatter): straight into the HR frames
+// [S][F][s*H][s*W][3], for owned selected MBs only (the scatter pass writes every other pixel).
+struct FrameOut {
+  const int32_t* map;        // [bin][bin_h][bin_w] LR bin pixel -> covering box, -1 outside boxes
+  const uint8_t* own8;       // [bin][bin_h][bin_w] 1: the pixel's source MB is owned by its box
+  const regen_box* boxes;
+  const int32_t* owner;      // [S][F][GH][GW]
+  void* out;
+  int out_fp32;
+  int F, W, H, GW, GH, mb, s;
+};
+
+template <int PS, bool FRAME>
+__global__ void __launch_bounds__(128) combine_kernel(const __nv_bfloat16* P, __nv_bfloat16* out, const uint32_t* mbits,
                                                       const float* bt, const int32_t* num_bins, int Wr, int Hr,
-                                                      int res, int bin_w, int bin_h, int c8) {
+                                                      int res, int bin_w, int bin_h, int c8, FrameOut fo) {
   const int bin = blockIdx.z;
   if (bin >= *num_bins) return;
   const int y = blockIdx.y;
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= Wr) return;
   const int words = (bin_w + 31) / 32;
-  const int xl = x / res;
-  const bool occ = (__ldg(mbits + ((size_t)bin * bin_h + y / res) * words + xl / 32) >> (xl & 31)) & 1u;
+  const int xl = x / res, yl = y / res;
+  // FRAME: only pixels whose source MB is owned by their box (the scatter pass writes the rest)
+  regen_box bx;
+  bool occ;
+  if (FRAME) {
+    const size_t lpx = ((size_t)bin * bin_h + yl) * bin_w + xl;
+    if (!__ldg(fo.own8 + lpx)) return;
+    bx = fo.boxes[__ldg(fo.map + lpx)];
+    occ = true;
+  } else {
+    occ = (__ldg(mbits + ((size_t)bin * bin_h + yl) * words + xl / 32) >> (xl & 31)) & 1u;
+  }
   float acc[PS][PS][3];
 #pragma unroll
   for (int i = 0; i < PS; ++i)
@@ -71,8 +94,6 @@ __global__ void __launch_bounds__(128) combine_kernel(const __nv_bfloat16* P, TO
         const int yy = y + ny, xx = x + nx;
         if (yy < 0 || yy >= Hr || xx < 0 || xx >= Wr) continue;   // zero padding at the bin edge
         const __nv_bfloat16* base = P + ((size_t)bin * Hr + yy) * c8 * pstride + (size_t)xx * 8;
-        constexpr int dummy = 0;
-        (void)dummy;
         const int off = block_off(ny, nx, PS), ci = cnt(ny, PS), cj = cnt(nx, PS);
         const int pl0 = off / 8, pl1 = (off + ci * cj * 3 - 1) / 8;
 #pragma unroll
@@ -97,23 +118,46 @@ __global__ void __launch_bounds__(128) combine_kernel(const __nv_bfloat16* P, TO
       }
   }
   const float b0 = __ldg(bt), b1 = __ldg(bt + 1), b2 = __ldg(bt + 2);
-  const int WO = Wr * PS;
+  if (!FRAME) {
+    const int WO = Wr * PS;
 #pragma unroll
-  for (int i = 0; i < PS; ++i) {
-    TO* o = out + (((size_t)bin * Hr * PS + (size_t)y * PS + i) * WO + (size_t)x * PS) * 4;
+    for (int i = 0; i < PS; ++i) {
+      __nv_bfloat16* o = out + (((size_t)bin * Hr * PS + (size_t)y * PS + i) * WO + (size_t)x * PS) * 4;
 #pragma unroll
-    for (int j = 0; j < PS; ++j) {
-      const float r0 = occ ? acc[i][j][0] + b0 : 0.f, r1 = occ ? acc[i][j][1] + b1 : 0.f,
-                  r2 = occ ? acc[i][j][2] + b2 : 0.f;
-      if (sizeof(TO) == 2) {
+      for (int j = 0; j < PS; ++j) {
         uint2 w;
-        w.x = pack_bf16x2(r0, r1);
-        w.y = pack_bf16x2(r2, 0.f);
+        w.x = pack_bf16x2(occ ? acc[i][j][0] + b0 : 0.f, occ ? acc[i][j][1] + b1 : 0.f);
+        w.y = pack_bf16x2(occ ? acc[i][j][2] + b2 : 0.f, 0.f);
         *reinterpret_cast<uint2*>(o + 4 * j) = w;
-      } else {
-        *reinterpret_cast<float4*>(o + 4 * j) = make_float4(r0, r1, r2, 0.f);
       }
     }
+  } else {
+    // bin HR pixel (X', Y') -> box-local (u, v) (un-rotate, D7) -> frame HR pixel (s*x0 + u, s*y0 + v);
+    // values rounded to bf16 first (bit-identical to the HR-bin round trip of the separate calls)
+    const int s = fo.s, OW = fo.W * s, OH = fo.H * s;
+    const size_t fbase = ((size_t)bx.stream * fo.F + bx.frame) * (size_t)OH * OW;
+#pragma unroll
+    for (int i = 0; i < PS; ++i)
+#pragma unroll
+      for (int j = 0; j < PS; ++j) {
+        const int Xb = PS * x + j - s * bx.bx, Yb = PS * y + i - s * bx.by;   // box-footprint-local HR
+        const int u = bx.rotated ? Yb : Xb;
+        const int v = bx.rotated ? s * bx.h - 1 - Xb : Yb;
+        const size_t px = fbase + (size_t)(s * bx.y0 + v) * OW + (size_t)(s * bx.x0 + u);
+        const __nv_bfloat16 c0 = __float2bfloat16_rn(acc[i][j][0] + b0), c1 = __float2bfloat16_rn(acc[i][j][1] + b1),
+                            c2 = __float2bfloat16_rn(acc[i][j][2] + b2);
+        if (fo.out_fp32) {
+          float* o = (float*)fo.out + px * 3;
+          o[0] = __bfloat162float(c0);
+          o[1] = __bfloat162float(c1);
+          o[2] = __bfloat162float(c2);
+        } else {
+          __nv_bfloat16* o = (__nv_bfloat16*)fo.out + px * 3;
+          o[0] = c0;
+          o[1] = c1;
+          o[2] = c2;
+        }
+      }
   }
 }
 
@@ -186,7 +230,8 @@ void fold_prepare(SRNet* net, std::vector<float>& w32) {
 }
 
 regen_status fold_combine_launch(const SRNet* net, const void* P, void* hr_bins, const uint32_t* mbits, int max_bins,
-                                 const int32_t* d_num_bins, int bin_w, int bin_h, cudaStream_t s) {
+                                 const int32_t* d_num_bins, int bin_w, int bin_h, cudaStream_t s,
+                                 const FoldFrameArgs* fa) {
   const ConvDesc& d = net->convs[net->fold_conv];
   const ConvDesc& up = net->convs[net->fold_conv - 2];
   const ConvDesc& tail = net->convs[net->fold_conv - 1];
@@ -197,12 +242,33 @@ regen_status fold_combine_launch(const SRNet* net, const void* P, void* hr_bins,
   const float* bt = net->d_w32 + tail.b_off;
   const __nv_bfloat16* Pb = (const __nv_bfloat16*)P;
   __nv_bfloat16* o = (__nv_bfloat16*)hr_bins;
-  if (p == 2)
-    fold::combine_kernel<2, __nv_bfloat16><<<grid, 128, 0, s>>>(Pb, o, mbits, bt, d_num_bins, Wr, Hr, res, bin_w, bin_h, c8);
-  else if (p == 3)
-    fold::combine_kernel<3, __nv_bfloat16><<<grid, 128, 0, s>>>(Pb, o, mbits, bt, d_num_bins, Wr, Hr, res, bin_w, bin_h, c8);
-  else
+  fold::FrameOut fo;
+  memset(&fo, 0, sizeof(fo));
+  if (fa) {
+    fo.map = fa->map;
+    fo.own8 = fa->own8;
+    fo.boxes = fa->boxes;
+    fo.owner = fa->owner;
+    fo.out = fa->out;
+    fo.out_fp32 = fa->out_dtype == REGEN_DTYPE_FP32;
+    fo.F = fa->geom.F;
+    fo.W = fa->geom.frame_w;
+    fo.H = fa->geom.frame_h;
+    fo.GW = grid_w(fa->geom);
+    fo.GH = grid_h(fa->geom);
+    fo.mb = fa->geom.mb;
+    fo.s = net->cfg.scale;
+  }
+#define LAUNCH(PS_, FR_) \
+  fold::combine_kernel<PS_, FR_><<<grid, 128, 0, s>>>(Pb, o, mbits, bt, d_num_bins, Wr, Hr, res, bin_w, bin_h, c8, fo)
+  if (p == 2) {
+    if (fa) LAUNCH(2, true); else LAUNCH(2, false);
+  } else if (p == 3) {
+    if (fa) LAUNCH(3, true); else LAUNCH(3, false);
+  } else {
     REGEN_REQUIRE(false, "fold: unsupported pixel-shuffle factor %d", p);
+  }
+#undef LAUNCH
   REGEN_LAUNCH_CHECK();
   return REGEN_OK;
 }

@@ -144,7 +144,10 @@ def _check_pixels(wl, seed=5, kind="blobs", box_sample=None, frame_sample=None):
     fr = synth.frames_rgb8(wl.S, wl.F, wl.H, wl.W, seed)
     w = synth.sr_weights(wl.sr, seed)
     p = _pipeline(wl, w)
-    out = p.run(torch.from_numpy(imp).cuda(), torch.from_numpy(fr).cuda())
+    imp_t, fr_t = torch.from_numpy(imp).cuda(), torch.from_numpy(fr).cuda()
+    out = p.run(imp_t, fr_t, fused=False).clone()            # regen_enhance_packed + regen_scatter_blend
+    out_fused = p.run(imp_t, fr_t, out=torch.empty_like(out))  # regen_enhance_scatter
+    assert torch.equal(out_fused, out), "regen_enhance_scatter differs from the separate calls"
     g = p.host_results()
     o = _oracle_index(wl, imp)
     _assert_index_equal(g, o)

@@ -1,3 +1,3 @@
-for d in 0 3 7; do echo "== dbg $d"; REGEN_RB_DBG=$d python tools/kernel_times.py --steps 3 2>&1 | grep -E "resblock|total"; done
-python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-REGEN_TC_PROF=1 python tools/kernel_times.py --steps 1 2>&1 | grep rb-prof | head -2
+python -m pytest tests -m gpu -x -q 2>&1 | tail -4
+python tools/kernel_times.py --steps 3 2>&1 | tail -12
+python bench.py --steps 20 --warmup 5 2>&1 | tail -1 | head -c 300
