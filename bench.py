@@ -48,6 +48,15 @@ def sr_flops_per_lr_px(sr: synth.SRConfig) -> int:
     return f
 
 
+def load_traffic(kernel: str):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            return json.load(fh)["kernels"].get(kernel)
+    except Exception:
+        return None
+
+
 def load_peaks() -> dict:
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -59,56 +68,71 @@ def load_peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled DURING the timed region."""
+    """SM clock and throttle reasons sampled DURING the timed region: NVML polled every ~0.5 ms from
+    a thread (nvidia-smi's 100 ms loop would see a 30 ms region once or never); nvidia-smi fallback."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
-        self.proc = None
-        self.lines: list[str] = []
+        self.sm: list[float] = []
+        self.mask = 0
+        self.max_mhz = None
+        self.stop = threading.Event()
+        self.t = None
+        self.nv = None
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                          "-lms", "100", "-i", str(self.gpu)], stdout=subprocess.PIPE,
-                                         stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+            self.sample()
+            self.t = threading.Thread(target=self._loop, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.nv = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def sample(self):
+        nv = self.nv
+        self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+        self.mask |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+
+    def _loop(self):
+        while not self.stop.is_set():
+            try:
+                self.sample()
+            except Exception:
+                return
+            time.sleep(0.0005)
 
     def __exit__(self, *a):
-        if self.proc is not None:
-            self.proc.terminate()
+        self.stop.set()
+        if self.t is not None:
+            self.t.join(timeout=2)
+        if self.nv is not None:
             try:
-                self.proc.wait(timeout=5)
+                self.sample()
             except Exception:
-                self.proc.kill()
+                pass
+        else:   # fallback: one nvidia-smi reading right after the region
+            try:
+                out = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,clocks.max.sm", "--format=csv,noheader,nounits",
+                                      "-i", str(self.gpu)], capture_output=True, text=True, timeout=20).stdout
+                sm, mx = (float(v) for v in out.strip().split(","))
+                self.sm.append(sm)
+                self.max_mhz = mx
+            except Exception:
+                pass
 
     def summary(self) -> dict:
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[4:8]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        reasons = sorted(k for k, bit in self.REASONS.items() if self.mask & bit)
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.sm),
+                "source": "nvml" if self.nv is not None else "nvidia-smi after the region"}
 
 
 # --------------------------------------------------------------------------------- reference arm
@@ -236,7 +260,7 @@ def main() -> None:
 
     # instrumented step (serial, L2 flushed before it): per-stage device time for the breakdown and
     # the roofline of the SR stage
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
 
     def step_instrumented():
         ev[0].record(stream)
@@ -244,19 +268,18 @@ def main() -> None:
         ev[1].record(stream)
         p.pack_step(imp)
         ev[2].record(stream)
-        p.enhance(fr)
+        p.enhance_scatter(fr)
         ev[3].record(stream)
-        p.scatter(fr)
-        ev[4].record(stream)
 
     front_done = [torch.cuda.Event() for _ in range(2)]
     back_done = [torch.cuda.Event() for _ in range(2)]
 
-    def pipelined_steps(n_steps: int):
+    def pipelined_steps(n_steps: int, capturing: bool = False):
         for k in range(n_steps):
             q = pipes[k % 2]
             with torch.cuda.stream(s_front):
-                s_front.wait_event(back_done[k % 2])        # buffers of batch k-2 are free
+                if not (capturing and k < 2):
+                    s_front.wait_event(back_done[k % 2])    # buffers of batch k-2 are free
                 q.select(imp, stream=s_front)
                 q.pack_step(imp, stream=s_front)
                 front_done[k % 2].record(s_front)
@@ -279,13 +302,13 @@ def main() -> None:
     flops_step = box_px * sr_flops_per_lr_px(wl.sr)
     frames_step = wl.S * wl.F
 
-    stage = np.zeros(4)
+    stage = np.zeros(3)
     n_instr = min(args.steps, 5)
     for _ in range(n_instr):
         flush.zero_()
         step_instrumented()
         torch.cuda.synchronize()
-        stage += [ev[i].elapsed_time(ev[i + 1]) for i in range(4)]
+        stage += [ev[i].elapsed_time(ev[i + 1]) for i in range(3)]
     stage /= n_instr
     # warm the pipelined schedule
     s_front.wait_stream(stream)
@@ -293,20 +316,68 @@ def main() -> None:
     pipelined_steps(max(args.warmup, 2))
     torch.cuda.synchronize()
 
+    # The K timed steps are one CUDA graph (captured once, replayed): no host launch overhead between
+    # the ~50 kernels of a step. A warm replay with every libregen launch bracketed by CUDA events on
+    # its own stream (regen_trace_*) gives the per-kernel table and names the dominant kernel; in the
+    # timed replay only the dominant kernel's launches are bracketed (its live device time for the
+    # roofline) so the event nodes barely perturb the step.
+    def capture(n_steps: int, trace_prefix):
+        if trace_prefix is not None:
+            rg.trace_filter(trace_prefix or None)
+            rg.trace_enable(True)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cap):
+            s_front.wait_stream(cap)
+            s_back.wait_stream(cap)
+            pipelined_steps(n_steps, capturing=True)
+            cap.wait_stream(s_front)
+            cap.wait_stream(s_back)
+        rg.trace_enable(False)
+        rg.trace_filter(None)
+        return g
+
+    graph = None
+    rg.trace_read()
+    kern_all = {}
+    if not args.no_graph:
+        cap = torch.cuda.Stream(dev)
+        warm = capture(max(args.warmup, 3), "")     # all kernels traced
+        warm.replay()
+        torch.cuda.synchronize()
+        for name, ms in rg.trace_read():
+            k = kern_all.setdefault(name, [0, 0.0])
+            k[0] += 1
+            k[1] += ms
+        n_warm = max(args.warmup, 3)
+        dom_name = max(kern_all.items(), key=lambda kv: kv[1][1])[0]
+        graph = capture(args.steps, dom_name)   # its trace records are read after the timed replay
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if graph is None:
+        rg.trace_enable(True)
     with ClockSampler(local) as clk:
         t0.record(stream)
-        s_front.wait_stream(stream)
-        s_back.wait_stream(stream)
-        pipelined_steps(args.steps)
-        stream.wait_stream(s_front)
-        stream.wait_stream(s_back)
+        if graph is not None:
+            graph.replay()
+        else:
+            s_front.wait_stream(stream)
+            s_back.wait_stream(stream)
+            pipelined_steps(args.steps)
+            stream.wait_stream(s_front)
+            stream.wait_stream(s_back)
         t1.record(stream)
         torch.cuda.synchronize()
+    rg.trace_enable(False)
+    trace = rg.trace_read()
     total_ms = t0.elapsed_time(t1)
+    kern = {}
+    for name, ms in trace:
+        k = kern.setdefault(name, [0, 0.0])
+        k[0] += 1
+        k[1] += ms
     if world > 1:
         dist.barrier()
     frames = frames_step * args.steps
@@ -345,11 +416,37 @@ def main() -> None:
         e2e_t = float(t.item())
     e2e_val = frames_step * world / (e2e_t / 1000.0)
 
+    if not kern_all:   # no graph: the timed region itself traced every kernel
+        kern_all, n_warm = kern, args.steps
     if rank == 0:
         peaks = load_peaks()
-        enh_ms = stage[2]
-        achieved = flops_step / (enh_ms / 1000.0) / 1e12
+        # dominant kernel = largest share of the summed device time (warm traced replay); its live
+        # launch times come from the timed region
+        dom = max(kern.items(), key=lambda kv: kv[1][1])[0]
+        dom_n, dom_ms_total = kern[dom]
+        dom_ms = dom_ms_total / dom_n
+        C = wl.sr.channels
+        per_px = {"resblock": 2 * 2 * 9 * C * C, "conv_res_a": 2 * 9 * C * C, "conv_res_b": 2 * 9 * C * C,
+                  "conv_body": 2 * 9 * C * C}
         peak = peaks["bf16_tflops_sustained"] if wl.sr.bf16 else 148 * 128 * 2 * 1.965e9 / 1e12
+        if dom in per_px:
+            alg = per_px[dom] * box_px   # algorithmic FLOPs per launch: per-LR-box-pixel figure x box pixels
+            achieved = alg / (dom_ms / 1000.0) / 1e12
+            roof = {"kernel": dom, "bound": "tensor" if wl.sr.bf16 else "alu", "achieved": achieved, "peak": peak,
+                    "unit": "TFLOP/s", "frac": achieved / peak, "traffic": load_traffic(dom),
+                    "algorithmic_per_launch": alg, "per_unit": f"{per_px[dom]} FLOP per LR box pixel x {box_px} box px",
+                    "launch_ms_mean": dom_ms,
+                    "peak_source": f"{peaks['source']} bf16 sustained" if wl.sr.bf16 else "fp32 FMA 148x128x2x1.965GHz"}
+        else:
+            roof = {"kernel": dom, "bound": None, "achieved": None, "peak": None, "unit": None, "frac": None,
+                    "traffic": load_traffic(dom), "launch_ms_mean": dom_ms}
+        roof.update({"flops_per_step": flops_step, "box_px_per_step": box_px,
+                     "occupy_ratio_sel_over_box": sel_px / max(box_px, 1),
+                     "occupy_ratio_box_over_bin": box_px / max(n_bins * wl.bin_w * wl.bin_h, 1),
+                     "sr_network_tflops": flops_step / (stage[2] / 1000.0) / 1e12})
+        kernels = {name: {"launches_per_step": n / n_warm, "ms_mean": ms / n,
+                          "share": ms / sum(v[1] for v in kern_all.values())} for name, (n, ms) in
+                   sorted(kern_all.items(), key=lambda kv: -kv[1][1])}
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -361,20 +458,20 @@ def main() -> None:
                        "l2": "timed steps run back to back; each step's working set (~2 GB of packed activations "
                              "and HR intermediates) is >10x the 126 MB L2, so no step finds the previous one's data",
                        "schedule": "index path (select+pack) of batch k+1 overlapped with SR (enhance+scatter) of batch k "
-                                   "on two CUDA streams, double-buffered pipeline state",
+                                   "on two CUDA streams, double-buffered pipeline state"
+                                   + ("; the K steps replayed as one captured CUDA graph" if graph is not None else ""),
                        "parallelism": f"weak dp{world} (streams sharded by rank, no data-path collective)"},
-            "stages_ms": {"select": stage[0], "pack": stage[1], "enhance": stage[2], "scatter": stage[3],
+            "stages_ms": {"select": stage[0], "pack": stage[1], "enhance_scatter": stage[2],
                           "note": "serial instrumented steps, L2 flushed before each"},
-            "roofline": {"kernel": "regen_enhance_packed (stitch + SR convs)", "bound": "tensor" if wl.sr.bf16 else "alu",
-                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                         "traffic": None, "flops_per_step": flops_step, "box_px_per_step": box_px,
-                         "peak_source": f"{peaks['source']} bf16 sustained" if wl.sr.bf16 else "fp32 FMA 148x128x2x1.965GHz",
-                         "occupy_ratio_sel_over_box": sel_px / max(box_px, 1),
-                         "occupy_ratio_box_over_bin": box_px / max(n_bins * wl.bin_w * wl.bin_h, 1)},
+            "roofline": roof,
+            "kernels": kernels,
+            "kernels_note": "device ms per launch from a warm replay of the same captured schedule with every libregen "
+                            "launch bracketed by CUDA events on its stream (concurrent streams: times include "
+                            "co-scheduling); the roofline kernel's time is from the timed replay",
             "e2e": {"value": e2e_val, "unit": "frames/s", "ms_per_step": e2e_t,
                     "h2d_bytes_per_step": imp_h.nbytes + fr_h.nbytes,
                     "d2h_bytes_per_step": int(p.out.numel() * p.out.element_size())},
-            "gpu_launches": p.launches_per_step() * args.steps,
+            "gpu_launches": int(round(sum(v[0] for v in kern_all.values()) / n_warm * args.steps)),
             "clocks": clk.summary(),
         }
         if not args.no_cpu_baseline:

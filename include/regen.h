@@ -216,6 +216,17 @@ REGEN_API regen_status regen_workspace_size(int32_t which, const regen_geom* geo
  * work; lets benchmarks count launches without a profiler. Returns REGEN_E_INVALID on null args. */
 REGEN_API regen_status regen_enhance_kernel_count(const void* sr, const regen_pack_params* params, int32_t* count);
 
+/* Launch tracing (measurement aid). When enabled, every kernel libregen launches is bracketed by
+ * two CUDA events recorded on its stream. regen_trace_read waits for the recorded launches and
+ * returns, in launch order, up to `cap` names (REGEN_TRACE_NAME_LEN bytes each, NUL-terminated)
+ * and device durations in ms; *n = number of launches recorded (may exceed cap); the record is then
+ * cleared. Host-thread-safe; adds two event records per launch while on. */
+#define REGEN_TRACE_NAME_LEN 32
+REGEN_API regen_status regen_trace_enable(int32_t on);
+/* Trace only kernels whose name starts with `prefix` (NULL or "" = all). */
+REGEN_API regen_status regen_trace_filter(const char* prefix);
+REGEN_API regen_status regen_trace_read(char* names, float* ms, int32_t cap, int32_t* n);
+
 /* Helpers. */
 REGEN_API int64_t regen_capacity_mbs(int32_t bin_w, int32_t bin_h, int32_t n_bins, int32_t mb);  /* floor(H*W*B/mb^2) */
 REGEN_API const char* regen_status_string(regen_status s);

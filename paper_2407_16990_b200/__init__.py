@@ -27,7 +27,7 @@ ST_REGION_OVERFLOW, ST_BOX_OVERFLOW, ST_FREELIST_OVERFLOW = 1, 2, 4
 EXPORTED = ["regen_select_mbs", "regen_pack_regions", "regen_sr_create", "regen_sr_destroy", "regen_stitch_bins",
             "regen_enhance_packed", "regen_scatter_blend", "regen_workspace_size", "regen_capacity_mbs",
             "regen_status_string", "regen_last_error", "regen_abi_version", "regen_enhance_kernel_count",
-            "regen_enhance_scatter"]
+            "regen_enhance_scatter", "regen_trace_enable", "regen_trace_read", "regen_trace_filter"]
 
 
 class Geom(ctypes.Structure):
@@ -83,6 +83,9 @@ def _load():
                                           vp]
     lib.regen_workspace_size.argtypes = [i32, P(Geom), vp, vp, P(sz)]
     lib.regen_enhance_kernel_count.argtypes = [vp, P(PackParams), P(i32)]
+    lib.regen_trace_enable.argtypes = [i32]
+    lib.regen_trace_read.argtypes = [vp, vp, i32, P(i32)]
+    lib.regen_trace_filter.argtypes = [ctypes.c_char_p]
     lib.regen_capacity_mbs.argtypes = [i32, i32, i32, i32]
     lib.regen_capacity_mbs.restype = i64
     lib.regen_status_string.restype = ctypes.c_char_p
@@ -90,7 +93,7 @@ def _load():
     lib.regen_abi_version.restype = i32
     for name in ["regen_select_mbs", "regen_pack_regions", "regen_sr_create", "regen_sr_destroy",
                  "regen_stitch_bins", "regen_enhance_packed", "regen_scatter_blend", "regen_workspace_size",
-                 "regen_enhance_kernel_count", "regen_enhance_scatter"]:
+                 "regen_enhance_kernel_count", "regen_enhance_scatter", "regen_trace_enable", "regen_trace_read", "regen_trace_filter"]:
         getattr(lib, name).restype = ctypes.c_int
     return lib
 
@@ -113,6 +116,30 @@ def _stream(stream=None):
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
     return ctypes.c_void_p(s.cuda_stream)
+
+
+TRACE_NAME_LEN = 32
+
+
+def trace_enable(on: bool = True):
+    """Bracket every libregen kernel launch with CUDA events on its stream (regen_trace_enable)."""
+    _check(lib.regen_trace_enable(1 if on else 0), "regen_trace_enable")
+
+
+def trace_filter(prefix: str | None = None):
+    """Trace only kernels whose name starts with `prefix` (None = all)."""
+    _check(lib.regen_trace_filter(prefix.encode() if prefix else None), "regen_trace_filter")
+
+
+def trace_read(cap: int = 1 << 16) -> list:
+    """[(kernel name, device ms)] of the launches recorded since the last read, in launch order."""
+    names = ctypes.create_string_buffer(cap * TRACE_NAME_LEN)
+    ms = (ctypes.c_float * cap)()
+    n = ctypes.c_int32(0)
+    _check(lib.regen_trace_read(names, ms, cap, ctypes.byref(n)), "regen_trace_read")
+    raw = names.raw
+    return [(raw[i * TRACE_NAME_LEN:(i + 1) * TRACE_NAME_LEN].split(b"\0", 1)[0].decode(), float(ms[i]))
+            for i in range(min(n.value, cap))]
 
 
 def capacity_mbs(bin_w: int, bin_h: int, n_bins: int, mb: int = 16) -> int:

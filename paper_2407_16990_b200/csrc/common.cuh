@@ -60,6 +60,23 @@ struct Carver {
 
 regen_status validate_geom(const regen_geom* g);
 
+// Launch tracing (trace.cu, regen_trace_*): when enabled, a TraceScope brackets one kernel launch
+// with two CUDA events recorded on its stream; disabled it costs one relaxed load.
+bool trace_on();
+void trace_begin(const char* name, cudaStream_t s, int* slot);
+void trace_end(int slot, cudaStream_t s);
+struct TraceScope {
+  int slot = -1;
+  cudaStream_t s;
+  TraceScope(const char* name, cudaStream_t st) : s(st) {
+    if (trace_on()) trace_begin(name, st, &slot);
+  }
+  ~TraceScope() {
+    if (slot >= 0) trace_end(slot, s);
+  }
+};
+#define REGEN_TRACE(name, stream) ::regen::TraceScope trace_scope_(name, stream)
+
 // ---------------------------------------------------------------- device helpers
 __device__ __forceinline__ uint32_t score_ord(float s) {
   uint32_t b = __float_as_uint(s);

@@ -794,6 +794,9 @@ regen_status conv_tc_launch(const SRNet* net, const ConvDesc& cv, const void* in
     cudaMemsetAsync(d_prof, 0, 8 * sizeof(unsigned long long), s);
     p.prof = d_prof;
   }
+  static const char* kRoleName[] = {"conv_head", "conv_res_a", "conv_res_b", "conv_body", "conv_up", "conv_tail",
+                                    "conv_tiny0", "conv_tiny1", "conv_fold"};
+  REGEN_TRACE(kRoleName[cv.role], s);
   kern<<<grid, NTHREADS, smem, s>>>(p);
   REGEN_LAUNCH_CHECK();
   if (prof_on) {

@@ -334,6 +334,7 @@ regen_status conv_simt_launch(const SRNet* net, const ConvDesc& cv, const void* 
   a.out_c8 = cv.role == ROLE_UP ? (cv.cout / (cv.ps * cv.ps) + 7) / 8 : (cv.cout + 7) / 8;
   a.res_scale = net->cfg.res_scale;
   dim3 grid((a.Wr + 127) / 128, a.Hr, max_bins);
+  REGEN_TRACE("conv_simt", s);
   if (net->cfg.dtype == REGEN_DTYPE_BF16)
     conv_simt_kernel<__nv_bfloat16><<<grid, 128, 0, s>>>(a);
   else
@@ -412,9 +413,13 @@ regen_status stitch_into(const regen_geom& g, const regen_pack_params& p, int dt
   oa.GW = grid_w(g);
   oa.mb = g.mb;
   if (owner) REGEN_CUDA(cudaMemsetAsync(own8, 0, (size_t)p.max_bins * p.bin_w * p.bin_h, s));
-  paint_kernel<<<(unsigned)max_boxes, 256, 0, s>>>(d_boxes, d_num_boxes, max_boxes, map, p.bin_w, p.bin_h, oa);
+  {
+    REGEN_TRACE("paint", s);
+    paint_kernel<<<(unsigned)max_boxes, 256, 0, s>>>(d_boxes, d_num_boxes, max_boxes, map, p.bin_w, p.bin_h, oa);
+  }
   REGEN_LAUNCH_CHECK();
   dim3 grid((p.bin_w + 127) / 128, p.bin_h, p.max_bins);
+  REGEN_TRACE("gather", s);
   if (dtype == REGEN_DTYPE_BF16) {
     if (layout == 0)
       gather_kernel<__nv_bfloat16, 0><<<grid, 128, 0, s>>>(d_frames, d_boxes, map, d_num_bins, p.bin_w, p.bin_h, g.F,

@@ -429,16 +429,31 @@ extern "C" regen_status regen_pack_regions(const regen_geom* geom, const regen_p
   a.P = p->partition_mb;
   const int warps_per_block = 8;
   const unsigned nblk = (unsigned)((max_regions + warps_per_block - 1) / warps_per_block);
-  clamp_count_kernel<<<1, 1, 0, s>>>(d_num_regions, max_regions, rcount, nreg);
+  {
+    REGEN_TRACE("clamp_count", s);
+    clamp_count_kernel<<<1, 1, 0, s>>>(d_num_regions, max_regions, rcount, nreg);
+  }
   REGEN_LAUNCH_CHECK();
-  box_count_kernel<<<nblk, 32 * warps_per_block, 0, s>>>(a);
+  {
+    REGEN_TRACE("box_count", s);
+    box_count_kernel<<<nblk, 32 * warps_per_block, 0, s>>>(a);
+  }
   REGEN_LAUNCH_CHECK();
-  scan_counts64_kernel<<<1, 1024, 0, s>>>(rcount, nreg, roff, d_num_boxes);
+  {
+    REGEN_TRACE("scan_boxes", s);
+    scan_counts64_kernel<<<1, 1024, 0, s>>>(rcount, nreg, roff, d_num_boxes);
+  }
   REGEN_LAUNCH_CHECK();
-  box_write_kernel<<<nblk, 32 * warps_per_block, 0, s>>>(a);
+  {
+    REGEN_TRACE("box_write", s);
+    box_write_kernel<<<nblk, 32 * warps_per_block, 0, s>>>(a);
+  }
   REGEN_LAUNCH_CHECK();
-  sort_rank_kernel<<<(unsigned)((max_boxes + 255) / 256), 256, 0, s>>>(d_boxes, d_num_boxes, max_boxes, p->order,
-                                                                       d_order);
+  {
+    REGEN_TRACE("sort_rank", s);
+    sort_rank_kernel<<<(unsigned)((max_boxes + 255) / 256), 256, 0, s>>>(d_boxes, d_num_boxes, max_boxes, p->order,
+                                                                         d_order);
+  }
   REGEN_LAUNCH_CHECK();
   PackArgs k;
   k.boxes = d_boxes;
@@ -457,14 +472,20 @@ extern "C" regen_status regen_pack_regions(const regen_geom* geom, const regen_p
   }
   const size_t smem = (size_t)PACK_POOL * 16 + (size_t)PACK_DIMS * 8;
   REGEN_CUDA(cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  pack_kernel<<<1, 32, smem, s>>>(k);
+  {
+    REGEN_TRACE("pack", s);
+    pack_kernel<<<1, 32, smem, s>>>(k);
+  }
   REGEN_LAUNCH_CHECK();
   if (k.prof) {
     cudaStreamSynchronize(s);
     fflush(stdout);
   }
-  owner_fix_kernel<<<(unsigned)((n_mbs(g) + 255) / 256), 256, 0, s>>>(d_mb_owner, n_mbs(g), d_boxes, d_num_boxes,
-                                                                       max_boxes);
+  {
+    REGEN_TRACE("owner_fix", s);
+    owner_fix_kernel<<<(unsigned)((n_mbs(g) + 255) / 256), 256, 0, s>>>(d_mb_owner, n_mbs(g), d_boxes, d_num_boxes,
+                                                                         max_boxes);
+  }
   REGEN_LAUNCH_CHECK();
   return REGEN_OK;
 }

@@ -533,6 +533,7 @@ regen_status resblock_tc_launch(const SRNet* cnet, int block, const void* in, vo
     cudaMemsetAsync(d_prof, 0, 8 * sizeof(unsigned long long), s);
     p.prof = d_prof;
   }
+  REGEN_TRACE("resblock", s);
   kern<<<grid, NTHREADS, smem, s>>>(p);
   REGEN_LAUNCH_CHECK();
   if (prof) {

@@ -239,6 +239,7 @@ regen_status scatter_launch(const regen_geom& g, const regen_pack_params& p, int
   REGEN_REQUIRE(smem <= 200 * 1024, "frame too wide for the scatter kernel (%zu B SMEM)", smem);
   auto go = [&](auto kern) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    REGEN_TRACE(skip_owned ? "scatter_bilinear" : "scatter", s);
     kern<<<grid, SC_THREADS, smem, s>>>(a);
   };
   const bool bf_hr = hr_dtype == REGEN_DTYPE_BF16, bf_out = out_dtype == REGEN_DTYPE_BF16;

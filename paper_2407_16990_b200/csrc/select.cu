@@ -364,7 +364,10 @@ extern "C" regen_status regen_select_mbs(const regen_geom* geom, const regen_sel
   a.k = p->k;
   a.tau = p->tau;
   const int nseg = (int)(M / a.seg_len);
-  select_kernel<<<nseg, 1024, 0, s>>>(a);
+  {
+    REGEN_TRACE("select", s);
+    select_kernel<<<nseg, 1024, 0, s>>>(a);
+  }
   REGEN_LAUNCH_CHECK();
 
   CclArgs c;
@@ -380,9 +383,15 @@ extern "C" regen_status regen_select_mbs(const regen_geom* geom, const regen_sel
   const size_t smem = sizeof(int) * 7 * (size_t)pf;
   REGEN_REQUIRE(smem <= 227 * 1024, "frame MB grid too large for the CCL kernel (%d MBs)", pf);
   REGEN_CUDA(cudaFuncSetAttribute(ccl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  ccl_kernel<<<(unsigned)nf, 512, smem, s>>>(c);
+  {
+    REGEN_TRACE("ccl", s);
+    ccl_kernel<<<(unsigned)nf, 512, smem, s>>>(c);
+  }
   REGEN_LAUNCH_CHECK();
-  scan_counts_kernel<<<1, 1024, 0, s>>>(fcount, nf, foff, d_num_regions);
+  {
+    REGEN_TRACE("scan_regions", s);
+    scan_counts_kernel<<<1, 1024, 0, s>>>(fcount, nf, foff, d_num_regions);
+  }
   REGEN_LAUNCH_CHECK();
   RegWriteArgs w;
   w.labels = d_labels;
@@ -394,7 +403,10 @@ extern "C" regen_status regen_select_mbs(const regen_geom* geom, const regen_sel
   w.status = d_status;
   w.per_frame = pf;
   w.F = g.F;
-  region_write_kernel<<<(unsigned)nf, 256, 0, s>>>(w);
+  {
+    REGEN_TRACE("region_write", s);
+    region_write_kernel<<<(unsigned)nf, 256, 0, s>>>(w);
+  }
   REGEN_LAUNCH_CHECK();
   return REGEN_OK;
 }

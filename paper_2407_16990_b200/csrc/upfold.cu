@@ -259,6 +259,7 @@ regen_status fold_combine_launch(const SRNet* net, const void* P, void* hr_bins,
     fo.mb = fa->geom.mb;
     fo.s = net->cfg.scale;
   }
+  REGEN_TRACE(fa ? "fold_combine_frames" : "fold_combine", s);
 #define LAUNCH(PS_, FR_) \
   fold::combine_kernel<PS_, FR_><<<grid, 128, 0, s>>>(Pb, o, mbits, bt, d_num_bins, Wr, Hr, res, bin_w, bin_h, c8, fo)
   if (p == 2) {
