@@ -235,11 +235,15 @@ def main() -> None:
         dist.init_process_group("nccl", device_id=dev)
 
     import paper_2407_16990_b200 as rg
+    from paper_2407_16990_b200 import shard
 
-    # per-rank workload: its own streams (seeded by the global stream index)
-    seed = 1000 + rank
-    imp_h = synth.importance_maps(wl.S, wl.F, wl.GH, wl.GW, seed)
-    fr_h = synth.frames_rgb8(wl.S, wl.F, wl.H, wl.W, seed)
+    # weak scaling: rank r enhances selection group r, i.e. streams r*S .. r*S+S-1 of the global set
+    # (each stream seeded by its global index; shard.py). No data-path collective.
+    seed = 0
+    groups = shard.rank_groups(wl.S * world, wl.S, world, rank)
+    assert len(groups) == 1 and groups[0] == (rank * wl.S, (rank + 1) * wl.S)
+    imp_h = synth.importance_maps(wl.S, wl.F, wl.GH, wl.GW, seed, s0=groups[0][0])
+    fr_h = synth.frames_rgb8(wl.S, wl.F, wl.H, wl.W, seed, s0=groups[0][0])
     w = synth.sr_weights(wl.sr, 0)
     def make_pipe():
         return rg.Pipeline(S=wl.S, F=wl.F, W=wl.W, H=wl.H, k=wl.k, bin_w=wl.bin_w, bin_h=wl.bin_h,
@@ -380,13 +384,7 @@ def main() -> None:
         k[1] += ms
     if world > 1:
         dist.barrier()
-    frames = frames_step * args.steps
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        f = torch.tensor([frames], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(f, op=dist.ReduceOp.SUM)
-        total_ms, frames = float(t.item()), float(f.item())
+    total_ms, frames = shard.reduce_timing(total_ms, frames_step * args.steps, device=dev)
     value = frames / (total_ms / 1000.0)
     for q in pipes:
         assert q.host_results()["status"] == 0

@@ -30,12 +30,13 @@ def _rng(seed: int, *keys: int) -> np.random.Generator:
     return np.random.Generator(np.random.PCG64(np.random.SeedSequence([seed, *keys])))
 
 
-def importance_maps(S: int, F: int, GH: int, GW: int, seed: int = 0, kind: str = "blobs") -> np.ndarray:
-    """fp32 [S][F][GH][GW] importance scores."""
+def importance_maps(S: int, F: int, GH: int, GW: int, seed: int = 0, kind: str = "blobs", s0: int = 0) -> np.ndarray:
+    """fp32 [S][F][GH][GW] importance scores of streams s0 .. s0+S-1 (each stream seeded by its global
+    index, so any shard of a multi-stream workload sees the same maps)."""
     out = np.zeros((S, F, GH, GW), np.float32)
     yy, xx = np.mgrid[0:GH, 0:GW].astype(np.float64)
     for s in range(S):
-        rng = _rng(seed, 1, s)
+        rng = _rng(seed, 1, s0 + s)
         for f in range(F):
             if kind == "equal":
                 out[s, f] = 0.5
@@ -61,11 +62,11 @@ def importance_maps(S: int, F: int, GH: int, GW: int, seed: int = 0, kind: str =
     return out
 
 
-def frames_rgb8(S: int, F: int, H: int, W: int, seed: int = 0) -> np.ndarray:
-    """uint8 [S][F][H][W][3] RGB frames."""
+def frames_rgb8(S: int, F: int, H: int, W: int, seed: int = 0, s0: int = 0) -> np.ndarray:
+    """uint8 [S][F][H][W][3] RGB frames of streams s0 .. s0+S-1 (seeded by global stream index)."""
     out = np.empty((S, F, H, W, 3), np.uint8)
     for s in range(S):
-        rng = _rng(seed, 2, s)
+        rng = _rng(seed, 2, s0 + s)
         out[s] = rng.integers(0, 256, size=(F, H, W, 3), dtype=np.uint8)
     return out
 

@@ -1,0 +1,100 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2): selection-group sharding (shard.py, SURVEY
+§8(e)) gives every group to exactly one rank, the per-group results do not depend on the world size
+(checked with the oracle's index path, bit for bit), and the measurement's reductions are MAX of
+the elapsed time and SUM of the frames."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+from paper_2407_16990_b200 import shard
+
+N_STREAMS, GROUP, F, W, H = 6, 2, 2, 160, 96
+K_PCT = 20.0
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _group_result(s0: int, s1: int) -> dict:
+    GW, GH = synth.grid(W, H)
+    imp = synth.importance_maps(s1 - s0, F, GH, GW, 3, "blobs", s0=s0)
+    k = int((s1 - s0) * F * GH * GW * K_PCT // 100)
+    ip = oracle.index_path(imp, W, H, k, partition_mb=3, bin_w=64, bin_h=64, max_bins=64)
+    return {"sel": ip["sel"].tobytes(), "boxes": ip["boxes"].tobytes(), "placement": ip["placement"].tobytes(),
+            "owner": ip["owner"].tobytes(), "num_bins": int(ip["num_bins"])}
+
+
+def _worker(rank: int, world: int, port: int, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mine = {g: _group_result(*g) for g in shard.rank_groups(N_STREAMS, GROUP, world, rank)}
+        gathered = [None] * world
+        dist.all_gather_object(gathered, mine)
+        t, f = shard.reduce_timing(10.0 * (rank + 1), 30.0 * (rank + 1), device="cpu")
+        if rank == 0:
+            merged = {}
+            for part in gathered:
+                for g, v in part.items():
+                    assert g not in merged, f"group {g} computed twice"
+                    merged[g] = v
+            q.put((merged, t, f))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_group_and_rank_slices():
+    assert shard.group_bounds(5, 2) == [(0, 2), (2, 4), (4, 5)]
+    assert shard.group_bounds(0, 8) == []
+    # balanced contiguous shares cover every item exactly once
+    for n in range(0, 20):
+        for world in range(1, 9):
+            spans = [shard.rank_slice(n, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+            assert max(b - a for a, b in spans) - min(b - a for a, b in spans) <= 1
+    # C4: 64 streams = 8 groups of 8 -> 8/4/2/1 groups per rank at 1/2/4/8 ranks
+    for world in (1, 2, 4, 8):
+        assert all(len(shard.rank_groups(64, 8, world, r)) == 8 // world for r in range(world))
+    with pytest.raises(ValueError):
+        shard.rank_slice(4, 2, 2)
+
+
+def test_sharded_results_identical_for_any_world_size():
+    """world_size 2 over gloo vs world_size 1 in-process: same groups, bit-identical index path."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    merged, t, f = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert t == 20.0 and f == 90.0          # MAX of 10, 20; SUM of 30, 60
+    single = {g: _group_result(*g) for g in shard.rank_groups(N_STREAMS, GROUP, 1, 0)}
+    assert sorted(merged) == sorted(single) == shard.group_bounds(N_STREAMS, GROUP)
+    for g in single:
+        for key in single[g]:
+            assert merged[g][key] == single[g][key], f"group {g}: {key} differs"
+
+
+def test_group_maps_are_slices_of_the_global_workload():
+    """A shard's inputs equal the same streams of the whole workload (seeded by global stream index)."""
+    GW, GH = synth.grid(W, H)
+    full = synth.importance_maps(N_STREAMS, F, GH, GW, 3, "blobs")
+    frames = synth.frames_rgb8(N_STREAMS, F, 8, 8, 3)
+    for s0, s1 in shard.group_bounds(N_STREAMS, GROUP):
+        np.testing.assert_array_equal(synth.importance_maps(s1 - s0, F, GH, GW, 3, "blobs", s0=s0), full[s0:s1])
+        np.testing.assert_array_equal(synth.frames_rgb8(s1 - s0, F, 8, 8, 3, s0=s0), frames[s0:s1])
