@@ -212,7 +212,7 @@ REGEN_API regen_status regen_workspace_size(int32_t which, const regen_geom* geo
                                   size_t* bytes);
 
 /* Number of kernels one regen_enhance_packed call launches for this SR handle and bin geometry
- * (paint + gather + one per conv launch + the fold combine; memsets excluded). Host-only, no device
+ * (clear + paint + gather + one per conv launch + the fold combine; memsets excluded). Host-only, no device
  * work; lets benchmarks count launches without a profiler. Returns REGEN_E_INVALID on null args. */
 REGEN_API regen_status regen_enhance_kernel_count(const void* sr, const regen_pack_params* params, int32_t* count);
 

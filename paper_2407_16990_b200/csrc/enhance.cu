@@ -10,6 +10,8 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include <vector>
 
 #include "net.cuh"
@@ -146,16 +148,37 @@ namespace regen {
 
 struct OwnArgs {          // optional: mark bin pixels whose source MB is owned by their box
   const int32_t* owner;  // [S][F][GH][GW], null: skip
-  uint8_t* own8;
-  int F, GH, GW, mb;
+  int64_t* dst;
+  int F, GH, GW, mb, W, H, s;
 };
+
+// Grids of the stitch kernels are sized to the GPU, not to the capacities (max_boxes, max_bins):
+// the counts live on the device, so the kernels loop over them (grid-stride).
+constexpr int STITCH_CTAS = 148 * 8;
+
+// map = -1 (and dst = -1) over the bins actually used
+__global__ void clear_kernel(const int32_t* num_bins, int max_bins, size_t bin_px, int32_t* map, int64_t* dst) {
+  const size_t n = (size_t)min(*num_bins, max_bins) * bin_px;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n / 4; i += stride) {
+    reinterpret_cast<int4*>(map)[i] = make_int4(-1, -1, -1, -1);
+    if (dst) {
+      reinterpret_cast<longlong2*>(dst)[2 * i] = make_longlong2(-1, -1);
+      reinterpret_cast<longlong2*>(dst)[2 * i + 1] = make_longlong2(-1, -1);
+    }
+  }
+  for (size_t i = n / 4 * 4 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    map[i] = -1;
+    if (dst) dst[i] = -1;
+  }
+}
 
 __global__ void paint_kernel(const regen_box* boxes, const int64_t* num_boxes, int64_t max_boxes, int32_t* map,
                              int bin_w, int bin_h, OwnArgs oa) {
-  const int64_t b = blockIdx.x;
-  if (b >= min(*num_boxes, max_boxes)) return;
+  const int64_t nb = min(*num_boxes, max_boxes);
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
   const regen_box bx = boxes[b];
-  if (bx.bin < 0) return;
+  if (bx.bin < 0) continue;
   const int fw = bx.rotated ? bx.h : bx.w, fh = bx.rotated ? bx.w : bx.h;
   int32_t* m = map + (int64_t)bx.bin * bin_w * bin_h;
   const int32_t* ow = oa.owner ? oa.owner + ((size_t)bx.stream * oa.F + bx.frame) * oa.GH * oa.GW : nullptr;
@@ -166,8 +189,13 @@ __global__ void paint_kernel(const regen_box* boxes, const int64_t* num_boxes, i
     if (ow) {
       const int sx = bx.rotated ? bx.x0 + q : bx.x0 + p;
       const int sy = bx.rotated ? bx.y0 + bx.h - 1 - p : bx.y0 + q;
-      oa.own8[(size_t)bx.bin * bin_w * bin_h + px] = ow[(sy / oa.mb) * oa.GW + sx / oa.mb] == (int32_t)b;
+      const bool own = ow[(sy / oa.mb) * oa.GW + sx / oa.mb] == (int32_t)b;
+      const int64_t OW = (int64_t)oa.W * oa.s, OH = (int64_t)oa.H * oa.s;
+      const int64_t d = ((((int64_t)bx.stream * oa.F + bx.frame) * OH + (int64_t)oa.s * sy) * OW + (int64_t)oa.s * sx) |
+                        ((int64_t)bx.rotated << 62);
+      oa.dst[(size_t)bx.bin * bin_w * bin_h + px] = own ? d : -1;
     }
+  }
   }
 }
 
@@ -190,10 +218,10 @@ template <typename T, int LAYOUT>
 __global__ void gather_kernel(const uint8_t* frames, const regen_box* boxes, const int32_t* map,
                               const int32_t* num_bins, int bin_w, int bin_h, int F, int W, int H, T* out,
                               uint32_t* mbits) {
-  const int b = blockIdx.z;
-  if (b >= *num_bins) return;
-  const int y = blockIdx.y;
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n_rows = *num_bins * bin_h;
+  for (int item = blockIdx.y; item < n_rows; item += gridDim.y) {
+  const int b = item / bin_h, y = item - b * bin_h;
   const int32_t id = x < bin_w ? map[((int64_t)b * bin_h + y) * bin_w + x] : -1;
   if (mbits != nullptr) {
     // per-row occupancy bitmask for the tensor-core epilogue: bit x%32 of word [b][y][x/32]
@@ -201,7 +229,7 @@ __global__ void gather_kernel(const uint8_t* frames, const regen_box* boxes, con
     const int words = (bin_w + 31) / 32;
     if ((threadIdx.x & 31) == 0 && x < bin_w) mbits[((int64_t)b * bin_h + y) * words + x / 32] = bits;
   }
-  if (x >= bin_w) return;
+  if (x >= bin_w) continue;
   float v[3] = {0.f, 0.f, 0.f};
   if (id >= 0) {
     const regen_box bx = boxes[id];
@@ -214,12 +242,19 @@ __global__ void gather_kernel(const uint8_t* frames, const regen_box* boxes, con
   }
   if (LAYOUT == 0) {
     T* o = out + (((int64_t)b * bin_h + y) * bin_w + x) * 8;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) o[c] = to_t<T>(c < 3 ? v[c] : 0.0f);
+    if (sizeof(T) == 2) {
+      const __nv_bfloat162 h01 = __floats2bfloat162_rn(v[0], v[1]), h2 = __floats2bfloat162_rn(v[2], 0.f);
+      *reinterpret_cast<uint4*>(o) = make_uint4(*reinterpret_cast<const uint32_t*>(&h01),
+                                                *reinterpret_cast<const uint32_t*>(&h2), 0u, 0u);
+    } else {
+      reinterpret_cast<float4*>(o)[0] = make_float4(v[0], v[1], v[2], 0.f);
+      reinterpret_cast<float4*>(o)[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
   } else {
     T* o = out + (((int64_t)b * bin_h + y) * bin_w + x) * 4;
 #pragma unroll
     for (int c = 0; c < 4; ++c) o[c] = to_t<T>(c < 3 ? v[c] : 0.0f);
+  }
   }
 }
 
@@ -353,7 +388,7 @@ EnhanceBufs enhance_bufs(const SRNet* net, const regen_pack_params& p, void* bas
   EnhanceBufs e;
   e.map = c.take<int32_t>(px);
   e.mbits = c.take<uint32_t>((size_t)p.max_bins * p.bin_h * ((p.bin_w + 31) / 32));
-  e.own8 = c.take<uint8_t>(px);
+  e.dst = c.take<int64_t>(px);
   e.counters = c.take<int32_t>(N_COUNTERS);
   e.x0 = c.take<uint8_t>(px * 8 * es);
   e.a0 = c.take<uint8_t>(px * C8 * 8 * es);
@@ -403,22 +438,30 @@ namespace regen {
 regen_status stitch_into(const regen_geom& g, const regen_pack_params& p, int dtype, int layout,
                          const uint8_t* d_frames, const regen_box* d_boxes, const int64_t* d_num_boxes,
                          int64_t max_boxes, const int32_t* d_num_bins, int32_t* map, void* out, cudaStream_t s,
-                         uint32_t* mbits = nullptr, const int32_t* owner = nullptr, uint8_t* own8 = nullptr) {
-  REGEN_CUDA(cudaMemsetAsync(map, 0xFF, (size_t)p.max_bins * p.bin_w * p.bin_h * 4, s));
+                         uint32_t* mbits = nullptr, const int32_t* owner = nullptr, int64_t* dst = nullptr,
+                         int scale = 0) {
   OwnArgs oa;
   oa.owner = owner;
-  oa.own8 = own8;
+  oa.dst = dst;
+  oa.W = g.frame_w;
+  oa.H = g.frame_h;
+  oa.s = scale;
   oa.F = g.F;
   oa.GH = grid_h(g);
   oa.GW = grid_w(g);
   oa.mb = g.mb;
-  if (owner) REGEN_CUDA(cudaMemsetAsync(own8, 0, (size_t)p.max_bins * p.bin_w * p.bin_h, s));
+  {
+    REGEN_TRACE("clear", s);
+    clear_kernel<<<STITCH_CTAS, 256, 0, s>>>(d_num_bins, p.max_bins, (size_t)p.bin_w * p.bin_h, map,
+                                             owner ? dst : nullptr);
+  }
   {
     REGEN_TRACE("paint", s);
-    paint_kernel<<<(unsigned)max_boxes, 256, 0, s>>>(d_boxes, d_num_boxes, max_boxes, map, p.bin_w, p.bin_h, oa);
+    paint_kernel<<<(unsigned)std::min<int64_t>(max_boxes, STITCH_CTAS), 256, 0, s>>>(d_boxes, d_num_boxes, max_boxes,
+                                                                                    map, p.bin_w, p.bin_h, oa);
   }
   REGEN_LAUNCH_CHECK();
-  dim3 grid((p.bin_w + 127) / 128, p.bin_h, p.max_bins);
+  dim3 grid((p.bin_w + 127) / 128, (unsigned)std::min<int64_t>((int64_t)p.max_bins * p.bin_h, STITCH_CTAS));
   REGEN_TRACE("gather", s);
   if (dtype == REGEN_DTYPE_BF16) {
     if (layout == 0)
@@ -464,7 +507,7 @@ extern "C" regen_status regen_enhance_kernel_count(const void* sr, const regen_p
   REGEN_REQUIRE(sr && p && count, "null argument");
   const SRNet* net = (const SRNet*)sr;
   const int nr = net->cfg.n_resblocks;
-  int n = 2;   // paint + gather
+  int n = 3;   // clear + paint + gather
   if (nr == 0) {
     n += 2;
   } else {
@@ -486,7 +529,8 @@ static regen_status enhance_run(const SRNet* net, const regen_geom* geom, const 
                                 const EnhanceBufs& e, cudaStream_t s, FoldFrameArgs* fa) {
   REGEN_CUDA(cudaMemsetAsync(e.counters, 0, N_COUNTERS * sizeof(int32_t), s));
   regen_status st = stitch_into(*geom, *p, net->cfg.dtype, 0, d_frames, d_boxes, d_num_boxes, max_boxes, d_num_bins,
-                                e.map, e.x0, s, e.mbits, fa ? fa->owner : nullptr, e.own8);
+                                e.map, e.x0, s, e.mbits, fa ? fa->owner : nullptr, e.dst,
+                                net->cfg.scale);
   if (st != REGEN_OK) return st;
   const auto& cv = net->convs;
   if (net->cfg.n_resblocks == 0) {
@@ -530,7 +574,7 @@ static regen_status enhance_run(const SRNet* net, const regen_geom* geom, const 
     st = run_conv(net, cv[net->fold_conv], up_in, e.u, nullptr, e, *p, d_num_bins, s, ord++);
     if (fa) {
       fa->map = e.map;
-      fa->own8 = e.own8;
+      fa->dst = e.dst;
     }
     if (st == REGEN_OK)
       st = fold_combine_launch(net, e.u, d_hr_bins, e.mbits, p->max_bins, d_num_bins, p->bin_w, p->bin_h, s, fa);

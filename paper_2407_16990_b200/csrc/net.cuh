@@ -55,7 +55,8 @@ constexpr int N_COUNTERS = 256, RB_COUNTER0 = 160;   // convs <= 2*64 + 6, resid
 struct EnhanceBufs {
   int32_t* map;      // [max_bins][bin_h][bin_w] box index covering the pixel, -1 outside boxes
   uint32_t* mbits;   // [max_bins][bin_h][ceil(bin_w/32)] occupancy bits (map >= 0)
-  uint8_t* own8;     // [max_bins][bin_h][bin_w] 1 where the pixel's source MB is owned by its box
+  int64_t* dst;      // [max_bins][bin_h][bin_w] for a pixel whose source MB is owned by its box: the
+                     // HR frame pixel index of its top-left HR pixel | rotated << 62; -1 otherwise
                      // (written by paint only when the owner grid is given: regen_enhance_scatter)
   int32_t* counters; // [N_COUNTERS] dynamic scheduler counters, zeroed per call: conv i at i,
                      // fused residual block k at RB_COUNTER0 + k
@@ -83,7 +84,7 @@ void fold_prepare(SRNet* net, std::vector<float>& w32);
 struct FoldFrameArgs {
   regen_geom geom;
   const int32_t* map;
-  const uint8_t* own8;
+  const int64_t* dst;
   const regen_box* boxes;
   const int32_t* owner;
   void* out;

@@ -29,17 +29,16 @@ struct ScatterArgs {
   int skip_owned;   // regen_enhance_scatter: owned MBs were written by the fold combine
 };
 
-// One CTA per (frame, LR row y) writes the S HR rows S*y .. S*y+S-1:
-//   1. vertical pass of the S rows from the LR frame (L2-resident) -> SMEM [S][W] float4, and the
-//      owner row of their MB row -> SMEM
-//   2. horizontal pass: a thread per (HR row, pair of LR columns) computes their 2*S HR pixels
-//      (6*S values, a whole number of 32-bit words, consecutive threads -> consecutive words: no
-//      bank conflicts) into an SMEM copy of the output rows. D10 weights per sub-pixel phase are
-//      compile-time: HR pixel X = S*x + j samples src = x + (j + 0.5)/S - 0.5, i.e. columns
-//      (x-1, x) or (x, x+1) with a fixed fraction, clamped at the edges exactly as the oracle.
-//   3. copy-out in coalesced 16-B chunks (an MB's HR square is a whole number of chunks), skipping
-//      the chunks of owned MBs; those get the owner box's HR bin pixels (SKIP = false) or nothing
-//      (SKIP: regen_enhance_scatter wrote them already).
+// One CTA per (frame, LR row y) writes the S HR rows S*y .. S*y+S-1. The (at most three) LR rows
+// they interpolate from (16-B loads) and the owner row of their MB row go to SMEM once; then per HR
+// row: (1) vertical pass -> SMEM [W] float4; (2) horizontal pass, a thread per pair of LR columns
+// computing their 2*S HR pixels (6*S values = whole 32-bit words, consecutive threads ->
+// consecutive words: no bank conflicts) into an SMEM copy of the output row, with the D10 weights
+// of each sub-pixel phase compile-time (HR pixel X = S*x + j samples src = x + (j + 0.5)/S - 0.5:
+// columns (x-1, x) or (x, x+1) with a fixed fraction, clamped at the edges exactly as the oracle);
+// (3) coalesced 16-B copy-out (an MB's HR square is a whole number of chunks) skipping owned MB
+// squares, which get the owner box's HR bin pixels (SKIP = false) or nothing (SKIP:
+// regen_enhance_scatter wrote them already). ~28 KB SMEM per CTA: 8 CTAs per SM.
 constexpr int SC_THREADS = 256;
 
 template <int S>
@@ -69,45 +68,63 @@ __global__ void __launch_bounds__(SC_THREADS) scatter_rows_kernel(ScatterArgs a)
   const int npair = (W + 1) / 2;
   constexpr int WPP = 3 * S * (int)sizeof(TO) / 2;                            // 32-bit words per column pair
   const int row_words = (npair * WPP + 3) / 4 * 4;                            // staging row (16-B multiple)
-  float4* vr = reinterpret_cast<float4*>(sm);                                 // [S][W]
-  uint32_t* orow = reinterpret_cast<uint32_t*>(vr + S * W);                   // [S][row_words]
-  int32_t* own = reinterpret_cast<int32_t*>(orow + S * row_words);            // [GW]
+  const int W3p = (W3 + 15) / 16 * 16;
+  float4* vr = reinterpret_cast<float4*>(sm);                                 // [W]
+  uint32_t* orow = reinterpret_cast<uint32_t*>(vr + W);                       // [row_words]
+  int32_t* own = reinterpret_cast<int32_t*>(orow + row_words);                // [GW (+pad)]
+  uint8_t* lr = reinterpret_cast<uint8_t*>(own + (a.GW + 3) / 4 * 4);         // [3][W3p]
   const uint8_t* img = a.frames + sf * (int64_t)a.H * W3;
+  // ---- 0. the (at most three) LR rows (16-B loads when aligned) and the owner row -> SMEM
+  for (int k = 0; k < 3; ++k) {
+    const uint8_t* src = img + (size_t)min(max(y - 1 + k, 0), a.H - 1) * W3;
+    uint8_t* dst = lr + k * W3p;
+    if ((((uintptr_t)src) & 15) == 0) {
+      for (int j = threadIdx.x; j < W3 / 16; j += SC_THREADS)
+        reinterpret_cast<uint4*>(dst)[j] = __ldg(reinterpret_cast<const uint4*>(src) + j);
+      for (int j = W3 / 16 * 16 + threadIdx.x; j < W3; j += SC_THREADS) dst[j] = src[j];
+    } else {
+      for (int j = threadIdx.x; j < W3; j += SC_THREADS) dst[j] = src[j];
+    }
+  }
   const int my = y / a.mb;   // MB row of all S HR rows
   for (int j = threadIdx.x; j < a.GW; j += SC_THREADS) own[j] = a.owner[(sf * a.GH + my) * a.GW + j];
-  // ---- 1. vertical pass (D10) for the S rows
+  constexpr int MB_BYTES = 16 * S * 3 * (int)sizeof(TO);     // HR width of an MB in bytes (mb = 16)
+  static_assert(MB_BYTES % 16 == 0, "MB squares must be whole 16-B chunks");
+  const int row_bytes = a.OW * 3 * (int)sizeof(TO);
+  const int n16 = row_bytes / 16;
 #pragma unroll
   for (int i = 0; i < S; ++i) {
+    const int Y = y * S + i;
+    // ---- 1. vertical pass (D10) of HR row i
     int yl0 = y + Phase<S>::d(i);
     float ly = Phase<S>::f(i);
     if (yl0 < 0) { yl0 = 0; ly = 0.f; }
     const int yl1 = min(yl0 + 1, a.H - 1);
     if (yl1 == yl0) ly = 0.f;
-    const uint8_t* r0 = img + (size_t)yl0 * W3;
-    const uint8_t* r1 = img + (size_t)yl1 * W3;
-    for (int x = threadIdx.x; x < W; x += SC_THREADS) {
-      float4 v;
-      float p0 = (float)__ldg(r0 + 3 * x), p1 = (float)__ldg(r1 + 3 * x);
-      v.x = fmaf(ly, p1 - p0, p0);
-      p0 = (float)__ldg(r0 + 3 * x + 1); p1 = (float)__ldg(r1 + 3 * x + 1);
-      v.y = fmaf(ly, p1 - p0, p0);
-      p0 = (float)__ldg(r0 + 3 * x + 2); p1 = (float)__ldg(r1 + 3 * x + 2);
-      v.z = fmaf(ly, p1 - p0, p0);
-      v.w = 0.f;
-      vr[i * W + x] = v;
+    __syncthreads();   // LR rows staged / previous row's horizontal pass done
+    {
+      const uint8_t* r0 = lr + (yl0 - (y - 1)) * W3p;   // slot k holds row clamp(y-1+k)
+      const uint8_t* r1 = lr + (yl1 - (y - 1)) * W3p;
+      for (int x = threadIdx.x; x < W; x += SC_THREADS) {
+        float4 v;
+        float p0 = (float)r0[3 * x], p1 = (float)r1[3 * x];
+        v.x = fmaf(ly, p1 - p0, p0);
+        p0 = (float)r0[3 * x + 1]; p1 = (float)r1[3 * x + 1];
+        v.y = fmaf(ly, p1 - p0, p0);
+        p0 = (float)r0[3 * x + 2]; p1 = (float)r1[3 * x + 2];
+        v.z = fmaf(ly, p1 - p0, p0);
+        v.w = 0.f;
+        vr[x] = v;
+      }
     }
-  }
-  __syncthreads();
-  // ---- 2. horizontal pass into the SMEM output rows
-#pragma unroll
-  for (int i = 0; i < S; ++i) {
-    const float4* vrow = vr + i * W;
-    uint32_t* orw = orow + i * row_words;
+    __syncthreads();   // vr ready; previous row's copy-out done
+    // ---- 2. horizontal pass: a thread per pair of LR columns -> 2*S HR pixels (6*S values, whole
+    // 32-bit words; consecutive threads -> consecutive words: no bank conflicts)
     for (int t = threadIdx.x; t < npair; t += SC_THREADS) {
       const int x0 = 2 * t;
       float4 v[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) v[q] = vrow[min(max(x0 - 1 + q, 0), W - 1)];
+      for (int q = 0; q < 4; ++q) v[q] = vr[min(max(x0 - 1 + q, 0), W - 1)];
       float o[6 * S];
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
@@ -133,20 +150,12 @@ __global__ void __launch_bounds__(SC_THREADS) scatter_rows_kernel(ScatterArgs a)
 #pragma unroll
       for (int k = 0; k < 3 * S; ++k) put2<TO>(w, k, o[2 * k], o[2 * k + 1]);
 #pragma unroll
-      for (int k = 0; k < WPP; ++k) orw[t * WPP + k] = w[k];
+      for (int k = 0; k < WPP; ++k) orow[t * WPP + k] = w[k];
     }
-  }
-  __syncthreads();
-  // ---- 3. copy-out
-  constexpr int MB_BYTES = 16 * S * 3 * (int)sizeof(TO);     // HR width of an MB in bytes (mb = 16)
-  static_assert(MB_BYTES % 16 == 0, "MB squares must be whole 16-B chunks");
-  const int row_bytes = a.OW * 3 * (int)sizeof(TO);
-  const int n16 = row_bytes / 16;
-#pragma unroll
-  for (int i = 0; i < S; ++i) {
-    const int Y = y * S + i;
+    __syncthreads();
+    // ---- 3. copy-out of HR row i in coalesced 16-B chunks, owned MB squares skipped
     uint8_t* drow = (uint8_t*)a.out + ((sf * a.OH + Y) * (int64_t)a.OW) * 3 * sizeof(TO);
-    const uint8_t* srow = reinterpret_cast<const uint8_t*>(orow + i * row_words);
+    const uint8_t* srow = reinterpret_cast<const uint8_t*>(orow);
     if ((((uintptr_t)drow) & 15) == 0) {
       for (int c = threadIdx.x; c < n16; c += SC_THREADS) {
         if (own[(c * 16) / MB_BYTES] >= 0) continue;
@@ -235,7 +244,8 @@ regen_status scatter_launch(const regen_geom& g, const regen_pack_params& p, int
   const size_t es = out_dtype == REGEN_DTYPE_BF16 ? 2 : 4;
   const size_t npair = ((size_t)g.frame_w + 1) / 2;
   const size_t row_words = (npair * 3 * scale * es / 2 + 3) / 4 * 4;
-  const size_t smem = (size_t)g.frame_w * 16 * scale + (size_t)scale * row_words * 4 + (size_t)a.GW * 4 + 16;
+  const size_t smem = (size_t)g.frame_w * 16 + row_words * 4 + ((size_t)a.GW + 3) / 4 * 16 +
+                      3 * (((size_t)g.frame_w * 3 + 15) / 16 * 16) + 16;
   REGEN_REQUIRE(smem <= 200 * 1024, "frame too wide for the scatter kernel (%zu B SMEM)", smem);
   auto go = [&](auto kern) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

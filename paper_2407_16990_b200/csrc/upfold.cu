@@ -18,6 +18,7 @@
 // result equals UP -> mask -> TAIL -> mask up to rounding (no bf16 HR activation is formed), at
 // 3(p+2)^2 * 9C instead of (p^2 + 3p^2) * 9C multiply-adds per source pixel, and without the
 // HR activation round trip through HBM (9.4 MB per 128x128 bin at C = 32, p = 3).
+#include <algorithm>
 #include <vector>
 
 #include "net.cuh"
@@ -43,12 +44,38 @@ __host__ __device__ constexpr int block_off(int ny, int nx, int p) {
 }
 __host__ __device__ constexpr int n_channels(int p) { return 3 * (p + 2) * (p + 2); }
 
+// the 16-B plane loads of one pixel's combine, in (neighbour, plane) order: l-th load
+__host__ __device__ constexpr int plane_lo(int ny, int nx, int p) { return block_off(ny, nx, p) / 8; }
+__host__ __device__ constexpr int plane_hi(int ny, int nx, int p) {
+  return (block_off(ny, nx, p) + cnt(ny, p) * cnt(nx, p) * 3 - 1) / 8;
+}
+__host__ __device__ constexpr int n_loads(int p) {
+  int n = 0;
+  for (int a = -1; a <= 1; ++a)
+    for (int b = -1; b <= 1; ++b) n += plane_hi(a, b, p) - plane_lo(a, b, p) + 1;
+  return n;
+}
+// (ny, nx, plane) of load l, packed as (ny+1)*3 + (nx+1) in the high bits
+__host__ __device__ constexpr int load_code(int p, int l) {
+  for (int a = -1; a <= 1; ++a)
+    for (int b = -1; b <= 1; ++b) {
+      const int n = plane_hi(a, b, p) - plane_lo(a, b, p) + 1;
+      if (l < n) return ((a + 1) * 3 + (b + 1)) * 64 + plane_lo(a, b, p) + l;
+      l -= n;
+    }
+  return 0;
+}
+__host__ __device__ constexpr int load_ny(int p, int l) { return load_code(p, l) / 64 / 3 - 1; }
+__host__ __device__ constexpr int load_nx(int p, int l) { return load_code(p, l) / 64 % 3 - 1; }
+__host__ __device__ constexpr int load_pl(int p, int l) { return load_code(p, l) % 64; }
+
 // Where the combined HR pixels go. BINS: the HR bin layout [bin][PS*Hr][PS*Wr][4] of
 // regen_enhance_packed. FRAME (regen_enhance_scatter): straight into the HR frames
 // [S][F][s*H][s*W][3], for owned selected MBs only (the scatter pass writes every other pixel).
 struct FrameOut {
   const int32_t* map;        // [bin][bin_h][bin_w] LR bin pixel -> covering box, -1 outside boxes
-  const uint8_t* own8;       // [bin][bin_h][bin_w] 1: the pixel's source MB is owned by its box
+  const int64_t* dst;        // [bin][bin_h][bin_w] owned pixel: HR frame index of its top-left HR pixel
+                             // | rotated << 62; -1: not owned (the scatter pass writes it)
   const regen_box* boxes;
   const int32_t* owner;      // [S][F][GH][GW]
   void* out;
@@ -57,23 +84,23 @@ struct FrameOut {
 };
 
 template <int PS, bool FRAME>
-__global__ void __launch_bounds__(128) combine_kernel(const __nv_bfloat16* P, __nv_bfloat16* out, const uint32_t* mbits,
+__global__ void __launch_bounds__(128, 8) combine_kernel(const __nv_bfloat16* P, __nv_bfloat16* out, const uint32_t* mbits,
                                                       const float* bt, const int32_t* num_bins, int Wr, int Hr,
                                                       int res, int bin_w, int bin_h, int c8, FrameOut fo) {
-  const int bin = blockIdx.z;
-  if (bin >= *num_bins) return;
-  const int y = blockIdx.y;
+  // grid-stride over the (bin, row) items of the bins actually used (the grid is sized to the GPU)
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n_items = *num_bins * Hr;
   if (x >= Wr) return;
+  for (int item = blockIdx.y; item < n_items; item += gridDim.y) {
+  const int bin = item / Hr, y = item - bin * Hr;
   const int words = (bin_w + 31) / 32;
   const int xl = x / res, yl = y / res;
   // FRAME: only pixels whose source MB is owned by their box (the scatter pass writes the rest)
-  regen_box bx;
+  int64_t dst = 0;
   bool occ;
   if (FRAME) {
-    const size_t lpx = ((size_t)bin * bin_h + yl) * bin_w + xl;
-    if (!__ldg(fo.own8 + lpx)) return;
-    bx = fo.boxes[__ldg(fo.map + lpx)];
+    dst = __ldg(fo.dst + ((size_t)bin * bin_h + yl) * bin_w + xl);
+    if (dst < 0) continue;
     occ = true;
   } else {
     occ = (__ldg(mbits + ((size_t)bin * bin_h + yl) * words + xl / 32) >> (xl & 31)) & 1u;
@@ -86,36 +113,34 @@ __global__ void __launch_bounds__(128) combine_kernel(const __nv_bfloat16* P, __
 #pragma unroll
       for (int o = 0; o < 3; ++o) acc[i][j][o] = 0.f;
   if (occ) {
+    // all partial-sum planes this pixel needs (<= 16 16-B loads over its 3x3 neighbourhood) are
+    // issued before any is used, so their latencies overlap
     const size_t pstride = (size_t)Wr * 8;
+    constexpr int NL = n_loads(PS);
+    uint4 q[NL];
 #pragma unroll
-    for (int ny = -1; ny <= 1; ++ny)
+    for (int l = 0; l < NL; ++l) {
+      const int ny = load_ny(PS, l), nx = load_nx(PS, l), pl = load_pl(PS, l);
+      const int yy = y + ny, xx = x + nx;
+      q[l] = (yy < 0 || yy >= Hr || xx < 0 || xx >= Wr)   // zero padding at the bin edge
+                 ? make_uint4(0, 0, 0, 0)
+                 : __ldg(reinterpret_cast<const uint4*>(P + ((size_t)bin * Hr + yy) * c8 * pstride +
+                                                        (size_t)pl * pstride + (size_t)xx * 8));
+    }
 #pragma unroll
-      for (int nx = -1; nx <= 1; ++nx) {
-        const int yy = y + ny, xx = x + nx;
-        if (yy < 0 || yy >= Hr || xx < 0 || xx >= Wr) continue;   // zero padding at the bin edge
-        const __nv_bfloat16* base = P + ((size_t)bin * Hr + yy) * c8 * pstride + (size_t)xx * 8;
-        const int off = block_off(ny, nx, PS), ci = cnt(ny, PS), cj = cnt(nx, PS);
-        const int pl0 = off / 8, pl1 = (off + ci * cj * 3 - 1) / 8;
+    for (int l = 0; l < NL; ++l) {
+      const int ny = load_ny(PS, l), nx = load_nx(PS, l), pl = load_pl(PS, l);
+      const int off = block_off(ny, nx, PS), ci = cnt(ny, PS), cj = cnt(nx, PS);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q[l]);
 #pragma unroll
-        for (int pl = pl0; pl <= pl1; ++pl) {
-          const uint4 q = __ldg(reinterpret_cast<const uint4*>(base + (size_t)pl * pstride));
-          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
-          float v[8];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 f = __bfloat1622float2(h[e]);
-            v[2 * e] = f.x;
-            v[2 * e + 1] = f.y;
-          }
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int ch = pl * 8 + e - off;   // index within the block
-            if (ch < 0 || ch >= ci * cj * 3) continue;
-            const int o = ch % 3, t = ch / 3, jj = t % cj, ii = t / cj;
-            acc[first(ny, PS) + ii][first(nx, PS) + jj][o] += v[e];
-          }
-        }
+      for (int e = 0; e < 8; ++e) {
+        const int ch = pl * 8 + e - off;   // index within the neighbour's block
+        if (ch < 0 || ch >= ci * cj * 3) continue;
+        const float v = (e & 1) ? __high2float(h[e / 2]) : __low2float(h[e / 2]);
+        const int o = ch % 3, t = ch / 3, jj = t % cj, ii = t / cj;
+        acc[first(ny, PS) + ii][first(nx, PS) + jj][o] += v;
       }
+    }
   }
   const float b0 = __ldg(bt), b1 = __ldg(bt + 1), b2 = __ldg(bt + 2);
   if (!FRAME) {
@@ -132,32 +157,49 @@ __global__ void __launch_bounds__(128) combine_kernel(const __nv_bfloat16* P, __
       }
     }
   } else {
-    // bin HR pixel (X', Y') -> box-local (u, v) (un-rotate, D7) -> frame HR pixel (s*x0 + u, s*y0 + v);
-    // values rounded to bf16 first (bit-identical to the HR-bin round trip of the separate calls)
-    const int s = fo.s, OW = fo.W * s, OH = fo.H * s;
-    const size_t fbase = ((size_t)bx.stream * fo.F + bx.frame) * (size_t)OH * OW;
+    // the PS x PS HR block of this pixel inside the HR frame (D7 un-rotation: bin-HR sub-pixel (i, j)
+    // -> frame (j, i) unrotated, (i, PS-1-j) rotated; for res 2 (x4) the block is offset inside the
+    // LR pixel's 4x4 square by the res-2 sub-position). Values rounded to bf16 first (bit-identical
+    // to the HR-bin round trip of the separate calls). Each frame row of the block gets 3*PS
+    // contiguous elements, stored as 32-bit words after a leading 16-bit one when misaligned.
+    const bool rot = (dst >> 62) & 1;
+    const int OW = fo.W * fo.s;
+    int64_t base = dst & ((1ll << 62) - 1);
+    if (res > 1) {   // x4: this res-2 pixel's 2x2 HR block inside the LR pixel's 4x4 square
+      const int sx2 = x % res, sy2 = y % res;
+      base += rot ? (int64_t)(PS * (res - 1 - sx2)) * OW + PS * sy2 : (int64_t)(PS * sy2) * OW + PS * sx2;
+    }
 #pragma unroll
-    for (int i = 0; i < PS; ++i)
+    for (int r = 0; r < PS; ++r) {   // frame row r of the block
+      float v[3 * PS];
 #pragma unroll
-      for (int j = 0; j < PS; ++j) {
-        const int Xb = PS * x + j - s * bx.bx, Yb = PS * y + i - s * bx.by;   // box-footprint-local HR
-        const int u = bx.rotated ? Yb : Xb;
-        const int v = bx.rotated ? s * bx.h - 1 - Xb : Yb;
-        const size_t px = fbase + (size_t)(s * bx.y0 + v) * OW + (size_t)(s * bx.x0 + u);
-        const __nv_bfloat16 c0 = __float2bfloat16_rn(acc[i][j][0] + b0), c1 = __float2bfloat16_rn(acc[i][j][1] + b1),
-                            c2 = __float2bfloat16_rn(acc[i][j][2] + b2);
-        if (fo.out_fp32) {
-          float* o = (float*)fo.out + px * 3;
-          o[0] = __bfloat162float(c0);
-          o[1] = __bfloat162float(c1);
-          o[2] = __bfloat162float(c2);
+      for (int c = 0; c < PS; ++c) {   // frame column c
+        // bin-HR sub-pixel (c, PS-1-r) when rotated, (r, c) otherwise (compile-time indices)
+        v[3 * c] = (rot ? acc[c][PS - 1 - r][0] : acc[r][c][0]) + b0;
+        v[3 * c + 1] = (rot ? acc[c][PS - 1 - r][1] : acc[r][c][1]) + b1;
+        v[3 * c + 2] = (rot ? acc[c][PS - 1 - r][2] : acc[r][c][2]) + b2;
+      }
+      const size_t e0 = (size_t)(base + (int64_t)r * OW) * 3;   // element index of the run
+      if (fo.out_fp32) {
+        float* o = (float*)fo.out + e0;
+#pragma unroll
+        for (int e = 0; e < 3 * PS; ++e) o[e] = __bfloat162float(__float2bfloat16_rn(v[e]));
+      } else {
+        __nv_bfloat16* o = (__nv_bfloat16*)fo.out + e0;
+        constexpr int NE = 3 * PS;
+        if (e0 & 1) {   // odd start: one 16-bit store, then 32-bit pairs
+          o[0] = __float2bfloat16_rn(v[0]);
+#pragma unroll
+          for (int e = 1; e + 1 < NE; e += 2) *reinterpret_cast<uint32_t*>(o + e) = pack_bf16x2(v[e], v[e + 1]);
+          if ((NE - 1) % 2 == 1) o[NE - 1] = __float2bfloat16_rn(v[NE - 1]);
         } else {
-          __nv_bfloat16* o = (__nv_bfloat16*)fo.out + px * 3;
-          o[0] = c0;
-          o[1] = c1;
-          o[2] = c2;
+#pragma unroll
+          for (int e = 0; e + 1 < NE; e += 2) *reinterpret_cast<uint32_t*>(o + e) = pack_bf16x2(v[e], v[e + 1]);
+          if (NE % 2 == 1) o[NE - 1] = __float2bfloat16_rn(v[NE - 1]);
         }
       }
+    }
+  }
   }
 }
 
@@ -238,7 +280,7 @@ regen_status fold_combine_launch(const SRNet* net, const void* P, void* hr_bins,
   const int p = up.ps, res = d.res;
   const int Wr = bin_w * res, Hr = bin_h * res;
   const int c8 = (d.cout + 7) / 8;
-  dim3 grid((unsigned)((Wr + 127) / 128), (unsigned)Hr, (unsigned)max_bins);
+  dim3 grid((unsigned)((Wr + 127) / 128), (unsigned)std::min(max_bins * Hr, 148 * 16));
   const float* bt = net->d_w32 + tail.b_off;
   const __nv_bfloat16* Pb = (const __nv_bfloat16*)P;
   __nv_bfloat16* o = (__nv_bfloat16*)hr_bins;
@@ -246,7 +288,7 @@ regen_status fold_combine_launch(const SRNet* net, const void* P, void* hr_bins,
   memset(&fo, 0, sizeof(fo));
   if (fa) {
     fo.map = fa->map;
-    fo.own8 = fa->own8;
+    fo.dst = fa->dst;
     fo.boxes = fa->boxes;
     fo.owner = fa->owner;
     fo.out = fa->out;

@@ -1,2 +1,2 @@
-python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench_dbg.txt 2>&1
-tail -30 gpurun_out/bench_dbg.txt
+python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+python tools/kernel_times.py --steps 3 2>&1 | grep -E "scatter|combine|total"
