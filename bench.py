@@ -236,6 +236,7 @@ def main() -> None:
 
     import paper_2407_16990_b200 as rg
     from paper_2407_16990_b200 import shard
+    from paper_2407_16990_b200.schedule import PipelinedRunner
 
     # weak scaling: rank r enhances selection group r, i.e. streams r*S .. r*S+S-1 of the global set
     # (each stream seeded by its global index; shard.py). No data-path collective.
@@ -252,15 +253,15 @@ def main() -> None:
                            res_scale=wl.sr.res_scale, device=dev)
 
     # two pipelines (double-buffered state) so that the index path (select + pack) of batch k+1 runs
-    # on one CUDA stream while the SR (enhance + scatter) of batch k runs on another
-    pipes = [make_pipe(), make_pipe()]
+    # on one CUDA stream while the SR (enhance + scatter) of batch k runs on another (schedule.py: the
+    # same runner the full-size parity test drives)
+    runner = PipelinedRunner(make_pipe, dev)
+    pipes = runner.pipes
     p = pipes[0]
     imp = torch.from_numpy(imp_h).to(dev)
     fr = torch.from_numpy(fr_h).to(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
-    s_front = torch.cuda.Stream(dev)
-    s_back = torch.cuda.Stream(dev)
 
     # instrumented step (serial, L2 flushed before it): per-stage device time for the breakdown and
     # the roofline of the SR stage
@@ -275,24 +276,7 @@ def main() -> None:
         p.enhance_scatter(fr)
         ev[3].record(stream)
 
-    front_done = [torch.cuda.Event() for _ in range(2)]
-    back_done = [torch.cuda.Event() for _ in range(2)]
-
-    def pipelined_steps(n_steps: int, capturing: bool = False):
-        for k in range(n_steps):
-            q = pipes[k % 2]
-            with torch.cuda.stream(s_front):
-                if not (capturing and k < 2):
-                    s_front.wait_event(back_done[k % 2])    # buffers of batch k-2 are free
-                q.select(imp, stream=s_front)
-                q.pack_step(imp, stream=s_front)
-                front_done[k % 2].record(s_front)
-            with torch.cuda.stream(s_back):
-                s_back.wait_event(front_done[k % 2])
-                q.enhance_scatter(fr, stream=s_back)
-                back_done[k % 2].record(s_back)
-
-    for _ in range(args.warmup):
+    for _ in range(max(args.warmup, 1)):   # >= 1: the box/bin statistics below read a finished step
         flush.zero_()
         step_instrumented()
     torch.cuda.synchronize()
@@ -315,9 +299,7 @@ def main() -> None:
         stage += [ev[i].elapsed_time(ev[i + 1]) for i in range(3)]
     stage /= n_instr
     # warm the pipelined schedule
-    s_front.wait_stream(stream)
-    s_back.wait_stream(stream)
-    pipelined_steps(max(args.warmup, 2))
+    runner.run_eager(imp, fr, max(args.warmup, 2))
     torch.cuda.synchronize()
 
     # The K timed steps are one CUDA graph (captured once, replayed): no host launch overhead between
@@ -329,13 +311,7 @@ def main() -> None:
         if trace_prefix is not None:
             rg.trace_filter(trace_prefix or None)
             rg.trace_enable(True)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=cap):
-            s_front.wait_stream(cap)
-            s_back.wait_stream(cap)
-            pipelined_steps(n_steps, capturing=True)
-            cap.wait_stream(s_front)
-            cap.wait_stream(s_back)
+        g = runner.capture(imp, fr, n_steps)
         rg.trace_enable(False)
         rg.trace_filter(None)
         return g
@@ -344,7 +320,6 @@ def main() -> None:
     rg.trace_read()
     kern_all = {}
     if not args.no_graph:
-        cap = torch.cuda.Stream(dev)
         warm = capture(max(args.warmup, 3), "")     # all kernels traced
         warm.replay()
         torch.cuda.synchronize()
@@ -367,11 +342,7 @@ def main() -> None:
         if graph is not None:
             graph.replay()
         else:
-            s_front.wait_stream(stream)
-            s_back.wait_stream(stream)
-            pipelined_steps(args.steps)
-            stream.wait_stream(s_front)
-            stream.wait_stream(s_back)
+            runner.run_eager(imp, fr, args.steps, stream)
         t1.record(stream)
         torch.cuda.synchronize()
     rg.trace_enable(False)

@@ -206,6 +206,27 @@ REGEN_API regen_status regen_enhance_scatter(void* sr, const regen_geom* geom, c
                                    const int32_t* d_mb_owner, void* d_out, int32_t out_dtype,
                                    int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------------------------------------------------------
+ * The two halves of regen_enhance_scatter, for callers that schedule them on different streams
+ * (the bilinear half needs only the frames and the MB owners, so it can run while the previous
+ * batch's SR still occupies the tensor cores). Together they write every HR pixel of d_out exactly
+ * once, bit-identical to regen_enhance_scatter (eq. P:461-464: SR(MB_s) + IN(rest)).
+ *   regen_enhance_owned: a6+a7 and the paste-back of the HR square of every MB with
+ *     d_mb_owner >= 0; pixels of the other MBs are not touched. Same arguments, workspace and
+ *     errors as regen_enhance_scatter.
+ *   regen_scatter_bilinear: a8's bilinear x scale of u8/255 (D10) on the HR square of every
+ *     MB with d_mb_owner < 0; owned squares are not touched. d_frames [S][F][frame_h][frame_w][3]
+ *     u8, d_mb_owner [S][F][GH][GW] int32, d_out as regen_scatter_blend. No workspace.
+ *     REGEN_E_INVALID on null pointers, scale outside {2,3,4}, a bad out_dtype or geometry.
+ * ------------------------------------------------------------------------------------------- */
+REGEN_API regen_status regen_enhance_owned(void* sr, const regen_geom* geom, const regen_pack_params* params,
+                                 const uint8_t* d_frames, const regen_box* d_boxes, int64_t max_boxes,
+                                 const int64_t* d_num_boxes, const int32_t* d_num_bins,
+                                 const int32_t* d_mb_owner, void* d_out, int32_t out_dtype,
+                                 int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream);
+REGEN_API regen_status regen_scatter_bilinear(const regen_geom* geom, int32_t scale, const uint8_t* d_frames,
+                                    const int32_t* d_mb_owner, void* d_out, int32_t out_dtype, void* stream);
+
 /* Workspace bytes for a call (which = REGEN_CALL_*; params = the call's params struct;
  * sr = SR handle for ENHANCE, else NULL). */
 REGEN_API regen_status regen_workspace_size(int32_t which, const regen_geom* geom, const void* params, const void* sr,

@@ -27,7 +27,8 @@ ST_REGION_OVERFLOW, ST_BOX_OVERFLOW, ST_FREELIST_OVERFLOW = 1, 2, 4
 EXPORTED = ["regen_select_mbs", "regen_pack_regions", "regen_sr_create", "regen_sr_destroy", "regen_stitch_bins",
             "regen_enhance_packed", "regen_scatter_blend", "regen_workspace_size", "regen_capacity_mbs",
             "regen_status_string", "regen_last_error", "regen_abi_version", "regen_enhance_kernel_count",
-            "regen_enhance_scatter", "regen_trace_enable", "regen_trace_read", "regen_trace_filter"]
+            "regen_enhance_scatter", "regen_trace_enable", "regen_trace_read", "regen_trace_filter",
+            "regen_enhance_owned", "regen_scatter_bilinear"]
 
 
 class Geom(ctypes.Structure):
@@ -81,6 +82,8 @@ def _load():
     lib.regen_scatter_blend.argtypes = [P(Geom), P(PackParams), i32, vp, vp, vp, vp, i32, vp, i32, vp]
     lib.regen_enhance_scatter.argtypes = [vp, P(Geom), P(PackParams), vp, vp, i64, vp, vp, vp, vp, i32, vp, vp, sz,
                                           vp]
+    lib.regen_enhance_owned.argtypes = list(lib.regen_enhance_scatter.argtypes)
+    lib.regen_scatter_bilinear.argtypes = [P(Geom), i32, vp, vp, vp, i32, vp]
     lib.regen_workspace_size.argtypes = [i32, P(Geom), vp, vp, P(sz)]
     lib.regen_enhance_kernel_count.argtypes = [vp, P(PackParams), P(i32)]
     lib.regen_trace_enable.argtypes = [i32]
@@ -93,7 +96,8 @@ def _load():
     lib.regen_abi_version.restype = i32
     for name in ["regen_select_mbs", "regen_pack_regions", "regen_sr_create", "regen_sr_destroy",
                  "regen_stitch_bins", "regen_enhance_packed", "regen_scatter_blend", "regen_workspace_size",
-                 "regen_enhance_kernel_count", "regen_enhance_scatter", "regen_trace_enable", "regen_trace_read", "regen_trace_filter"]:
+                 "regen_enhance_kernel_count", "regen_enhance_scatter", "regen_trace_enable", "regen_trace_read", "regen_trace_filter",
+                 "regen_enhance_owned", "regen_scatter_bilinear"]:
         getattr(lib, name).restype = ctypes.c_int
     return lib
 
@@ -190,6 +194,18 @@ def enhance_scatter(sr, geom, params, frames, boxes, max_boxes, num_boxes, num_b
     _check(lib.regen_enhance_scatter(sr.handle, ctypes.byref(geom), ctypes.byref(params), _ptr(frames), _ptr(boxes),
                                      max_boxes, _ptr(num_boxes), _ptr(num_bins), _ptr(mb_owner), _ptr(out), out_dtype,
                                      _ptr(status), _ptr(ws), ws.numel(), _stream(stream)), "regen_enhance_scatter")
+
+
+def enhance_owned(sr, geom, params, frames, boxes, max_boxes, num_boxes, num_bins, mb_owner, out, out_dtype, status,
+                  ws, stream=None):
+    _check(lib.regen_enhance_owned(sr.handle, ctypes.byref(geom), ctypes.byref(params), _ptr(frames), _ptr(boxes),
+                                   max_boxes, _ptr(num_boxes), _ptr(num_bins), _ptr(mb_owner), _ptr(out), out_dtype,
+                                   _ptr(status), _ptr(ws), ws.numel(), _stream(stream)), "regen_enhance_owned")
+
+
+def scatter_bilinear(geom, scale, frames, mb_owner, out, out_dtype, stream=None):
+    _check(lib.regen_scatter_bilinear(ctypes.byref(geom), scale, _ptr(frames), _ptr(mb_owner), _ptr(out), out_dtype,
+                                      _stream(stream)), "regen_scatter_bilinear")
 
 
 def scatter_blend(geom, params, scale, frames, boxes, mb_owner, hr_bins, hr_dtype, out, out_dtype, stream=None):
@@ -302,6 +318,19 @@ class Pipeline:
         out = self.out if out is None else out
         enhance_scatter(self.sr, self.geom, self.pack, frames, self.boxes, self.max_boxes, self.counts[1:2],
                         self.num_bins, self.owner, out, self.out_dtype, self.status, self.ws, stream)
+        return out
+
+    def enhance_owned(self, frames, out=None, stream=None):
+        """regen_enhance_owned: the SR pixels of the owned MBs only."""
+        out = self.out if out is None else out
+        enhance_owned(self.sr, self.geom, self.pack, frames, self.boxes, self.max_boxes, self.counts[1:2],
+                      self.num_bins, self.owner, out, self.out_dtype, self.status, self.ws, stream)
+        return out
+
+    def scatter_bilinear(self, frames, out=None, stream=None):
+        """regen_scatter_bilinear: the bilinear pixels (MBs without an owner) only."""
+        out = self.out if out is None else out
+        scatter_bilinear(self.geom, self.scale, frames, self.owner, out, self.out_dtype, stream)
         return out
 
     def run(self, importance, frames, out=None, stream=None, fused=True):

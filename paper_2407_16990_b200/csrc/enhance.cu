@@ -619,11 +619,13 @@ extern "C" regen_status regen_enhance_packed(void* sr, const regen_geom* geom, c
                      (cudaStream_t)stream, nullptr);
 }
 
-extern "C" regen_status regen_enhance_scatter(void* sr, const regen_geom* geom, const regen_pack_params* p,
-                                              const uint8_t* d_frames, const regen_box* d_boxes, int64_t max_boxes,
-                                              const int64_t* d_num_boxes, const int32_t* d_num_bins,
-                                              const int32_t* d_mb_owner, void* d_out, int32_t out_dtype,
-                                              int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream) {
+namespace regen {
+// parts: 1 = the owned MBs' SR pixels, 2 = the bilinear pixels (the rest), 3 = the whole HR frames
+static regen_status enhance_scatter_parts(void* sr, const regen_geom* geom, const regen_pack_params* p,
+                                          const uint8_t* d_frames, const regen_box* d_boxes, int64_t max_boxes,
+                                          const int64_t* d_num_boxes, const int32_t* d_num_bins,
+                                          const int32_t* d_mb_owner, void* d_out, int32_t out_dtype,
+                                          int32_t* d_status, void* d_ws, size_t ws_bytes, cudaStream_t s, int parts) {
   REGEN_REQUIRE(sr != nullptr, "null SR handle");
   regen_status st = validate_geom(geom);
   if (st != REGEN_OK) return st;
@@ -638,7 +640,6 @@ extern "C" regen_status regen_enhance_scatter(void* sr, const regen_geom* geom, 
   const size_t need = enhance_scatter_ws_bytes(net, *p);
   REGEN_REQUIRE(d_ws && ws_bytes >= need, "workspace too small (%zu < %zu)", ws_bytes, need);
   EnhanceBufs e = enhance_bufs(net, *p, d_ws);
-  cudaStream_t s = (cudaStream_t)stream;
   if (fold_enabled(net, p->bin_w)) {
     FoldFrameArgs fa;
     fa.geom = *geom;
@@ -648,13 +649,32 @@ extern "C" regen_status regen_enhance_scatter(void* sr, const regen_geom* geom, 
     fa.out = d_out;
     fa.out_dtype = out_dtype;
     st = enhance_run(net, geom, p, d_frames, d_boxes, max_boxes, d_num_boxes, d_num_bins, nullptr, e, s, &fa);
-    if (st != REGEN_OK) return st;
+    if (st != REGEN_OK || !(parts & 2)) return st;
     return scatter_launch(*geom, *p, net->cfg.scale, d_frames, d_boxes, d_mb_owner, nullptr, net->cfg.dtype, d_out,
-                          out_dtype, true, s);
+                          out_dtype, 1, s);
   }
   void* hr = (uint8_t*)d_ws + (e.bytes + 255) / 256 * 256;
   st = enhance_run(net, geom, p, d_frames, d_boxes, max_boxes, d_num_boxes, d_num_bins, hr, e, s, nullptr);
   if (st != REGEN_OK) return st;
   return scatter_launch(*geom, *p, net->cfg.scale, d_frames, d_boxes, d_mb_owner, hr, net->cfg.dtype, d_out, out_dtype,
-                        false, s);
+                        parts == 3 ? 0 : 2, s);
+}
+}  // namespace regen
+
+extern "C" regen_status regen_enhance_scatter(void* sr, const regen_geom* geom, const regen_pack_params* p,
+                                              const uint8_t* d_frames, const regen_box* d_boxes, int64_t max_boxes,
+                                              const int64_t* d_num_boxes, const int32_t* d_num_bins,
+                                              const int32_t* d_mb_owner, void* d_out, int32_t out_dtype,
+                                              int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream) {
+  return enhance_scatter_parts(sr, geom, p, d_frames, d_boxes, max_boxes, d_num_boxes, d_num_bins, d_mb_owner, d_out,
+                               out_dtype, d_status, d_ws, ws_bytes, (cudaStream_t)stream, 3);
+}
+
+extern "C" regen_status regen_enhance_owned(void* sr, const regen_geom* geom, const regen_pack_params* p,
+                                            const uint8_t* d_frames, const regen_box* d_boxes, int64_t max_boxes,
+                                            const int64_t* d_num_boxes, const int32_t* d_num_bins,
+                                            const int32_t* d_mb_owner, void* d_out, int32_t out_dtype,
+                                            int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream) {
+  return enhance_scatter_parts(sr, geom, p, d_frames, d_boxes, max_boxes, d_num_boxes, d_num_bins, d_mb_owner, d_out,
+                               out_dtype, d_status, d_ws, ws_bytes, (cudaStream_t)stream, 1);
 }

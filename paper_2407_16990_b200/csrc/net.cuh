@@ -95,7 +95,7 @@ regen_status fold_combine_launch(const SRNet* net, const void* P, void* hr_bins,
                                  const FoldFrameArgs* fa = nullptr);
 regen_status scatter_launch(const regen_geom& g, const regen_pack_params& p, int scale, const uint8_t* d_frames,
                             const regen_box* d_boxes, const int32_t* d_mb_owner, const void* d_hr_bins, int hr_dtype,
-                            void* d_out, int out_dtype, bool skip_owned, cudaStream_t s);
+                            void* d_out, int out_dtype, int mode, cudaStream_t s);   // mode: 0 all, 1 bilinear only, 2 owned only
 void resblock_tc_release(SRNet* net);
 regen_status resblock_tc_launch(const SRNet* net, int block, const void* in, void* out, const uint32_t* mbits,
                                 int max_bins, const int32_t* d_num_bins, int bin_w, int bin_h, int* counter,

@@ -12,6 +12,8 @@
 //                      owners apply the guillotine remainders (D6). Unopened bins are implicit.
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace regen {
@@ -108,19 +110,22 @@ __device__ int region_pieces(const BoxArgs& a, int64_t r, int64_t box_base) {
   return produced;
 }
 
+// warp-stride over the regions actually found (device-side count; the grid is sized to the GPU, not
+// to the region capacity)
 __global__ void box_count_kernel(BoxArgs a) {
-  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int64_t nr = min(*a.num_regions, a.max_regions);
-  if (r >= nr) return;
-  const int n = region_pieces<false>(a, r, 0);
-  if ((threadIdx.x & 31) == 0) a.region_count[r] = n;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < nr; r += nw) {
+    const int n = region_pieces<false>(a, r, 0);
+    if ((threadIdx.x & 31) == 0) a.region_count[r] = n;
+  }
 }
 
 __global__ void box_write_kernel(BoxArgs a) {
-  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int64_t nr = min(*a.num_regions, a.max_regions);
-  if (r >= nr) return;
-  region_pieces<true>(a, r, a.region_off[r]);
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < nr; r += nw)
+    region_pieces<true>(a, r, a.region_off[r]);
 }
 
 __global__ void clamp_count_kernel(const int64_t* num_regions, int64_t max_regions, int32_t* region_count,
@@ -181,11 +186,12 @@ __global__ void __launch_bounds__(256) sort_rank_kernel(regen_box* boxes, const 
 
 // ------------------------------------------------------------------------------------ pack
 
-constexpr int PACK_POOL = 8192;   // live free areas (SMEM), kept compact
-constexpr int PACK_DIMS = 8192;   // box footprints + indices staged in SMEM in packing order
+constexpr int PACK_POOL = 8192;   // live free areas beyond the register slots (global workspace, L1/L2)
+constexpr int PACK_DIMS = 4096;   // box footprints + indices staged in SMEM in packing order (32 KB)
 
 struct PackArgs {
   regen_box* boxes;
+  uint64_t* pool;           // [2][PACK_POOL] keys then rects of the slots beyond the registers (workspace)
   const int32_t* order;
   const int64_t* num_boxes;
   int64_t max_boxes;
@@ -195,17 +201,26 @@ struct PackArgs {
   int prof;   // REGEN_PACK_PROF=1: print per-phase cycle counts
 };
 
-// One warp. The live free areas of the opened bins form a compact pool in SMEM: key = bin << 32 |
-// creation sequence (unique; its minimum is the first area in (bin, seq) order, D12), rect = x | y<<16
-// | w<<32 | h<<48. Per box: lanes scan the pool (fit test unrotated or rotated), a warp
-// min-reduction picks the first fit, every lane replays the placement and lane 0 applies the
-// guillotine remainders (D6): the consumed area is overwritten by the first kept remainder (or by the
-// pool's last entry), the second is appended. Unopened bins are implicit (opened lazily in order).
+// One warp. The live free areas of the opened bins form a compact pool: key = bin << 32 | creation
+// sequence (unique; its minimum is the first area in (bin, seq) order, D12), rect = x | y<<16 | w<<32
+// | h<<48. Slot s < 32 lives in a REGISTER of lane s (the pool holds ~15 areas on the paper's maps
+// after pruning), slots >= 32 in a global overflow array (L1-resident). Per box: lanes test their
+// areas (fit unrotated or rotated), a warp min-reduction picks the first fit, every lane
+// replays the placement and the guillotine remainders (D6) on identical state: the consumed area's
+// slot takes the first kept remainder (or the pool's last entry), the second is appended. Unopened
+// bins are implicit (opened lazily in order). The packer is one dependent chain per box, so it is
+// written for the fewest instructions on that chain: the next footprint is prefetched, a register
+// slot update is one predicated move, the clock probes run only under REGEN_PACK_PROF=1.
+__device__ __forceinline__ bool fits(uint64_t r, int pw, int ph) {
+  const int fw = (int)((r >> 32) & 0xFFFF), fh = (int)(r >> 48);
+  return (fw >= pw && fh >= ph) || (fw >= ph && fh >= pw);
+}
+
 __global__ void __launch_bounds__(32, 1) pack_kernel(PackArgs a) {
   extern __shared__ uint8_t psm[];
-  uint64_t* key = (uint64_t*)psm;                       // PACK_POOL
-  uint64_t* rect = key + PACK_POOL;                     // PACK_POOL
-  uint32_t* dims = (uint32_t*)(rect + PACK_POOL);       // (w+g) | (h+g)<<16 of the oi-th box in order
+  uint64_t* key = a.pool;                               // slots >= 32 (rarely used)
+  uint64_t* rect = a.pool + PACK_POOL;
+  uint32_t* dims = (uint32_t*)psm;                      // (w+g) | (h+g)<<16 of the oi-th box in order
   int32_t* ords = (int32_t*)(dims + PACK_DIMS);         // box index of the oi-th box in order
   const int lane = threadIdx.x;
   const int64_t n = min(*a.num_boxes, a.max_boxes);
@@ -222,122 +237,136 @@ __global__ void __launch_bounds__(32, 1) pack_kernel(PackArgs a) {
       ords[i] = bi;
     }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    mA = min(mA, __shfl_xor_sync(0xffffffffu, mA, o));
-    mB = min(mB, __shfl_xor_sync(0xffffffffu, mB, o));
-  }
+  mA = __reduce_min_sync(0xffffffffu, mA);
+  mB = __reduce_min_sync(0xffffffffu, mB);
   __syncwarp();
+  uint64_t rk = ~0ull, rr = 0ull;   // this lane's register slot: empty never fits, never wins
   const int FW = a.bin_w - 1, FH = a.bin_h + a.gutter;   // a fresh bin's free area (x=1, y=0)
-  int hw = 0;        // live areas: [0, hw)
+  int hw = 0;        // live areas: slots [0, hw)
   int opened = 0;    // bins opened (lazily, in index order)
-  uint64_t seq = 0;
+  uint32_t seq = 0;
   int used = 0;
   bool overflow = false;
   long long c_scan = 0, c_dec = 0, c_upd = 0, hw_sum = 0;
-  for (int64_t oi = 0; oi < n; ++oi) {
-    const long long t0 = clock64();
-    int pw, ph, b;
+  int npw = 0, nph = 0, nb = 0;
+  auto fetch = [&](int64_t oi) {
+    if (oi >= n) return;
     if (oi < PACK_DIMS) {
       const uint32_t d = dims[oi];
-      pw = (int)(d & 0xFFFF);
-      ph = (int)(d >> 16);
-      b = ords[oi];
+      npw = (int)(d & 0xFFFF);
+      nph = (int)(d >> 16);
+      nb = ords[oi];
     } else {
-      b = a.order[oi];
-      pw = a.boxes[b].w + a.gutter;
-      ph = a.boxes[b].h + a.gutter;
+      nb = a.order[oi];
+      npw = a.boxes[nb].w + a.gutter;
+      nph = a.boxes[nb].h + a.gutter;
     }
-    uint64_t best = ~0ull, brect = 0;
-    int bslot = -1;
-    // 4 independent SMEM loads in flight per lane per step
-    for (int s0 = lane; s0 < hw; s0 += 128) {
-      uint64_t kk[4], rr[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int s = s0 + 32 * u;
-        kk[u] = s < hw ? key[s] : ~0ull;
-        rr[u] = s < hw ? rect[s] : 0ull;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int fw = (int)((rr[u] >> 32) & 0xFFFF), fh = (int)(rr[u] >> 48);
-        if (((fw >= pw && fh >= ph) || (fw >= ph && fh >= pw)) && kk[u] < best) {
-          best = kk[u]; brect = rr[u]; bslot = s0 + 32 * u;
-        }
-      }
+  };
+  fetch(0);
+  for (int64_t oi = 0; oi < n; ++oi) {
+    long long t0 = 0;
+    if (a.prof) t0 = clock64();
+    const int pw = npw, ph = nph, b = nb;
+    fetch(oi + 1);   // prefetch: off the dependent chain
+    uint64_t best = fits(rr, pw, ph) ? rk : ~0ull;
+    uint64_t brect = rr;
+    int bslot = lane;
+    for (int s = 32 + lane; s < hw; s += 32) {   // overflow slots
+      const uint64_t kk = key[s - 32], rq = rect[s - 32];
+      if (fits(rq, pw, ph) && kk < best) { best = kk; brect = rq; bslot = s; }
     }
-    const long long t1 = clock64();
-    hw_sum += hw;
+    long long t1 = 0;
+    if (a.prof) { t1 = clock64(); hw_sum += hw; }
     // 64-bit warp min as two 32-bit REDUX (bin in the high word, sequence in the low word)
     const uint32_t bhi = (uint32_t)(best >> 32);
     const uint32_t mhi = __reduce_min_sync(0xffffffffu, bhi);
     const uint32_t mlo = __reduce_min_sync(0xffffffffu, bhi == mhi ? (uint32_t)best : 0xFFFFFFFFu);
-    const uint64_t wbest = ((uint64_t)mhi << 32) | mlo;
-    int fx = 0, fy = 0, fw = 0, fh = 0, bin = 0, slot = -1;
-    bool place = false;
-    if (wbest != ~0ull) {
+    int fx, fy, fw, fh, bin, slot = -1;
+    bool place = true;
+    if (mhi != 0xFFFFFFFFu || mlo != 0xFFFFFFFFu) {
       // the lane holding the winner broadcasts its rect and slot
-      const uint32_t holder = __ballot_sync(0xffffffffu, best == wbest);
-      const int hl = __ffs(holder) - 1;
-      brect = __shfl_sync(0xffffffffu, brect, hl);
+      const int hl = __ffs(__ballot_sync(0xffffffffu, bhi == mhi && (uint32_t)best == mlo)) - 1;
+      const uint32_t rlo = __shfl_sync(0xffffffffu, (uint32_t)brect, hl);
+      const uint32_t rhi = __shfl_sync(0xffffffffu, (uint32_t)(brect >> 32), hl);
       slot = __shfl_sync(0xffffffffu, bslot, hl);
-      fx = (int)(brect & 0xFFFF); fy = (int)((brect >> 16) & 0xFFFF);
-      fw = (int)((brect >> 32) & 0xFFFF); fh = (int)(brect >> 48);
-      bin = (int)(wbest >> 32);
-      place = true;
+      fx = (int)(rlo & 0xFFFF); fy = (int)(rlo >> 16);
+      fw = (int)(rhi & 0xFFFF); fh = (int)(rhi >> 16);
+      bin = (int)mhi;
     } else if (opened < a.max_bins && ((FW >= pw && FH >= ph) || (FW >= ph && FH >= pw))) {
       bin = opened++;
       fx = 1; fy = 0; fw = FW; fh = FH;
-      place = true;
+    } else {
+      place = false;
+      fx = fy = fw = fh = bin = 0;
     }
-    const long long t2 = clock64();
-    c_scan += t1 - t0;
-    c_dec += t2 - t1;
+    long long t2 = 0;
+    if (a.prof) {
+      t2 = clock64();
+      c_scan += t1 - t0;
+      c_dec += t2 - t1;
+    }
     if (place) {
       const bool rot = !(fw >= pw && fh >= ph);
       const int uw = rot ? ph : pw, uh = rot ? pw : ph;
       used = max(used, bin + 1);
-      // InnerFree (D6): guillotine remainders
-      const int64_t v_a = (int64_t)(fw - uw) * fh, v_b = (int64_t)uw * (fh - uh);
-      const int64_t h_a = (int64_t)fw * (fh - uh), h_b = (int64_t)(fw - uw) * uh;
+      if (lane == 0) {   // bin, bx / by, rotated: two 8-B stores
+        int2* pl = reinterpret_cast<int2*>(&a.boxes[b].bin);
+        pl[0] = make_int2(bin, fx);
+        pl[1] = make_int2(fy, rot ? 1 : 0);
+      }
+      // InnerFree (D6): guillotine remainders; vertical = {right full height, bottom}, horizontal =
+      // {bottom full width, right}; the option whose larger remainder is larger wins, ties vertical
+      const int dw = fw - uw, dh = fh - uh;
+      const int64_t v_a = (int64_t)dw * fh, v_b = (int64_t)uw * dh;
+      const int64_t h_a = (int64_t)fw * dh, h_b = (int64_t)dw * uh;
       const bool vert = max(v_a, v_b) >= max(h_a, h_b);
-      int rx[2], ry[2], rw[2], rh[2];
-      if (vert) {
-        rx[0] = fx + uw; ry[0] = fy; rw[0] = fw - uw; rh[0] = fh;
-        rx[1] = fx; ry[1] = fy + uh; rw[1] = uw; rh[1] = fh - uh;
-      } else {
-        rx[0] = fx; ry[0] = fy + uh; rw[0] = fw; rh[0] = fh - uh;
-        rx[1] = fx + uw; ry[1] = fy; rw[1] = fw - uw; rh[1] = uh;
-      }
-      if (lane == 0) {
-        a.boxes[b].bin = bin;
-        a.boxes[b].bx = fx;
-        a.boxes[b].by = fy;
-        a.boxes[b].rotated = rot ? 1 : 0;
-      }
-      // every lane replays the pool bookkeeping (identical state); lane 0 performs the SMEM writes
+      const int rx0 = vert ? fx + uw : fx, ry0 = vert ? fy : fy + uh;
+      const int rw0 = vert ? dw : fw, rh0 = vert ? fh : dh;
+      const int rx1 = vert ? fx : fx + uw, ry1 = vert ? fy + uh : fy;
+      const int rw1 = vert ? uw : dw, rh1 = vert ? dh : uh;
       int free_slot = slot;   // the consumed area's slot, to be refilled
+#pragma unroll
       for (int t = 0; t < 2; ++t) {
-        if (rw[t] <= 0 || rh[t] <= 0) continue;
-        const uint64_t sq = seq++;   // sequence numbers follow the oracle's creation order
-        if (min(rw[t], rh[t]) < mA || max(rw[t], rh[t]) < mB) continue;   // unusable: never stored
+        const int rx = t ? rx1 : rx0, ry = t ? ry1 : ry0, rw = t ? rw1 : rw0, rh = t ? rh1 : rh0;
+        if (rw <= 0 || rh <= 0) continue;
+        const uint32_t sq = seq++;   // sequence numbers follow the oracle's creation order
+        if (min(rw, rh) < mA || max(rw, rh) < mB) continue;   // unusable: never stored
         int dst;
         if (free_slot >= 0) { dst = free_slot; free_slot = -1; }
-        else if (hw < PACK_POOL) dst = hw++;
+        else if (hw < PACK_POOL + 32) dst = hw++;
         else { overflow = true; continue; }
-        if (lane == 0) {
-          key[dst] = ((uint64_t)bin << 32) | (uint32_t)sq;
-          rect[dst] = (uint64_t)rx[t] | ((uint64_t)ry[t] << 16) | ((uint64_t)rw[t] << 32) | ((uint64_t)rh[t] << 48);
+        const uint64_t nk = ((uint64_t)bin << 32) | sq;
+        const uint64_t nr = (uint64_t)(uint32_t)(rx | (ry << 16)) | ((uint64_t)(uint32_t)(rw | (rh << 16)) << 32);
+        if (dst < 32) {
+          if (lane == dst) { rk = nk; rr = nr; }
+        } else if (lane == 0) {
+          key[dst - 32] = nk;
+          rect[dst - 32] = nr;
         }
       }
       if (free_slot >= 0) {   // nothing refilled the consumed slot: move the last live area into it
         --hw;
-        if (lane == 0 && free_slot != hw) { key[free_slot] = key[hw]; rect[free_slot] = rect[hw]; }
+        if (free_slot != hw) {
+          uint64_t lk, lq;
+          if (hw < 32) {
+            lk = __shfl_sync(0xffffffffu, rk, hw);
+            lq = __shfl_sync(0xffffffffu, rr, hw);
+          } else {
+            lk = key[hw - 32];
+            lq = rect[hw - 32];
+          }
+          if (free_slot < 32) {
+            if (lane == free_slot) { rk = lk; rr = lq; }
+          } else if (lane == 0) {
+            key[free_slot - 32] = lk;
+            rect[free_slot - 32] = lq;
+          }
+        }
+        if (hw < 32 && lane == hw) { rk = ~0ull; rr = 0ull; }   // the vacated register slot is empty
       }
     }
-    __syncwarp();   // lane 0's pool writes are visible to every lane before the next scan
-    c_upd += clock64() - t2;
+    __syncwarp();   // lane 0's overflow-slot writes are visible to every lane before the next scan
+    if (a.prof) c_upd += clock64() - t2;
   }
   if (a.prof && lane == 0)
     printf("[pack-prof] boxes %lld scan %lld dec %lld upd %lld cycles, mean live areas %.1f, bins %d\n", (long long)n,
@@ -359,14 +388,16 @@ __global__ void owner_fix_kernel(int32_t* owner, int64_t n_mbs, const regen_box*
 }
 
 static size_t pack_ws(const regen_geom& g, int64_t max_regions, void* base, int32_t** rcount, int64_t** roff,
-                      int64_t** nreg) {
+                      int64_t** nreg, uint64_t** pool = nullptr) {
   Carver c(base);
   int32_t* rc = c.take<int32_t>((size_t)max_regions + 1);
   int64_t* ro = c.take<int64_t>((size_t)max_regions + 1);
   int64_t* nr = c.take<int64_t>(4);
+  uint64_t* pl = c.take<uint64_t>(2 * (size_t)PACK_POOL);
   if (rcount) *rcount = rc;
   if (roff) *roff = ro;
   if (nreg) *nreg = nr;
+  if (pool) *pool = pl;
   (void)g;
   return c.off + 256;
 }
@@ -404,7 +435,8 @@ extern "C" regen_status regen_pack_regions(const regen_geom* geom, const regen_p
   cudaStream_t s = (cudaStream_t)stream;
   int32_t* rcount;
   int64_t *roff, *nreg;
-  pack_ws(g, max_regions, d_ws, &rcount, &roff, &nreg);
+  uint64_t* pool;
+  pack_ws(g, max_regions, d_ws, &rcount, &roff, &nreg, &pool);
   REGEN_CUDA(cudaMemsetAsync(d_mb_owner, 0xFF, sizeof(int32_t) * (size_t)n_mbs(g), s));
 
   BoxArgs a;
@@ -427,8 +459,8 @@ extern "C" regen_status regen_pack_regions(const regen_geom* geom, const regen_p
   a.mb = g.mb;
   a.expand = p->expand;
   a.P = p->partition_mb;
-  const int warps_per_block = 8;
-  const unsigned nblk = (unsigned)((max_regions + warps_per_block - 1) / warps_per_block);
+  const int warps_per_block = 4;   // 128 threads x <= 56 registers: fits beside a resident SR conv CTA
+  const unsigned nblk = (unsigned)std::min<int64_t>((max_regions + warps_per_block - 1) / warps_per_block, 148 * 4);
   {
     REGEN_TRACE("clamp_count", s);
     clamp_count_kernel<<<1, 1, 0, s>>>(d_num_regions, max_regions, rcount, nreg);
@@ -441,7 +473,7 @@ extern "C" regen_status regen_pack_regions(const regen_geom* geom, const regen_p
   REGEN_LAUNCH_CHECK();
   {
     REGEN_TRACE("scan_boxes", s);
-    scan_counts64_kernel<<<1, 1024, 0, s>>>(rcount, nreg, roff, d_num_boxes);
+    scan_counts64_kernel<<<1, 256, 0, s>>>(rcount, nreg, roff, d_num_boxes);
   }
   REGEN_LAUNCH_CHECK();
   {
@@ -457,6 +489,7 @@ extern "C" regen_status regen_pack_regions(const regen_geom* geom, const regen_p
   REGEN_LAUNCH_CHECK();
   PackArgs k;
   k.boxes = d_boxes;
+  k.pool = pool;
   k.order = d_order;
   k.num_boxes = d_num_boxes;
   k.max_boxes = max_boxes;
@@ -470,8 +503,7 @@ extern "C" regen_status regen_pack_regions(const regen_geom* geom, const regen_p
     const char* e = getenv("REGEN_PACK_PROF");
     k.prof = (e && e[0] == '1') ? 1 : 0;
   }
-  const size_t smem = (size_t)PACK_POOL * 16 + (size_t)PACK_DIMS * 8;
-  REGEN_CUDA(cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const size_t smem = (size_t)PACK_DIMS * 8;   // dims + ords
   {
     REGEN_TRACE("pack", s);
     pack_kernel<<<1, 32, smem, s>>>(k);

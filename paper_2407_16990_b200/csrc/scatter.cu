@@ -2,6 +2,8 @@
 // back to bi-linear-interpolated non-regions". Every HR pixel is written exactly once: the bilinear
 // value (D10: half-pixel centres, edge clamp, fp32) or, inside the HR square of an owned selected MB,
 // the box's HR bin pixel (un-rotated, D7). Stores are 16-B vectors (bf16) / 32-B (fp32).
+#include <string.h>
+
 #include "net.cuh"
 
 namespace regen {
@@ -18,6 +20,8 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+enum { SC_ALL = 0, SC_BILINEAR = 1, SC_OWNED = 2 };
+
 struct ScatterArgs {
   const uint8_t* frames;
   const regen_box* boxes;
@@ -26,7 +30,7 @@ struct ScatterArgs {
   void* out;
   int W, H, OW, OH, GW, GH, mb, s, bin_w, bin_h;
   float inv_s;
-  int skip_owned;   // regen_enhance_scatter: owned MBs were written by the fold combine
+  int mode;         // SC_ALL, SC_BILINEAR (owned MBs written elsewhere: the fold combine), SC_OWNED
 };
 
 // One CTA per (frame, LR row y) writes the S HR rows S*y .. S*y+S-1. The (at most three) LR rows
@@ -37,9 +41,11 @@ struct ScatterArgs {
 // of each sub-pixel phase compile-time (HR pixel X = S*x + j samples src = x + (j + 0.5)/S - 0.5:
 // columns (x-1, x) or (x, x+1) with a fixed fraction, clamped at the edges exactly as the oracle);
 // (3) coalesced 16-B copy-out (an MB's HR square is a whole number of chunks) skipping owned MB
-// squares, which get the owner box's HR bin pixels (SKIP = false) or nothing (SKIP:
+// squares, which get the owner box's HR bin pixels (SC_ALL, SC_OWNED) or nothing (SC_BILINEAR:
 // regen_enhance_scatter wrote them already). ~28 KB SMEM per CTA: 8 CTAs per SM.
-constexpr int SC_THREADS = 256;
+// 128 threads x <= 64 registers and ~28 KB SMEM per CTA, so a CTA fits beside a resident SR conv
+// CTA (the bilinear pass of batch k+1 runs concurrently with the SR of batch k, schedule.py)
+constexpr int SC_THREADS = 128;
 
 template <int S>
 struct Phase {   // sub-pixel phase j: source offset d (-1 or 0) and fraction
@@ -59,8 +65,8 @@ __device__ __forceinline__ void put2<float>(uint32_t* w, int k, float a, float b
   w[2 * k + 1] = __float_as_uint(b);
 }
 
-template <int S, typename TH, typename TO, bool SKIP>
-__global__ void __launch_bounds__(SC_THREADS) scatter_rows_kernel(ScatterArgs a) {
+template <int S, typename TH, typename TO, int MODE>
+__global__ void __launch_bounds__(SC_THREADS, 8) scatter_rows_kernel(ScatterArgs a) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int64_t sf = blockIdx.y;
   const int y = blockIdx.x;
@@ -75,7 +81,7 @@ __global__ void __launch_bounds__(SC_THREADS) scatter_rows_kernel(ScatterArgs a)
   uint8_t* lr = reinterpret_cast<uint8_t*>(own + (a.GW + 3) / 4 * 4);         // [3][W3p]
   const uint8_t* img = a.frames + sf * (int64_t)a.H * W3;
   // ---- 0. the (at most three) LR rows (16-B loads when aligned) and the owner row -> SMEM
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < (MODE == SC_OWNED ? 0 : 3); ++k) {
     const uint8_t* src = img + (size_t)min(max(y - 1 + k, 0), a.H - 1) * W3;
     uint8_t* dst = lr + k * W3p;
     if ((((uintptr_t)src) & 15) == 0) {
@@ -92,8 +98,9 @@ __global__ void __launch_bounds__(SC_THREADS) scatter_rows_kernel(ScatterArgs a)
   static_assert(MB_BYTES % 16 == 0, "MB squares must be whole 16-B chunks");
   const int row_bytes = a.OW * 3 * (int)sizeof(TO);
   const int n16 = row_bytes / 16;
+  if (MODE == SC_OWNED) __syncthreads();   // owner row staged
 #pragma unroll
-  for (int i = 0; i < S; ++i) {
+  for (int i = 0; i < (MODE == SC_OWNED ? 0 : S); ++i) {
     const int Y = y * S + i;
     // ---- 1. vertical pass (D10) of HR row i
     int yl0 = y + Phase<S>::d(i);
@@ -168,7 +175,7 @@ __global__ void __launch_bounds__(SC_THREADS) scatter_rows_kernel(ScatterArgs a)
         if (own[(2 * c) / MB_BYTES] < 0) reinterpret_cast<uint16_t*>(drow)[c] = reinterpret_cast<const uint16_t*>(srow)[c];
     }
   }
-  if (SKIP) return;
+  if (MODE == SC_BILINEAR) return;
   // ---- owned MBs: the box's HR bin pixels (un-rotated, D7), 8 pixels per thread
   const int HW = S * a.bin_w, HH = S * a.bin_h;
   const int nchunk = (a.OW + 7) / 8;
@@ -219,7 +226,7 @@ namespace regen {
 
 regen_status scatter_launch(const regen_geom& g, const regen_pack_params& p, int scale, const uint8_t* d_frames,
                             const regen_box* d_boxes, const int32_t* d_mb_owner, const void* d_hr_bins, int hr_dtype,
-                            void* d_out, int out_dtype, bool skip_owned, cudaStream_t s) {
+                            void* d_out, int out_dtype, int mode, cudaStream_t s) {
   ScatterArgs a;
   a.frames = d_frames;
   a.boxes = d_boxes;
@@ -237,10 +244,11 @@ regen_status scatter_launch(const regen_geom& g, const regen_pack_params& p, int
   a.bin_w = p.bin_w;
   a.bin_h = p.bin_h;
   a.inv_s = 1.0f / (float)scale;
-  a.skip_owned = skip_owned ? 1 : 0;
+  a.mode = mode;
   dim3 grid((unsigned)g.frame_h, (unsigned)n_frames(g));
   REGEN_REQUIRE(g.mb == 16, "scatter expects 16-pixel MBs");
   REGEN_REQUIRE(scale == 2 || scale == 3 || scale == 4, "scatter scale must be 2, 3 or 4");
+  REGEN_REQUIRE(n_frames(g) <= 65535, "scatter: at most 65535 frames per call");
   const size_t es = out_dtype == REGEN_DTYPE_BF16 ? 2 : 4;
   const size_t npair = ((size_t)g.frame_w + 1) / 2;
   const size_t row_words = (npair * 3 * scale * es / 2 + 3) / 4 * 4;
@@ -249,23 +257,30 @@ regen_status scatter_launch(const regen_geom& g, const regen_pack_params& p, int
   REGEN_REQUIRE(smem <= 200 * 1024, "frame too wide for the scatter kernel (%zu B SMEM)", smem);
   auto go = [&](auto kern) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    REGEN_TRACE(skip_owned ? "scatter_bilinear" : "scatter", s);
+    REGEN_TRACE(mode == SC_BILINEAR ? "scatter_bilinear" : (mode == SC_OWNED ? "scatter_owned" : "scatter"), s);
     kern<<<grid, SC_THREADS, smem, s>>>(a);
   };
   const bool bf_hr = hr_dtype == REGEN_DTYPE_BF16, bf_out = out_dtype == REGEN_DTYPE_BF16;
   using bf = __nv_bfloat16;
-#define SC_DISPATCH(S_)                                                              \
-  if (skip_owned) {                                                                  \
-    if (bf_out) go(scatter_rows_kernel<S_, bf, bf, true>);                           \
-    else go(scatter_rows_kernel<S_, bf, float, true>);                               \
+#define SC_DISPATCH(S_, M_)                                                          \
+  if (M_ == SC_BILINEAR) {                                                           \
+    if (bf_out) go(scatter_rows_kernel<S_, bf, bf, M_>);                             \
+    else go(scatter_rows_kernel<S_, bf, float, M_>);                                 \
   } else if (bf_hr) {                                                                \
-    if (bf_out) go(scatter_rows_kernel<S_, bf, bf, false>);                          \
-    else go(scatter_rows_kernel<S_, bf, float, false>);                              \
+    if (bf_out) go(scatter_rows_kernel<S_, bf, bf, M_>);                             \
+    else go(scatter_rows_kernel<S_, bf, float, M_>);                                 \
   } else {                                                                           \
-    if (bf_out) go(scatter_rows_kernel<S_, float, bf, false>);                       \
-    else go(scatter_rows_kernel<S_, float, float, false>);                           \
+    if (bf_out) go(scatter_rows_kernel<S_, float, bf, M_>);                          \
+    else go(scatter_rows_kernel<S_, float, float, M_>);                              \
   }
-  if (scale == 2) { SC_DISPATCH(2) } else if (scale == 3) { SC_DISPATCH(3) } else { SC_DISPATCH(4) }
+#define SC_MODES(S_)                                                                 \
+  if (mode == SC_BILINEAR) { SC_DISPATCH(S_, SC_BILINEAR) }                          \
+  else if (mode == SC_OWNED) { SC_DISPATCH(S_, SC_OWNED) }                           \
+  else { SC_DISPATCH(S_, SC_ALL) }
+  REGEN_REQUIRE(mode == SC_ALL || mode == SC_BILINEAR || mode == SC_OWNED, "bad scatter mode");
+  REGEN_REQUIRE(mode == SC_BILINEAR || d_hr_bins != nullptr, "scatter: HR bins required");
+  if (scale == 2) { SC_MODES(2) } else if (scale == 3) { SC_MODES(3) } else { SC_MODES(4) }
+#undef SC_MODES
 #undef SC_DISPATCH
   REGEN_LAUNCH_CHECK();
   return REGEN_OK;
@@ -284,6 +299,20 @@ extern "C" regen_status regen_scatter_blend(const regen_geom* geom, const regen_
   REGEN_REQUIRE(hr_dtype == REGEN_DTYPE_BF16 || hr_dtype == REGEN_DTYPE_FP32, "bad hr dtype");
   REGEN_REQUIRE(out_dtype == REGEN_DTYPE_BF16 || out_dtype == REGEN_DTYPE_FP32, "bad out dtype");
   REGEN_REQUIRE(d_frames && d_boxes && d_mb_owner && d_hr_bins && d_out, "null device pointer");
-  return scatter_launch(*geom, *p, scale, d_frames, d_boxes, d_mb_owner, d_hr_bins, hr_dtype, d_out, out_dtype, false,
+  return scatter_launch(*geom, *p, scale, d_frames, d_boxes, d_mb_owner, d_hr_bins, hr_dtype, d_out, out_dtype, SC_ALL,
                         (cudaStream_t)stream);
+}
+
+extern "C" regen_status regen_scatter_bilinear(const regen_geom* geom, int32_t scale, const uint8_t* d_frames,
+                                               const int32_t* d_mb_owner, void* d_out, int32_t out_dtype,
+                                               void* stream) {
+  regen_status st = validate_geom(geom);
+  if (st != REGEN_OK) return st;
+  REGEN_REQUIRE(scale >= 2 && scale <= 4, "scale must be 2, 3 or 4");
+  REGEN_REQUIRE(out_dtype == REGEN_DTYPE_BF16 || out_dtype == REGEN_DTYPE_FP32, "bad out dtype");
+  REGEN_REQUIRE(d_frames && d_mb_owner && d_out, "null device pointer");
+  regen_pack_params p;
+  memset(&p, 0, sizeof(p));
+  return scatter_launch(*geom, p, scale, d_frames, nullptr, d_mb_owner, nullptr, REGEN_DTYPE_BF16, d_out, out_dtype,
+                        SC_BILINEAR, (cudaStream_t)stream);
 }

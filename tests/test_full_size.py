@@ -1,0 +1,99 @@
+"""Full-size parity (BASELINE.json configs at their stated sizes) in the launch configuration bench.py
+times: two pipelines on two streams, the steps captured into one CUDA graph and replayed
+(paper_2407_16990_b200.schedule.PipelinedRunner). The index path (selection, regions, boxes, order,
+placements, owners) is compared bit-exactly with the oracle over the whole workload; the HR frames
+on a sample the fp64 oracle can compute in seconds: every pixel of the owned MB squares of a few
+sampled boxes (SR, within the bf16 tolerance 2e-2 of north_star) and every bilinear pixel (owner -1)
+of a few sampled frames."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL_BF16 = 2e-2
+
+
+def _runner(wl, w):
+    import paper_2407_16990_b200 as rg
+    from paper_2407_16990_b200.schedule import PipelinedRunner
+
+    def make():
+        return rg.Pipeline(S=wl.S, F=wl.F, W=wl.W, H=wl.H, k=wl.k, bin_w=wl.bin_w, bin_h=wl.bin_h,
+                           max_bins=wl.max_bins, partition_mb=wl.partition_mb, scale=wl.sr.scale,
+                           channels=wl.sr.channels, n_resblocks=wl.sr.n_resblocks, weights=w, bf16=wl.sr.bf16,
+                           res_scale=wl.sr.res_scale)
+    return PipelinedRunner(make, "cuda")
+
+
+def _check_index(g, o):
+    assert g["status"] == 0
+    np.testing.assert_array_equal(g["sel"], o["sel"])
+    np.testing.assert_array_equal(g["labels"], o["labels"])
+    assert g["num_boxes"] == len(o["boxes"])
+    gb = g["boxes"]
+    cols = ["stream", "frame", "mx0", "my0", "mx1", "my1", "x0", "y0", "w", "h", "n_members", "region"]
+    np.testing.assert_array_equal(np.stack([gb[c] for c in cols], 1), o["boxes"])
+    np.testing.assert_array_equal(gb["density"].view(np.uint64), o["density"].view(np.uint64))
+    np.testing.assert_array_equal(g["order"], o["order"])
+    np.testing.assert_array_equal(np.stack([gb["bin"], gb["bx"], gb["by"], gb["rotated"]], 1), o["placement"])
+    assert g["num_bins"] == o["num_bins"]
+    np.testing.assert_array_equal(g["owner"], o["owner"])
+
+
+@pytest.mark.parametrize("cfg,n_box_sample,n_frame_sample", [("c2", 6, 3), ("c3", 4, 2), ("c5", 2, 2)])
+def test_full_size_graph_replay(cfg, n_box_sample, n_frame_sample):
+    wl = synth.CONFIGS[cfg]
+    seed = 21
+    imp_h = synth.importance_maps(wl.S, wl.F, wl.GH, wl.GW, seed)
+    fr_h = synth.frames_rgb8(wl.S, wl.F, wl.H, wl.W, seed)
+    w = synth.sr_weights(wl.sr, seed)
+    r = _runner(wl, w)
+    imp, fr = torch.from_numpy(imp_h).cuda(), torch.from_numpy(fr_h).cuda()
+    for q in r.pipes:
+        q.out.fill_(float("nan"))    # every HR pixel must be written by the step
+    r.run_eager(imp, fr, 2)          # warm (lazy allocations), then the captured schedule
+    torch.cuda.synchronize()
+    for q in r.pipes:
+        q.out.fill_(float("nan"))
+    g = r.capture(imp, fr, 3)
+    g.replay()
+    torch.cuda.synchronize()
+
+    o = oracle.index_path(imp_h, wl.W, wl.H, wl.k, partition_mb=wl.partition_mb, bin_w=wl.bin_w, bin_h=wl.bin_h,
+                          max_bins=wl.max_bins)
+    res = [q.host_results() for q in r.pipes]
+    for gres in res:
+        _check_index(gres, o)
+    outs = [q.out.float().cpu().numpy() for q in r.pipes]
+    assert np.array_equal(outs[0], outs[1], equal_nan=True), "the two pipelines disagree"
+    out = outs[0].reshape(-1, *outs[0].shape[2:])
+    assert not np.isnan(out).any(), "HR pixels left unwritten"
+
+    # sampled boxes: oracle SR of each (independent of its bin neighbours, D8), pasted by the oracle scatter
+    nb = o["num_bins"]
+    placed = np.nonzero(o["placement"][:, 0] >= 0)[0]
+    rng = np.random.default_rng(seed)
+    sample = np.sort(rng.choice(placed, size=min(n_box_sample, len(placed)), replace=False))
+    lr = oracle.gather(fr_h, o["boxes"], o["placement"], wl.bin_w, wl.bin_h, nb, wl.sr.bf16)
+    w64 = oracle.sr_weights_for(wl.sr, w)
+    hr = np.zeros((nb, wl.sr.scale * wl.bin_h, wl.sr.scale * wl.bin_w, 3))
+    for b in sample:
+        hr += oracle.enhance(wl.sr, w64, lr, o["boxes"], o["placement"], int(b), int(b) + 1)
+    s = wl.sr.scale
+    frames_of = sorted({int(o["boxes"][b, 0]) * wl.F + int(o["boxes"][b, 1]) for b in sample})
+    extra = rng.choice(wl.S * wl.F, size=n_frame_sample, replace=False)
+    owner = o["owner"].reshape(-1, wl.GH, wl.GW)
+    checked_sr = checked_bl = 0
+    for f in sorted(set(frames_of) | {int(x) for x in extra}):
+        ref = oracle.scatter(fr_h, o["boxes"], o["placement"], o["owner"], hr, s, wl.bin_w, wl.bin_h, f, f + 1)[0]
+        own = np.repeat(np.repeat(owner[f], 16 * s, 0), 16 * s, 1)[: s * wl.H, : s * wl.W]
+        m = (own < 0) | np.isin(own, sample)
+        d = np.abs(out[f] - ref)[m]
+        assert d.max() <= TOL_BF16, f"frame {f}: max err {d.max()}"
+        checked_sr += int(np.isin(own, sample).sum())
+        checked_bl += int((own < 0).sum())
+    assert checked_sr > 0 and checked_bl > 0

@@ -148,6 +148,17 @@ def _check_pixels(wl, seed=5, kind="blobs", box_sample=None, frame_sample=None):
     out = p.run(imp_t, fr_t, fused=False).clone()            # regen_enhance_packed + regen_scatter_blend
     out_fused = p.run(imp_t, fr_t, out=torch.empty_like(out))  # regen_enhance_scatter
     assert torch.equal(out_fused, out), "regen_enhance_scatter differs from the separate calls"
+    # the two halves (regen_enhance_owned + regen_scatter_bilinear, in either order) cover every HR
+    # pixel exactly once (NaN-filled buffer) and equal the fused call
+    for order in (0, 1):
+        out_split = torch.full_like(out, float("nan"))
+        if order == 0:
+            p.enhance_owned(fr_t, out=out_split)
+            p.scatter_bilinear(fr_t, out=out_split)
+        else:
+            p.scatter_bilinear(fr_t, out=out_split)
+            p.enhance_owned(fr_t, out=out_split)
+        assert torch.equal(out_split, out), "regen_enhance_owned + regen_scatter_bilinear differ from the fused call"
     g = p.host_results()
     o = _oracle_index(wl, imp)
     _assert_index_equal(g, o)
