@@ -29,6 +29,7 @@
 
 #include <vector>
 
+#include "fold_common.cuh"
 #include "tc_common.cuh"
 
 namespace regen {
@@ -60,21 +61,35 @@ struct Params {
   unsigned long long* prof; // optional wait-time counters (REGEN_TC_PROF=1), else null
   int* counter;             // dynamic unit scheduler (zeroed before the launch)
   int reverse;              // hand out units last-to-first (L2 reuse along a conv chain)
+  // ROLE_FOLDF only: the fused combine's frame output (fold_common.cuh store_frame)
+  const int64_t* fdst;      // [bin][bin_h][bin_w] HR frame index of an owned pixel | rot << 62, else -1
+  void* fout;               // HR frames
+  const float* tbias;       // tail bias [3]
+  int fout_fp32, fOW;
+  int ff_debug;             // timing experiments only (REGEN_FF_DEBUG): 1 = skip the combine arithmetic
 };
 
 // ------------------------------------------------------------------------------- compile-time shape
 template <int ROLE, int C, int CP, int R, int G, int T, int PS>
 struct Shape {
+  // ROLE_FOLDF: a band computes the partial-sum rows y0-1 .. y0+64 (66 rows, one halo row each side)
+  // of which the fused combine turns rows y0 .. y0+63 into HR pixels; bands advance by 64 rows
+  static constexpr bool FF = ROLE == ROLE_FOLDF;
+  static constexpr int BRS = FF ? 66 : BR;                              // output rows computed per band
+  static constexpr int BSTR = FF ? 64 : BR;                             // band stride
+  static constexpr int ROFF = FF ? -1 : 0;                              // first computed row - band origin
+  static constexpr int NT = FF ? NTHREADS + 256 : NTHREADS;             // + 8 combiner warps
   static constexpr bool HEAD = ROLE == ROLE_HEAD || ROLE == ROLE_TINY0;   // Cin = 3, dx packed into K
   static constexpr int KC = HEAD ? 1 : C / 16;                           // K-chunk pairs per dx
   static constexpr int NS = HEAD ? 2 : 3 * KC;                           // MMAs per input row and tile
   static constexpr int N = 3 * CP;
-  static constexpr int NG_OUT = BR / G;                                  // accumulator groups per band
-  static constexpr int NG_IN = (BR + 2 + G - 1) / G;                     // input groups per band
+  static constexpr int NG_OUT = BRS / G;                                 // accumulator groups per band
+  static constexpr int NG_IN = (BRS + 2 + G - 1) / G;                    // input groups per band
   static constexpr int OGR = R / G;                                      // accumulator groups in the ring
   static constexpr int DONE_LAG = G == 1 ? 2 : 1;                        // input groups until a group completes
   static constexpr bool BIAS_IN_ACC = ROLE != ROLE_UP;                   // slots re-armed with the bias
-  static_assert(R % G == 0 && BR % R == 0 && OGR >= 3 && OGR <= MAX_OG, "ring/group shape");
+  static_assert(R % G == 0 && BRS % R == 0 && OGR >= 3 && OGR <= MAX_OG, "ring/group shape");
+  static_assert(!FF || (T == 1 && G == 1 && (PS == 2 || PS == 3)), "fused fold: one tile, G = 1");
   static_assert(NG_IN >= NG_OUT + DONE_LAG, "every accumulator group completes inside the band");
   static_assert(T * R * CP <= 512 && N <= 256 && CP % 16 == 0, "TMEM / MMA shape");
   // slot of band-local output row j (accumulator sequence q0 + j, q0 = 0 mod R)
@@ -124,8 +139,14 @@ __host__ __device__ constexpr int up_column(int n) {
 }
 
 // ------------------------------------------------------------------------------- kernel
+constexpr int FF_NPR = 4;   // ROLE_FOLDF: partial-sum rows held in SMEM for the fused combine (4 x 20.8 KB,
+                            // leaving room for an 8-row input ring: the row loads are latency-bound)
+constexpr int FF_W = 130;   // ring row width: 128 pixels + a zero column each side (the combine's x
+                            // padding, so its 16-B loads need no bounds checks)
+
 template <int ROLE, int C, int CP, int R, int G, int T, int PS>
-__global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(ROLE == ROLE_FOLDF ? NTHREADS + 256 : NTHREADS, 1)
+    conv_tc_kernel(const __grid_constant__ Params p) {
   using S = Shape<ROLE, C, CP, R, G, T, PS>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t in_full[MAX_GSLOTS], in_empty[MAX_GSLOTS];
@@ -133,15 +154,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
   __shared__ __align__(8) uint64_t b_full[2], b_empty[2];
   __shared__ uint32_t tmem_base_sh;
   __shared__ __align__(16) float bias_sm[768];   // bias per accumulator column (all chunks)
+  __shared__ __align__(8) uint64_t prow_full[FF_NPR], prow_empty[FF_NPR];   // ROLE_FOLDF partial-sum rows
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cin8 = S::HEAD ? 1 : C / 8;
   const uint32_t row_bytes = (uint32_t)cin8 * p.Wr * 16;
   const uint32_t grp_bytes = row_bytes * G;
   const uint32_t ngs = (uint32_t)p.ngs, gsm = ngs - 1, gslog = (uint32_t)p.gslog;
-  // SMEM: [1 KB guard][ngs x G rows][B image]
+  // SMEM: [1 KB guard][ngs x G rows][B image(s)][ROLE_FOLDF: FF_NPR partial-sum rows]
   uint8_t* ring = smem_raw + 1024;
   uint8_t* bimg = ring + ngs * grp_bytes;
+  uint8_t* pring = bimg + (p.nchunk > 1 ? 2u : 1u) * p.b_bytes;   // [FF_NPR][CP/8][Wr][16 B]
+  constexpr uint32_t PROW_BYTES = (uint32_t)CP / 8 * FF_W * 16;    // T == 1: Wr == 128 (+2 zero columns)
   // units are (bin, band, chunk), chunk fastest (the chunks of a band re-read its input rows from L2),
   // over the bins actually used; B images are double-buffered per unit when there are several chunks.
   // Units are handed out by
@@ -157,7 +181,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
     for (int i = 0; i < (int)ngs; ++i) { mbar_init(&in_full[i], 1); mbar_init(&in_empty[i], 1); }
     for (int i = 0; i < S::OGR; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
     for (int i = 0; i < 2; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
-    for (int i = 0; i < 4; ++i) { mbar_init(&unit_full[i], 1); mbar_init(&unit_empty[i], 9); }
+    for (int i = 0; i < 4; ++i) { mbar_init(&unit_full[i], 1); mbar_init(&unit_empty[i], S::FF ? 17 : 9); }
+    // a partial-sum row is written by one epilogue quad (4 warp arrivals) and read by the three
+    // combines of rows r-1, r, r+1 (3 x 4 warp arrivals; band-edge rows get the missing ones from
+    // the edge combines)
+    if (S::FF)
+      for (int i = 0; i < FF_NPR; ++i) { mbar_init(&prow_full[i], 4); mbar_init(&prow_empty[i], 12); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -167,7 +196,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
   // bias in accumulator-column order: chunk c column n = global column c*CP + n. Upsampler chunks are
   // (sub-row i, channel group g) with columns n = j*CG + e (sub-column j, channel g*CG + e): see
   // up_column() — each chunk then writes whole HR pixels of CG channels for all sub-columns j.
-  for (int n = threadIdx.x; n < 768; n += NTHREADS) {
+  for (int n = threadIdx.x; n < 768; n += S::NT) {
     float b = 0.f;
     if constexpr (ROLE == ROLE_UP) {
       const int co = up_column<C, CP, PS>(n);
@@ -176,6 +205,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
       b = __ldg(p.bias + n);
     }
     bias_sm[n] = b;
+  }
+  if (S::FF) {   // the ring rows' zero columns (x = -1 and x = 128), never overwritten
+    for (int i = threadIdx.x; i < FF_NPR * (CP / 8) * 2; i += S::NT) {
+      const int row = i / ((CP / 8) * 2), r2 = i - row * (CP / 8) * 2, pl = r2 >> 1, side = r2 & 1;
+      *reinterpret_cast<uint4*>(pring + row * PROW_BYTES + (uint32_t)(pl * FF_W + side * (FF_W - 1)) * 16) =
+          make_uint4(0, 0, 0, 0);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -198,7 +234,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  long long pw0 = 0, pw1 = 0, pw3 = 0, pwS = 0;
+  long long pw0 = 0, pw1 = 0, pw2 = 0, pw3 = 0, pwS = 0, pwR = 0;   // pwR: ROLE_FOLDF ring waits
   const long long pstart = clock64();
 
   if (warp == 0) {
@@ -215,7 +251,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
         mbar_arrive(&unit_full[us & 3]);
         if (u < 0) break;
         const int v = u / p.nchunk, chunk = u - v * p.nchunk;
-        const int bin = v / p.nbands, y0 = (v - bin * p.nbands) * BR;
+        const int bin = v / p.nbands, y0 = (v - bin * p.nbands) * S::BSTR + S::ROFF;
         if (p.nchunk > 1 || bload == 0) {
           const uint32_t bs = bload & 1;
           mbar_wait(&b_empty[bs], ((bload >> 1) & 1) ^ 1);
@@ -223,7 +259,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
           bulk_g2s(bimg + bs * p.b_bytes, p.wimg + (size_t)chunk * p.b_bytes, p.b_bytes, &b_full[bs]);
           ++bload;
         }
-        const int y1 = min(p.Hr, y0 + BR);
+        const int y1 = min(p.Hr, y0 + S::BRS);
         const int rlo = max(y0 - 1, 0), rhi = min(y1, p.Hr - 1);   // input rows this unit reads
         for (int k = 0; k < S::NG_IN; ++k) {
           const uint32_t slot = ig & gsm;
@@ -261,14 +297,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
         mbar_arrive(&unit_empty[us & 3]);
         if (u < 0) break;
         const int v = u / p.nchunk, chunk = u - v * p.nchunk;
-        const int bin = v / p.nbands, y0 = (v - bin * p.nbands) * BR;
+        const int bin = v / p.nbands, y0 = (v - bin * p.nbands) * S::BSTR + S::ROFF;
         if (p.nchunk > 1 || bwait == 0) {
           bs = bwait & 1;
           mbar_wait(&b_full[bs], (bwait >> 1) & 1);
           ++bwait;
           b16 = (smem_u32(bimg) + bs * p.b_bytes) >> 4;
         }
-        const int rlo = max(y0 - 1, 0), rhi = min(min(y0 + BR, p.Hr), p.Hr - 1);
+        const int rlo = max(y0 - 1, 0), rhi = min(min(y0 + S::BRS, p.Hr), p.Hr - 1);
 #pragma unroll
         for (int k = 0; k < S::NG_IN; ++k) {
           const uint32_t slot = (ig + k) & gsm;
@@ -282,7 +318,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
             const uint32_t igk = ig + k;
             const long long t0 = clock64();
             mbar_wait(&in_full[slot], (igk >> gslog) & 1);
-            if (p.prof) pw1 += clock64() - t0;
+            if (p.prof) pw2 += clock64() - t0;
           }
           tc_fence_after();
           const uint32_t grp_a = ring16 + slot * grp16;
@@ -291,11 +327,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
             constexpr int dummy = 0;
             (void)dummy;
             const int i = G * k + ii;                 // band-local input row: r = y0 - 1 + i
-            if (i > BR + 1) continue;                  // compile-time
+            if (i > S::BRS + 1) continue;              // compile-time
             const int r = y0 - 1 + i;
             const uint32_t en = (r >= rlo && r <= rhi) ? 1u : 0u;
             // window: output rows j = i (group 0, dy=-1), i-1 (group 1), i-2 (group 2) inside [0, BR)
-            const int gA = i < BR ? 0 : (i - 1 < BR ? 1 : 2);
+            const int gA = i < S::BRS ? 0 : (i - 1 < S::BRS ? 1 : 2);
             const int gB = i >= 2 ? 3 : (i >= 1 ? 2 : 1);
             const int ng = gB - gA;
             const int s0 = S::slot(i - gA);          // slot of the first group's output row
@@ -330,7 +366,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
       }
     }
     __syncwarp();
-  } else {
+  } else if (warp < NTHREADS / 32) {
     // =============================== epilogue ===============================
     const int quad = (warp - 2) >> 2;        // alternate accumulator groups between the two quads
     const int q4 = warp & 3;                 // TMEM lane quarter of this warp
@@ -342,6 +378,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
     const size_t bin_px = (size_t)p.Hr * p.Wr;
     const size_t pstride = (size_t)p.Wr * 8;                 // elements between planes of one row
     uint32_t og = 0;
+    uint32_t pbase = 0;   // ROLE_FOLDF: sequence number of this unit's first partial-sum row
     for (uint32_t us = 0;; ++us) {
       mbar_wait(&unit_full[us & 3], (us >> 2) & 1);
       const int u = *(volatile int*)&unit_ring[us & 3];
@@ -349,8 +386,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
       if (lane == 0) mbar_arrive(&unit_empty[us & 3]);
       if (u < 0) break;
       const int v = u / p.nchunk, chunk = u - v * p.nchunk;
-      const int bin = v / p.nbands, y0 = (v - bin * p.nbands) * BR;
-      const int nrows = min(BR, p.Hr - y0);
+      const int bin = v / p.nbands, y0 = (v - bin * p.nbands) * S::BSTR + S::ROFF;
+      const int nrows = min(S::BRS, p.Hr - y0);
+      // ROLE_FOLDF: the occupancy words of all 66 rows for this warp's 32 pixels, fetched once per
+      // unit (3 per lane) and handed to each row by a shuffle: the epilogue is this kernel's critical
+      // path, so no per-row global-load latency may sit on it
+      uint32_t occ_pre[3] = {0u, 0u, 0u};
+      if constexpr (S::FF) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const int r = 32 * q + lane;
+          const int y = min(max(y0 + r, 0), p.Hr - 1);
+          if (r < S::BRS) occ_pre[q] = __ldg(p.mbits + ((size_t)bin * p.bin_h + y) * words + q4);
+        }
+      }
       for (int k = 0; k < S::NG_OUT; ++k) {
         const uint32_t og_k = og + k;
         if ((int)(og_k & 1) != quad) continue;
@@ -360,10 +409,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
         uint4 sk[G][SK];
 #pragma unroll
         for (int jj = 0; jj < G; ++jj) {
-          const int y = min(ybase + jj, p.Hr - 1);
+          const int y = min(max(ybase + jj, 0), p.Hr - 1);
           const uint32_t* mrow = p.mbits + ((size_t)bin * p.bin_h + y / p.res) * words;
+          if constexpr (S::FF) {
+            const int r = G * k + jj;   // band-local row; shuffle the prefetched word (warp-uniform r)
+            const uint32_t w01 = r < 32 ? occ_pre[0] : occ_pre[1];
+            occw[jj][0] = __shfl_sync(0xffffffffu, r < 64 ? w01 : occ_pre[2], r & 31);
+            (void)mrow;
+          } else {
 #pragma unroll
-          for (int t = 0; t < T; ++t) occw[jj][t] = __ldg(mrow + ((t * 128 + m) / p.res) / 32);
+            for (int t = 0; t < T; ++t) occw[jj][t] = __ldg(mrow + ((t * 128 + m) / p.res) / 32);
+          }
           if (HAS_SKIP) {
             const size_t act_row = (size_t)bin * bin_px * p.out_c8 * 8 + (size_t)y * p.out_c8 * pstride;
 #pragma unroll
@@ -381,7 +437,46 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
         for (int jj = 0; jj < G; ++jj) {
           const int j = G * k + jj;
           const int y = y0 + j;
-          if (j < nrows) {
+          if constexpr (S::FF) {
+            // partial-sum row j -> SMEM ring (bf16, masked: exactly the values ROLE_FOLD writes to
+            // HBM); rows outside the bin are zero rows (the combine's zero padding)
+            const uint32_t q = pbase + (uint32_t)j;
+            const uint32_t sl = q % FF_NPR;
+            {
+              const long long t0 = clock64();
+              mbar_wait(&prow_empty[sl], ((q / FF_NPR) & 1) ^ 1);
+              if (p.prof) pwR += clock64() - t0;
+            }
+            uint8_t* rowp = pring + sl * PROW_BYTES + (uint32_t)(m + 1) * 16;
+            if (y >= 0 && y < p.Hr) {
+              const bool occ = (occw[jj][0] >> (m & 31)) & 1u;
+              const uint32_t taddr = tmem + lane_off + (uint32_t)(S::slot(j) * CP);
+              // two batches of TMEM columns (<= 48 live registers: no spills beside the r[] of 80)
+              constexpr int H1 = CP / 16 / 2 * 16 + (CP / 16 % 2) * 16;   // 48 of 80, 32 of 48
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int c0 = h ? H1 : 0, c1 = h ? CP : H1;
+                uint32_t r[H1];
+#pragma unroll
+                for (int c = 0; c < H1; c += 16)
+                  if (c0 + c < c1) tmem_ld16(taddr + (uint32_t)(c0 + c), r + c);
+                tmem_ld_wait();
+#pragma unroll
+                for (int g = 0; g < H1 / 8; ++g) {
+                  if (c0 + 8 * g >= c1) break;
+                  float vv[8];
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) vv[e] = __uint_as_float(r[8 * g + e]);
+                  *reinterpret_cast<uint4*>(rowp + (c0 / 8 + g) * FF_W * 16) = pack8(vv, occ);
+                }
+              }
+            } else {
+#pragma unroll
+              for (int g = 0; g < CP / 8; ++g) *reinterpret_cast<uint4*>(rowp + g * FF_W * 16) = make_uint4(0, 0, 0, 0);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&prow_full[sl]);
+          } else if (j < nrows) {
 #pragma unroll
             for (int t = 0; t < T; ++t) {
               const int x = t * 128 + m;
@@ -454,14 +549,86 @@ __global__ void __launch_bounds__(NTHREADS, 1) conv_tc_kernel(const __grid_const
         if (lane == 0) mbar_arrive(&acc_empty[og_k % S::OGR]);
       }
       og += S::NG_OUT;
+      pbase += S::BRS;
+    }
+  } else {
+    // =============================== fused combine (ROLE_FOLDF) ===============================
+    // Two groups of 4 warps take alternate band rows c (group 0 odd, group 1 even); a thread per bin
+    // pixel column x of the (single) tile. For band row c (bin row yb + c - 1) a group waits for the
+    // partial-sum rows c-1, c, c+1, sums the <= 4 partials of each HR sub-pixel exactly as the
+    // standalone combine does (fold_common.cuh), writes the owned pixel's HR block into the frame and
+    // then signals that it has read the three rows (a row's slot is free after all three readers).
+    if constexpr (S::FF) {
+      const int cw = warp - NTHREADS / 32;          // 0..7
+      const int grp = cw >> 2;
+      const int x = (cw & 3) * 32 + lane;
+      const float b0 = __ldg(p.tbias), b1 = __ldg(p.tbias + 1), b2 = __ldg(p.tbias + 2);
+      uint32_t pbase = 0;
+      for (uint32_t us = 0;; ++us) {
+        mbar_wait(&unit_full[us & 3], (us >> 2) & 1);
+        const int u = *(volatile int*)&unit_ring[us & 3];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&unit_empty[us & 3]);
+        if (u < 0) break;
+        const int bin = u / p.nbands, yb = (u - bin * p.nbands) * S::BSTR;   // nchunk == 1
+        const int64_t* drow = p.fdst + (size_t)bin * p.bin_h * p.bin_w + x;
+        // first row of this group: c0 = 1 (group 0) or 2 (group 1); the frame destination of the next
+        // row is loaded one row ahead (L2 latency off the chain)
+        const int c0 = grp ? 2 : 1;
+        int64_t dnext = yb + c0 - 1 < p.Hr ? __ldg(drow + (size_t)(yb + c0 - 1) * p.bin_w) : -1;
+#pragma unroll 1
+        for (int c = c0; c <= S::BSTR; c += 2) {
+          const int y = yb + c - 1;
+          const int64_t dst = dnext;
+          dnext = (c + 2 <= S::BSTR && y + 2 < p.Hr) ? __ldg(drow + (size_t)(y + 2) * p.bin_w) : -1;
+          const uint8_t* rb[3];
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            const uint32_t q = pbase + (uint32_t)(c - 1 + d);
+            const long long t0 = clock64();
+            mbar_wait(&prow_full[q % FF_NPR], (q / FF_NPR) & 1);
+            if (p.prof) pwR += clock64() - t0;
+            rb[d] = pring + (q % FF_NPR) * PROW_BYTES + (uint32_t)(x + 1) * 16;
+          }
+          if (y < p.Hr && dst >= 0 && p.ff_debug != 1) {
+            float acc[PS][PS][3];
+            fold::accumulate_batched<PS, 6>(
+                [&](int l) {
+                  const int ny = fold::load_ny(PS, l), nx = fold::load_nx(PS, l), pl = fold::load_pl(PS, l);
+                  return *reinterpret_cast<const uint4*>(rb[ny + 1] + (pl * FF_W + nx) * 16);
+                },
+                acc);
+            fold::store_frame<PS>(acc, b0, b1, b2, dst, 1, x, y, p.fOW, p.fout, p.fout_fp32);
+          }
+          __syncwarp();
+          if (lane == 0) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              // row c-1+d read once by this combine; the band-edge rows 0, 1, 64, 65 also take the
+              // arrivals of the combines that do not exist (c = 0, c = 65)
+              uint32_t n = 1;
+              if (c == 1 && d == 0) n = 3;
+              if (c == 1 && d == 1) n = 2;
+              if (c == S::BSTR && d == 1) n = 2;
+              if (c == S::BSTR && d == 2) n = 3;
+              mbar_arrive_cnt(&prow_empty[(pbase + (uint32_t)(c - 1 + d)) % FF_NPR], n);
+            }
+          }
+        }
+        pbase += S::BRS;
+      }
     }
   }
   if (p.prof && lane == 0) {
     const long long tot = clock64() - pstart;
     if (warp == 0) { atomicAdd(p.prof + 0, (unsigned long long)pw0); atomicAdd(p.prof + 4, (unsigned long long)tot); }
-    if (warp == 1) { atomicAdd(p.prof + 1, (unsigned long long)pw1); atomicAdd(p.prof + 5, (unsigned long long)tot); }
-    if (warp >= 2) { atomicAdd(p.prof + 3, (unsigned long long)pw3); atomicAdd(p.prof + 6, (unsigned long long)tot);
-                     atomicAdd(p.prof + 7, (unsigned long long)pwS); }
+    if (warp == 1) { atomicAdd(p.prof + 1, (unsigned long long)pw1); atomicAdd(p.prof + 2, (unsigned long long)pw2);
+                     atomicAdd(p.prof + 5, (unsigned long long)tot); }
+    if (warp >= 2 && warp < NTHREADS / 32) {
+      atomicAdd(p.prof + 3, (unsigned long long)pw3); atomicAdd(p.prof + 6, (unsigned long long)tot);
+      atomicAdd(p.prof + 7, (unsigned long long)pwS); atomicAdd(p.prof + 8, (unsigned long long)pwR);
+    }
+    if (warp >= NTHREADS / 32) { atomicAdd(p.prof + 9, (unsigned long long)pwR); atomicAdd(p.prof + 10, (unsigned long long)tot); }
   }
   tc_fence_before();
   __syncthreads();
@@ -648,6 +815,14 @@ static KernFn lookup(int role, int C, int CP, int R, int G, int T, int PS) {
   K(ROLE_FOLD, 64, 80, 4, 1, 1, 1)
   K(ROLE_FOLD, 64, 48, 8, 2, 1, 1)
   K(ROLE_FOLD, 64, 48, 4, 1, 2, 1)
+  K(ROLE_FOLDF, 16, 80, 6, 1, 1, 3)
+  K(ROLE_FOLDF, 16, 48, 6, 1, 1, 2)
+  K(ROLE_FOLDF, 32, 80, 6, 1, 1, 3)
+  K(ROLE_FOLDF, 32, 48, 6, 1, 1, 2)
+  K(ROLE_FOLDF, 48, 80, 6, 1, 1, 3)
+  K(ROLE_FOLDF, 48, 48, 6, 1, 1, 2)
+  K(ROLE_FOLDF, 64, 80, 6, 1, 1, 3)
+  K(ROLE_FOLDF, 64, 48, 6, 1, 1, 2)
 #undef K
   return nullptr;
 }
@@ -728,6 +903,8 @@ static tc::Plan* get_plan(SRNet* net, const ConvDesc& cv, int bin_w) {
   return q.ok ? &q : nullptr;
 }
 
+static const tc::Plan* tc_plan_of(SRNet* net, const ConvDesc& cv, int bin_w) { return get_plan(net, cv, bin_w); }
+
 bool conv_tc_supported(const SRNet* net, const ConvDesc& cv, int bin_w) {
   if (!net->use_tc) return false;
   return get_plan(const_cast<SRNet*>(net), cv, bin_w) != nullptr;
@@ -788,10 +965,10 @@ regen_status conv_tc_launch(const SRNet* net, const ConvDesc& cv, const void* in
   if (prof_on < 0) {
     const char* e = getenv("REGEN_TC_PROF");
     prof_on = (e && e[0] == '1') ? 1 : 0;
-    if (prof_on) cudaMalloc(&d_prof, 8 * sizeof(unsigned long long));
+    if (prof_on) cudaMalloc(&d_prof, 16 * sizeof(unsigned long long));
   }
   if (prof_on) {
-    cudaMemsetAsync(d_prof, 0, 8 * sizeof(unsigned long long), s);
+    cudaMemsetAsync(d_prof, 0, 16 * sizeof(unsigned long long), s);
     p.prof = d_prof;
   }
   static const char* kRoleName[] = {"conv_head", "conv_res_a", "conv_res_b", "conv_body", "conv_up", "conv_tail",
@@ -809,6 +986,117 @@ regen_status conv_tc_launch(const SRNet* net, const ConvDesc& cv, const void* in
             "mma total %.0f waits %.0f | epi total %.0f wait_accfull %.0f rearm %.0f (cycles/CTA)\n",
             cv.role, pl->cp, pl->R, pl->G, pl->T, pl->nchunk, p.ngs, h[4] / g, h[0] / g, h[5] / g, h[1] / g,
             h[6] / (8 * g), h[3] / (8 * g), h[7] / (8 * g));
+  }
+  return REGEN_OK;
+}
+
+}  // namespace regen
+
+// ---------------------------------------------------------------------------------- fused fold
+// The fold conv (ROLE_FOLD's B image and bias) run as ROLE_FOLDF: bands of 64 rows (66 computed),
+// a 6-slot TMEM ring, and 4 combiner warps that turn the partial sums into the owned MBs' HR pixels.
+namespace regen {
+
+static const tc::Plan* foldf_plan(const SRNet* net, int bin_w, int& ps) {
+  if (!net->use_tc || net->fold_conv < 0) return nullptr;
+  const ConvDesc& cv = net->convs[net->fold_conv];
+  const tc::Plan* pl = tc_plan_of(const_cast<SRNet*>(net), cv, bin_w);
+  if (pl == nullptr || pl->T != 1 || cv.res != 1 || pl->nchunk != 1) return nullptr;
+  ps = net->convs[net->fold_conv - 2].ps;
+  if (tc::lookup(ROLE_FOLDF, net->cfg.channels, pl->cp, 6, 1, 1, ps) == nullptr) return nullptr;
+  // SMEM with the shallowest input ring (2 rows): guard + rows + B image + partial-sum rows
+  const size_t need = 1024 + 2ull * (cv.cin / 8) * bin_w * 16 + pl->b_bytes + (size_t)tc::FF_NPR * (pl->cp / 8) * tc::FF_W * 16;
+  if (need > 224 * 1024) return nullptr;
+  return pl;
+}
+
+bool fold_fused_supported(const SRNet* net, int bin_w) {
+  int ps = 0;
+  const char* off = getenv("REGEN_NO_FOLDF");   // A/B aid: the fold conv + standalone combine
+  if (off && off[0] == '1') return false;
+  return foldf_plan(net, bin_w, ps) != nullptr;
+}
+
+regen_status fold_fused_launch(const SRNet* net, const void* in, const uint32_t* mbits, int max_bins,
+                               const int32_t* d_num_bins, int bin_w, int bin_h, int* counter, cudaStream_t s,
+                               int reverse, const FoldFrameArgs& fa) {
+  using namespace tc;
+  int ps = 0;
+  const Plan* pl = foldf_plan(net, bin_w, ps);
+  REGEN_REQUIRE(pl != nullptr, "no fused fold plan");
+  const ConvDesc& cv = net->convs[net->fold_conv];
+  const ConvDesc& tail = net->convs[net->fold_conv - 1];
+  Params p;
+  memset(&p, 0, sizeof(p));
+  p.in = (const __nv_bfloat16*)in;
+  p.bias = net->d_w32 + cv.b_off;
+  p.mbits = mbits;
+  p.num_bins = d_num_bins;
+  p.wimg = net->d_wtc + cv.tc_off;
+  p.b_bytes = pl->b_bytes;
+  p.Wr = bin_w;
+  p.Hr = bin_h;
+  p.res = 1;
+  p.bin_w = bin_w;
+  p.bin_h = bin_h;
+  p.cout = cv.cout;
+  p.nchunk = 1;
+  p.nbands = (bin_h + 63) / 64;
+  p.max_bins = max_bins;
+  p.out_c8 = (cv.cout + 7) / 8;
+  p.res_scale = 1.0f;
+  p.counter = counter;
+  p.reverse = reverse;
+  p.fdst = fa.dst;
+  p.fout = fa.out;
+  p.tbias = net->d_w32 + tail.b_off;
+  p.fout_fp32 = fa.out_dtype == REGEN_DTYPE_FP32 ? 1 : 0;
+  p.fOW = fa.geom.frame_w * net->cfg.scale;
+  {
+    const char* e = getenv("REGEN_FF_DEBUG");
+    p.ff_debug = e ? atoi(e) : 0;
+  }
+  const uint32_t grp_bytes = (uint32_t)(cv.cin / 8) * p.Wr * 16;   // G = 1
+  const size_t pring = (size_t)FF_NPR * (pl->cp / 8) * FF_W * 16;
+  int gslog = 3;
+  while (gslog > 1 && 1024 + ((size_t)1 << gslog) * grp_bytes + pl->b_bytes + pring > 224 * 1024) --gslog;
+  p.ngs = 1 << gslog;
+  p.gslog = gslog;
+  const size_t smem = 1024 + (size_t)p.ngs * grp_bytes + pl->b_bytes + pring;
+  REGEN_REQUIRE(smem <= 227 * 1024, "fused fold SMEM %zu too large", smem);
+  KernFn kern = lookup(ROLE_FOLDF, net->cfg.channels, pl->cp, 6, 1, 1, ps);
+  REGEN_REQUIRE(kern != nullptr, "no fused fold kernel instance");
+  REGEN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = std::min(max_bins * p.nbands, nsm);
+  static unsigned long long* d_prof = nullptr;
+  static int prof_on = -1;
+  if (prof_on < 0) {
+    const char* e = getenv("REGEN_TC_PROF");
+    prof_on = (e && e[0] == '1') ? 1 : 0;
+    if (prof_on) cudaMalloc(&d_prof, 16 * sizeof(unsigned long long));
+  }
+  if (prof_on) {
+    cudaMemsetAsync(d_prof, 0, 16 * sizeof(unsigned long long), s);
+    p.prof = d_prof;
+  }
+  REGEN_TRACE("conv_fold_frames", s);
+  kern<<<grid, NTHREADS + 256, smem, s>>>(p);
+  REGEN_LAUNCH_CHECK();
+  if (prof_on) {
+    unsigned long long h[16];
+    cudaMemcpyAsync(h, d_prof, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    const double g = (double)grid;
+    fprintf(stderr,
+            "[tc-prof] fused fold CP=%d gslots=%d | producer total %.0f wait_empty %.0f | mma total %.0f wait_accempty %.0f "
+            "wait_infull %.0f | "
+            "epi total %.0f wait_accfull %.0f rearm %.0f wait_ring %.0f | combine total %.0f wait_rows %.0f "
+            "(cycles/CTA, per warp)\n",
+            pl->cp, p.ngs, h[4] / g, h[0] / g, h[5] / g, h[1] / g, h[2] / g, h[6] / (8 * g), h[3] / (8 * g), h[7] / (8 * g),
+            h[8] / (8 * g), h[10] / (8 * g), h[9] / (8 * g));
   }
   return REGEN_OK;
 }

@@ -570,12 +570,15 @@ static regen_status enhance_run(const SRNet* net, const regen_geom* geom, const 
   }
   if (st != REGEN_OK) return st;
   if (fold_enabled(net, p->bin_w)) {
-    // last upsampler + tail as the folded conv (partials in e.u) and the partial-sum combine
-    st = run_conv(net, cv[net->fold_conv], up_in, e.u, nullptr, e, *p, d_num_bins, s, ord++);
     if (fa) {
       fa->map = e.map;
       fa->dst = e.dst;
+      if (fold_fused_supported(net, p->bin_w))   // combine fused into the fold conv: no partials in HBM
+        return fold_fused_launch(net, up_in, e.mbits, p->max_bins, d_num_bins, p->bin_w, p->bin_h,
+                                 e.counters + net->fold_conv, s, (ord++) & 1, *fa);
     }
+    // last upsampler + tail as the folded conv (partials in e.u) and the partial-sum combine
+    st = run_conv(net, cv[net->fold_conv], up_in, e.u, nullptr, e, *p, d_num_bins, s, ord++);
     if (st == REGEN_OK)
       st = fold_combine_launch(net, e.u, d_hr_bins, e.mbits, p->max_bins, d_num_bins, p->bin_w, p->bin_h, s, fa);
     return st;

@@ -20,7 +20,9 @@ enum ConvRole : int {
   ROLE_TAIL = 5,     // -> HR output [bin][y][x][4]
   ROLE_TINY0 = 6,    // x0 -> relu(conv)
   ROLE_TINY1 = 7,    // -> conv, PixelShuffle(scale) into the HR output
-  ROLE_FOLD = 8      // UP∘TAIL fold: conv C -> 3(p+2)^2 partial sums (upfold.cu)
+  ROLE_FOLD = 8,     // UP∘TAIL fold: conv C -> 3(p+2)^2 partial sums (upfold.cu)
+  ROLE_FOLDF = 9     // launch variant of ROLE_FOLD with the partial-sum combine fused into the epilogue:
+                     // writes the owned MBs' HR pixels straight into the frames (conv_tc.cu)
 };
 
 struct ConvDesc {
@@ -103,5 +105,10 @@ regen_status resblock_tc_launch(const SRNet* net, int block, const void* in, voi
 regen_status conv_tc_launch(const SRNet* net, const ConvDesc& cv, const void* in, void* out, const void* skip,
                             const uint32_t* mbits, int max_bins, const int32_t* d_num_bins, int bin_w, int bin_h,
                             int* counter, cudaStream_t s, int reverse = 0);
+// the fold conv with the combine fused (ROLE_FOLDF): true if this net/bin width has an instance
+bool fold_fused_supported(const SRNet* net, int bin_w);
+regen_status fold_fused_launch(const SRNet* net, const void* in, const uint32_t* mbits, int max_bins,
+                               const int32_t* d_num_bins, int bin_w, int bin_h, int* counter, cudaStream_t s,
+                               int reverse, const FoldFrameArgs& fa);
 
 }  // namespace regen

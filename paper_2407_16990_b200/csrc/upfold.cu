@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <vector>
 
+#include "fold_common.cuh"
 #include "net.cuh"
 #include "tc_common.cuh"
 
@@ -28,46 +29,6 @@ namespace regen {
 using tc::pack_bf16x2;
 
 namespace fold {
-
-// sub-pixels i of a target whose window reaches neighbour row ny, and their count
-__host__ __device__ constexpr int cnt(int ny, int p) { return ny == 0 ? p : 1; }
-__host__ __device__ constexpr int first(int ny, int p) { return ny == 1 ? p - 1 : 0; }
-// channel offset of neighbour block n = (ny, nx) (raster order over {-1,0,1}^2)
-__host__ __device__ constexpr int block_off(int ny, int nx, int p) {
-  int off = 0;
-  for (int a = -1; a <= 1; ++a)
-    for (int b = -1; b <= 1; ++b) {
-      if (a == ny && b == nx) return off;
-      off += cnt(a, p) * cnt(b, p) * 3;
-    }
-  return off;
-}
-__host__ __device__ constexpr int n_channels(int p) { return 3 * (p + 2) * (p + 2); }
-
-// the 16-B plane loads of one pixel's combine, in (neighbour, plane) order: l-th load
-__host__ __device__ constexpr int plane_lo(int ny, int nx, int p) { return block_off(ny, nx, p) / 8; }
-__host__ __device__ constexpr int plane_hi(int ny, int nx, int p) {
-  return (block_off(ny, nx, p) + cnt(ny, p) * cnt(nx, p) * 3 - 1) / 8;
-}
-__host__ __device__ constexpr int n_loads(int p) {
-  int n = 0;
-  for (int a = -1; a <= 1; ++a)
-    for (int b = -1; b <= 1; ++b) n += plane_hi(a, b, p) - plane_lo(a, b, p) + 1;
-  return n;
-}
-// (ny, nx, plane) of load l, packed as (ny+1)*3 + (nx+1) in the high bits
-__host__ __device__ constexpr int load_code(int p, int l) {
-  for (int a = -1; a <= 1; ++a)
-    for (int b = -1; b <= 1; ++b) {
-      const int n = plane_hi(a, b, p) - plane_lo(a, b, p) + 1;
-      if (l < n) return ((a + 1) * 3 + (b + 1)) * 64 + plane_lo(a, b, p) + l;
-      l -= n;
-    }
-  return 0;
-}
-__host__ __device__ constexpr int load_ny(int p, int l) { return load_code(p, l) / 64 / 3 - 1; }
-__host__ __device__ constexpr int load_nx(int p, int l) { return load_code(p, l) / 64 % 3 - 1; }
-__host__ __device__ constexpr int load_pl(int p, int l) { return load_code(p, l) % 64; }
 
 // Where the combined HR pixels go. BINS: the HR bin layout [bin][PS*Hr][PS*Wr][4] of
 // regen_enhance_packed. FRAME (regen_enhance_scatter): straight into the HR frames
@@ -106,13 +67,7 @@ __global__ void __launch_bounds__(128, 8) combine_kernel(const __nv_bfloat16* P,
     occ = (__ldg(mbits + ((size_t)bin * bin_h + yl) * words + xl / 32) >> (xl & 31)) & 1u;
   }
   float acc[PS][PS][3];
-#pragma unroll
-  for (int i = 0; i < PS; ++i)
-#pragma unroll
-    for (int j = 0; j < PS; ++j)
-#pragma unroll
-      for (int o = 0; o < 3; ++o) acc[i][j][o] = 0.f;
-  if (occ) {
+  {
     // all partial-sum planes this pixel needs (<= 16 16-B loads over its 3x3 neighbourhood) are
     // issued before any is used, so their latencies overlap
     const size_t pstride = (size_t)Wr * 8;
@@ -122,25 +77,12 @@ __global__ void __launch_bounds__(128, 8) combine_kernel(const __nv_bfloat16* P,
     for (int l = 0; l < NL; ++l) {
       const int ny = load_ny(PS, l), nx = load_nx(PS, l), pl = load_pl(PS, l);
       const int yy = y + ny, xx = x + nx;
-      q[l] = (yy < 0 || yy >= Hr || xx < 0 || xx >= Wr)   // zero padding at the bin edge
+      q[l] = (!occ || yy < 0 || yy >= Hr || xx < 0 || xx >= Wr)   // zero padding at the bin edge
                  ? make_uint4(0, 0, 0, 0)
                  : __ldg(reinterpret_cast<const uint4*>(P + ((size_t)bin * Hr + yy) * c8 * pstride +
                                                         (size_t)pl * pstride + (size_t)xx * 8));
     }
-#pragma unroll
-    for (int l = 0; l < NL; ++l) {
-      const int ny = load_ny(PS, l), nx = load_nx(PS, l), pl = load_pl(PS, l);
-      const int off = block_off(ny, nx, PS), ci = cnt(ny, PS), cj = cnt(nx, PS);
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q[l]);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int ch = pl * 8 + e - off;   // index within the neighbour's block
-        if (ch < 0 || ch >= ci * cj * 3) continue;
-        const float v = (e & 1) ? __high2float(h[e / 2]) : __low2float(h[e / 2]);
-        const int o = ch % 3, t = ch / 3, jj = t % cj, ii = t / cj;
-        acc[first(ny, PS) + ii][first(nx, PS) + jj][o] += v;
-      }
-    }
+    accumulate<PS>(q, acc);
   }
   const float b0 = __ldg(bt), b1 = __ldg(bt + 1), b2 = __ldg(bt + 2);
   if (!FRAME) {
@@ -157,48 +99,7 @@ __global__ void __launch_bounds__(128, 8) combine_kernel(const __nv_bfloat16* P,
       }
     }
   } else {
-    // the PS x PS HR block of this pixel inside the HR frame (D7 un-rotation: bin-HR sub-pixel (i, j)
-    // -> frame (j, i) unrotated, (i, PS-1-j) rotated; for res 2 (x4) the block is offset inside the
-    // LR pixel's 4x4 square by the res-2 sub-position). Values rounded to bf16 first (bit-identical
-    // to the HR-bin round trip of the separate calls). Each frame row of the block gets 3*PS
-    // contiguous elements, stored as 32-bit words after a leading 16-bit one when misaligned.
-    const bool rot = (dst >> 62) & 1;
-    const int OW = fo.W * fo.s;
-    int64_t base = dst & ((1ll << 62) - 1);
-    if (res > 1) {   // x4: this res-2 pixel's 2x2 HR block inside the LR pixel's 4x4 square
-      const int sx2 = x % res, sy2 = y % res;
-      base += rot ? (int64_t)(PS * (res - 1 - sx2)) * OW + PS * sy2 : (int64_t)(PS * sy2) * OW + PS * sx2;
-    }
-#pragma unroll
-    for (int r = 0; r < PS; ++r) {   // frame row r of the block
-      float v[3 * PS];
-#pragma unroll
-      for (int c = 0; c < PS; ++c) {   // frame column c
-        // bin-HR sub-pixel (c, PS-1-r) when rotated, (r, c) otherwise (compile-time indices)
-        v[3 * c] = (rot ? acc[c][PS - 1 - r][0] : acc[r][c][0]) + b0;
-        v[3 * c + 1] = (rot ? acc[c][PS - 1 - r][1] : acc[r][c][1]) + b1;
-        v[3 * c + 2] = (rot ? acc[c][PS - 1 - r][2] : acc[r][c][2]) + b2;
-      }
-      const size_t e0 = (size_t)(base + (int64_t)r * OW) * 3;   // element index of the run
-      if (fo.out_fp32) {
-        float* o = (float*)fo.out + e0;
-#pragma unroll
-        for (int e = 0; e < 3 * PS; ++e) o[e] = __bfloat162float(__float2bfloat16_rn(v[e]));
-      } else {
-        __nv_bfloat16* o = (__nv_bfloat16*)fo.out + e0;
-        constexpr int NE = 3 * PS;
-        if (e0 & 1) {   // odd start: one 16-bit store, then 32-bit pairs
-          o[0] = __float2bfloat16_rn(v[0]);
-#pragma unroll
-          for (int e = 1; e + 1 < NE; e += 2) *reinterpret_cast<uint32_t*>(o + e) = pack_bf16x2(v[e], v[e + 1]);
-          if ((NE - 1) % 2 == 1) o[NE - 1] = __float2bfloat16_rn(v[NE - 1]);
-        } else {
-#pragma unroll
-          for (int e = 0; e + 1 < NE; e += 2) *reinterpret_cast<uint32_t*>(o + e) = pack_bf16x2(v[e], v[e + 1]);
-          if (NE % 2 == 1) o[NE - 1] = __float2bfloat16_rn(v[NE - 1]);
-        }
-      }
-    }
+    store_frame<PS>(acc, b0, b1, b2, dst, res, x, y, fo.W * fo.s, fo.out, fo.out_fp32);
   }
   }
 }
