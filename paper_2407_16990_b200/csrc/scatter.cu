@@ -2,6 +2,8 @@
 // back to bi-linear-interpolated non-regions". Every HR pixel is written exactly once: the bilinear
 // value (D10: half-pixel centres, edge clamp, fp32) or, inside the HR square of an owned selected MB,
 // the box's HR bin pixel (un-rotated, D7). Stores are 16-B vectors (bf16) / 32-B (fp32).
+#include <algorithm>
+#include <stdlib.h>
 #include <string.h>
 
 #include "net.cuh"
@@ -31,6 +33,7 @@ struct ScatterArgs {
   int W, H, OW, OH, GW, GH, mb, s, bin_w, bin_h;
   float inv_s;
   int mode;         // SC_ALL, SC_BILINEAR (owned MBs written elsewhere: the fold combine), SC_OWNED
+  int64_t n_frames;
 };
 
 // One CTA per (frame, LR row y) writes the S HR rows S*y .. S*y+S-1. The (at most three) LR rows
@@ -218,6 +221,133 @@ __global__ void __launch_bounds__(SC_THREADS, 8) scatter_rows_kernel(ScatterArgs
   }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Bilinear-only pass (SC_BILINEAR; frame width a multiple of 8): a warp per (frame, HR row, 32 groups
+// of 8 LR columns); a lane computes the 8*S HR pixels of its group in registers — LR bytes read as
+// aligned 32-bit words (the group's 10 columns x 3 channels sit at a fixed byte offset 1 inside 9
+// words: 3*x0 - 4 is word aligned because x0 is a multiple of 8), vertical then horizontal D10 lerp
+// at compile-time phases — and stages them in SMEM; the warp then writes its contiguous run of the HR
+// row with coalesced 16-B stores (lane k -> chunk k), skipping groups in owned MBs (an MB is 16 LR
+// columns: a group never straddles one). The first and last group of a row take a clamped path.
+constexpr int BL_WARPS = 4;
+
+template <int S, typename TO>
+struct BL {
+  static constexpr int VALS = 8 * S * 3;                        // values per group
+  static constexpr int BYTES = VALS * (int)sizeof(TO);          // 144 B at S = 3, bf16
+  static constexpr int CHUNKS = BYTES / 16;
+  static_assert(BYTES % 16 == 0, "group bytes");
+};
+
+template <int S, typename TO>
+__global__ void __launch_bounds__(32 * BL_WARPS) bilinear_kernel(ScatterArgs a, int nwc) {
+  extern __shared__ __align__(16) uint8_t bsm[];
+  using G = BL<S, TO>;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* stage = bsm + warp * 32 * G::BYTES;
+  const int W = a.W, W3 = 3 * W, GW = a.GW;
+  const int ngroups = W / 8;
+  const int64_t n_items = (int64_t)a.n_frames * a.OH * nwc;
+  for (int64_t it = (int64_t)blockIdx.x * BL_WARPS + warp; it < n_items; it += (int64_t)gridDim.x * BL_WARPS) {
+    const int wc = (int)(it % nwc);
+    const int64_t rowi = it / nwc;             // frame * OH + Y
+    const int Y = (int)(rowi % a.OH);
+    const int64_t f = rowi / a.OH;
+    const int g = wc * 32 + lane;
+    const int x0 = 8 * g;
+    const int my = (Y / S) / 16;
+    bool act = g < ngroups;
+    if (act) act = __ldg(a.owner + (f * a.GH + my) * GW + x0 / 16) < 0;
+    const uint32_t amask = __ballot_sync(0xffffffffu, act);
+    if (amask == 0u) continue;
+    if (act) {
+      // vertical pass: HR row Y = S*y + i samples LR rows (yl0, yl1) at fraction ly (D10)
+      const int y = Y / S, i = Y - y * S;
+      int yl0 = y + (2 * i + 1 < S ? -1 : 0);
+      float ly = 0.f;
+#pragma unroll
+      for (int q = 0; q < S; ++q)
+        if (q == i) ly = Phase<S>::f(q);
+      if (yl0 < 0) { yl0 = 0; ly = 0.f; }
+      const int yl1 = min(yl0 + 1, a.H - 1);
+      if (yl1 == yl0) ly = 0.f;
+      const uint8_t* r0 = a.frames + (f * a.H + yl0) * (int64_t)W3;
+      const uint8_t* r1 = a.frames + (f * a.H + yl1) * (int64_t)W3;
+      // LR columns x0-1 .. x0+8 after the vertical lerp, pre-scaled by 1/255, and the differences
+      // of neighbouring columns: each HR value is then one FMA (or a copy at fraction 0)
+      float vr[10][3];
+      if (x0 >= 8 && x0 + 9 <= W && ((((uintptr_t)r0) | ((uintptr_t)r1)) & 3) == 0) {
+        const uint32_t* w0 = reinterpret_cast<const uint32_t*>(r0 + 3 * x0 - 4);
+        const uint32_t* w1 = reinterpret_cast<const uint32_t*>(r1 + 3 * x0 - 4);
+        uint32_t u0[8], u1[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) { u0[k] = __ldg(w0 + k); u1[k] = __ldg(w1 + k); }
+#pragma unroll
+        for (int c = 0; c < 10; ++c)
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            const int b = 1 + 3 * c + ch;   // byte within the words (compile-time)
+            // u8 -> fp32 exactly: the byte placed under the exponent of 2^23, minus 2^23
+            const float p0 = __uint_as_float(__byte_perm(u0[b >> 2], 0x4B000000u, 0x7650u | (b & 3))) - 8388608.0f;
+            const float p1 = __uint_as_float(__byte_perm(u1[b >> 2], 0x4B000000u, 0x7650u | (b & 3))) - 8388608.0f;
+            vr[c][ch] = fmaf(ly, p1 - p0, p0) * (1.0f / 255.0f);
+          }
+      } else {   // first / last group of the row: clamped byte loads
+#pragma unroll
+        for (int c = 0; c < 10; ++c) {
+          const int cx = min(max(x0 - 1 + c, 0), W - 1);
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            const float p0 = (float)__ldg(r0 + 3 * cx + ch), p1 = (float)__ldg(r1 + 3 * cx + ch);
+            vr[c][ch] = fmaf(ly, p1 - p0, p0) * (1.0f / 255.0f);
+          }
+        }
+      }
+      float dv[9][3];
+#pragma unroll
+      for (int c = 0; c < 9; ++c)
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) dv[c][ch] = vr[c + 1][ch] - vr[c][ch];
+      // horizontal pass at compile-time phases; edge clamps (x == 0 with d = -1, x == W-1 with d = 0)
+      // come out of the clamped column loads (A == B: the lerp returns A exactly)
+      float o[G::VALS];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+          const int ca = q + 1 + Phase<S>::d(j);
+          const float lx = Phase<S>::f(j);
+          const int e = 3 * (q * S + j);
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) o[e + ch] = lx == 0.f ? vr[ca][ch] : fmaf(lx, dv[ca][ch], vr[ca][ch]);
+        }
+      uint4* st = reinterpret_cast<uint4*>(stage + lane * G::BYTES);
+      if (sizeof(TO) == 2) {
+#pragma unroll
+        for (int k = 0; k < G::CHUNKS; ++k)
+          st[k] = make_uint4(pack_bf16(o[8 * k], o[8 * k + 1]), pack_bf16(o[8 * k + 2], o[8 * k + 3]),
+                             pack_bf16(o[8 * k + 4], o[8 * k + 5]), pack_bf16(o[8 * k + 6], o[8 * k + 7]));
+      } else {
+#pragma unroll
+        for (int k = 0; k < G::CHUNKS; ++k)
+          st[k] = make_uint4(__float_as_uint(o[4 * k]), __float_as_uint(o[4 * k + 1]), __float_as_uint(o[4 * k + 2]),
+                             __float_as_uint(o[4 * k + 3]));
+      }
+    }
+    __syncwarp();
+    // coalesced copy-out of the warp's run (chunks of groups in owned MBs / past the row are skipped)
+    uint8_t* drow = (uint8_t*)a.out + (rowi * a.OW + (int64_t)S * 8 * 32 * wc) * 3 * (int64_t)sizeof(TO);
+#pragma unroll 3
+    for (int k = lane; k < 32 * G::CHUNKS; k += 32) {
+      const int gl = k / G::CHUNKS;
+      if ((amask >> gl) & 1u)
+        *reinterpret_cast<uint4*>(drow + 16 * k) = *reinterpret_cast<const uint4*>(stage + 16 * k);
+    }
+    __syncwarp();
+  }
+}
+
 }  // namespace regen
 
 using namespace regen;
@@ -245,6 +375,7 @@ regen_status scatter_launch(const regen_geom& g, const regen_pack_params& p, int
   a.bin_h = p.bin_h;
   a.inv_s = 1.0f / (float)scale;
   a.mode = mode;
+  a.n_frames = n_frames(g);
   dim3 grid((unsigned)g.frame_h, (unsigned)n_frames(g));
   REGEN_REQUIRE(g.mb == 16, "scatter expects 16-pixel MBs");
   REGEN_REQUIRE(scale == 2 || scale == 3 || scale == 4, "scatter scale must be 2, 3 or 4");
@@ -255,6 +386,27 @@ regen_status scatter_launch(const regen_geom& g, const regen_pack_params& p, int
   const size_t smem = (size_t)g.frame_w * 16 + row_words * 4 + ((size_t)a.GW + 3) / 4 * 16 +
                       3 * (((size_t)g.frame_w * 3 + 15) / 16 * 16) + 16;
   REGEN_REQUIRE(smem <= 200 * 1024, "frame too wide for the scatter kernel (%zu B SMEM)", smem);
+  const size_t es_out = out_dtype == REGEN_DTYPE_BF16 ? 2 : 4;
+  if (mode == SC_BILINEAR && g.frame_w % 8 == 0 && ((size_t)a.OW * 3 * es_out) % 16 == 0 &&
+      getenv("REGEN_OLD_BILINEAR") == nullptr) {
+    const int ngroups = g.frame_w / 8, nwc = (ngroups + 31) / 32;
+    const int64_t items = a.n_frames * a.OH * nwc;
+    const unsigned grid2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>((items + BL_WARPS - 1) / BL_WARPS, 148 * 16));
+    auto go2 = [&](auto kern, int bytes) {
+      const size_t sm2 = (size_t)BL_WARPS * 32 * bytes;
+      if (sm2 > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+      REGEN_TRACE("scatter_bilinear", s);
+      kern<<<grid2, 32 * BL_WARPS, sm2, s>>>(a, nwc);
+    };
+    using bf = __nv_bfloat16;
+#define BL_GO(S_)                                                                      \
+    if (out_dtype == REGEN_DTYPE_BF16) go2(bilinear_kernel<S_, bf>, BL<S_, bf>::BYTES); \
+    else go2(bilinear_kernel<S_, float>, BL<S_, float>::BYTES);
+    if (scale == 2) { BL_GO(2) } else if (scale == 3) { BL_GO(3) } else { BL_GO(4) }
+#undef BL_GO
+    REGEN_LAUNCH_CHECK();
+    return REGEN_OK;
+  }
   auto go = [&](auto kern) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     REGEN_TRACE(mode == SC_BILINEAR ? "scatter_bilinear" : (mode == SC_OWNED ? "scatter_owned" : "scatter"), s);
