@@ -255,7 +255,7 @@ def main() -> None:
     # two pipelines (double-buffered state) so that the index path (select + pack) of batch k+1 runs
     # on one CUDA stream while the SR (enhance + scatter) of batch k runs on another (schedule.py: the
     # same runner the full-size parity test drives)
-    runner = PipelinedRunner(make_pipe, dev)
+    runner = PipelinedRunner(make_pipe, dev, bilinear_on_front=os.environ.get("REGEN_BILINEAR_BACK") != "1")
     pipes = runner.pipes
     p = pipes[0]
     imp = torch.from_numpy(imp_h).to(dev)

@@ -229,7 +229,7 @@ class SRNet:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h is not None and h.value:
+        if h is not None and h.value and lib is not None:   # lib is None at interpreter shutdown
             lib.regen_sr_destroy(h)
             self.handle = None
 

@@ -116,13 +116,13 @@ __global__ void __launch_bounds__(SC_THREADS, 8) scatter_rows_kernel(ScatterArgs
       const uint8_t* r0 = lr + (yl0 - (y - 1)) * W3p;   // slot k holds row clamp(y-1+k)
       const uint8_t* r1 = lr + (yl1 - (y - 1)) * W3p;
       for (int x = threadIdx.x; x < W; x += SC_THREADS) {
-        float4 v;
+        float4 v;   // pre-scaled by 1/255 (the same arithmetic as bilinear_kernel: bit-identical pixels)
         float p0 = (float)r0[3 * x], p1 = (float)r1[3 * x];
-        v.x = fmaf(ly, p1 - p0, p0);
+        v.x = __fmul_rn(fmaf(ly, p1 - p0, p0), 1.0f / 255.0f);
         p0 = (float)r0[3 * x + 1]; p1 = (float)r1[3 * x + 1];
-        v.y = fmaf(ly, p1 - p0, p0);
+        v.y = __fmul_rn(fmaf(ly, p1 - p0, p0), 1.0f / 255.0f);
         p0 = (float)r0[3 * x + 2]; p1 = (float)r1[3 * x + 2];
-        v.z = fmaf(ly, p1 - p0, p0);
+        v.z = __fmul_rn(fmaf(ly, p1 - p0, p0), 1.0f / 255.0f);
         v.w = 0.f;
         vr[x] = v;
       }
@@ -151,9 +151,10 @@ __global__ void __launch_bounds__(SC_THREADS, 8) scatter_rows_kernel(ScatterArgs
             if (x >= W - 1) lx = 0.f;                 // last column: i1 = i0
           }
           const int e = 3 * (q * S + j);
-          o[e] = fmaf(lx, B.x - A.x, A.x) * (1.0f / 255.0f);
-          o[e + 1] = fmaf(lx, B.y - A.y, A.y) * (1.0f / 255.0f);
-          o[e + 2] = fmaf(lx, B.z - A.z, A.z) * (1.0f / 255.0f);
+          // explicit rounding (no FMA contraction across the steps): bit-identical to bilinear_kernel
+          o[e] = fmaf(lx, __fsub_rn(B.x, A.x), A.x);
+          o[e + 1] = fmaf(lx, __fsub_rn(B.y, A.y), A.y);
+          o[e + 2] = fmaf(lx, __fsub_rn(B.z, A.z), A.z);
         }
       }
       uint32_t w[WPP];
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(32 * BL_WARPS) bilinear_kernel(ScatterArgs a, 
             // u8 -> fp32 exactly: the byte placed under the exponent of 2^23, minus 2^23
             const float p0 = __uint_as_float(__byte_perm(u0[b >> 2], 0x4B000000u, 0x7650u | (b & 3))) - 8388608.0f;
             const float p1 = __uint_as_float(__byte_perm(u1[b >> 2], 0x4B000000u, 0x7650u | (b & 3))) - 8388608.0f;
-            vr[c][ch] = fmaf(ly, p1 - p0, p0) * (1.0f / 255.0f);
+            vr[c][ch] = __fmul_rn(fmaf(ly, p1 - p0, p0), 1.0f / 255.0f);
           }
       } else {   // first / last group of the row: clamped byte loads
 #pragma unroll
@@ -300,7 +301,7 @@ __global__ void __launch_bounds__(32 * BL_WARPS) bilinear_kernel(ScatterArgs a, 
 #pragma unroll
           for (int ch = 0; ch < 3; ++ch) {
             const float p0 = (float)__ldg(r0 + 3 * cx + ch), p1 = (float)__ldg(r1 + 3 * cx + ch);
-            vr[c][ch] = fmaf(ly, p1 - p0, p0) * (1.0f / 255.0f);
+            vr[c][ch] = __fmul_rn(fmaf(ly, p1 - p0, p0), 1.0f / 255.0f);
           }
         }
       }
@@ -308,7 +309,7 @@ __global__ void __launch_bounds__(32 * BL_WARPS) bilinear_kernel(ScatterArgs a, 
 #pragma unroll
       for (int c = 0; c < 9; ++c)
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) dv[c][ch] = vr[c + 1][ch] - vr[c][ch];
+        for (int ch = 0; ch < 3; ++ch) dv[c][ch] = __fsub_rn(vr[c + 1][ch], vr[c][ch]);
       // horizontal pass at compile-time phases; edge clamps (x == 0 with d = -1, x == W-1 with d = 0)
       // come out of the clamped column loads (A == B: the lerp returns A exactly)
       float o[G::VALS];

@@ -12,7 +12,8 @@ from . import Pipeline
 
 
 class PipelinedRunner:
-    def __init__(self, make_pipe, device):
+    def __init__(self, make_pipe, device, bilinear_on_front: bool = True):
+        self.bilinear_on_front = bilinear_on_front
         self.dev = torch.device(device)
         self.pipes: list[Pipeline] = [make_pipe(), make_pipe()]
         # the index path is a chain of small latency-bound kernels: give its stream the higher priority
@@ -32,10 +33,13 @@ class PipelinedRunner:
                 q.select(imp, stream=self.s_front)
                 q.pack_step(imp, stream=self.s_front)
                 self.front_done[k % 2].record(self.s_front)
-                q.scatter_bilinear(frames, stream=self.s_front)
+                if self.bilinear_on_front:
+                    q.scatter_bilinear(frames, stream=self.s_front)
             with torch.cuda.stream(self.s_back):
                 self.s_back.wait_event(self.front_done[k % 2])
                 q.enhance_owned(frames, stream=self.s_back)
+                if not self.bilinear_on_front:
+                    q.scatter_bilinear(frames, stream=self.s_back)
                 self.back_done[k % 2].record(self.s_back)
 
     def run_eager(self, imp, frames, n_steps: int, stream=None):

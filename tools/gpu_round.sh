@@ -16,8 +16,10 @@ tail -c 600 $O/${TAG}_bench.json
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${TAG}_launches.csv \
     python bench.py --steps 1 --warmup 1 --no-graph --no-cpu-baseline --e2e-steps 0 > $O/${TAG}_ncu_launch.log 2>&1
 echo "ncu launches rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:'resblock|conv_tc|scatter_rows|combine|gather|select_kernel|pack_kernel' -c 14 -o $O/${TAG}_prof -f \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'resblock' -c 2 -o $O/${TAG}_prof_rb -f \
     python bench.py --steps 1 --warmup 0 --no-graph --no-cpu-baseline --e2e-steps 0 > $O/${TAG}_ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on \
+    -k regex:'conv_tc|bilinear|gather|pack_kernel|select_kernel|ccl_kernel|box_write' -c 10 -o $O/${TAG}_prof -f \
+    python bench.py --steps 1 --warmup 0 --no-graph --no-cpu-baseline --e2e-steps 0 >> $O/${TAG}_ncu_full.log 2>&1
 echo "ncu full rc=$?"
-ls -la $O
+ls -la $O; du -sh $O

@@ -15,7 +15,7 @@ import re
 import subprocess
 
 ROLE = {0: "conv_head", 1: "conv_res_a", 2: "conv_res_b", 3: "conv_body", 4: "conv_up", 5: "conv_tail",
-        6: "conv_tiny0", 7: "conv_tiny1", 8: "conv_fold"}
+        6: "conv_tiny0", 7: "conv_tiny1", 8: "conv_fold", 9: "conv_fold_frames"}
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
@@ -25,6 +25,8 @@ def trace_name(kernel: str) -> str | None:
     m = re.search(r"conv_tc_kernel<\(?(?:int\))?(\d+)", kernel)
     if m:
         return ROLE.get(int(m.group(1)))
+    if "bilinear_kernel" in kernel:
+        return "scatter_bilinear"
     if "scatter_rows_kernel" in kernel:
         return "scatter_bilinear" if re.search(r"(true|\(bool\)1|, 1)>", kernel) else "scatter"
     if "combine_kernel" in kernel:
