@@ -41,8 +41,8 @@ def main():
     rnd, launches, raws = sys.argv[1], sys.argv[2], sys.argv[3:]
     print(f"# ncu summary — {rnd}\n")
     print("Captured with `ncu --metrics gpu__time_duration.sum --clock-control none` (launch list) and")
-    print("`ncu --set full --clock-control none -k regex:conv_tc_kernel -s N -c 1` per kernel, on one B200,")
-    print("running `bench.py --steps 1` (C2 workload). ncu times are cold-cache and serialised: compare")
+    print("`ncu --set full --clock-control none --import-source on -k regex:<kernels> -c N` (tools/gpu_round.sh), on")
+    print("one B200, running `bench.py --steps 1 --no-graph` (C2 workload). ncu times are cold-cache and serialised: compare")
     print("shares, not absolutes. Units as reported by ncu (MB = 1e6 bytes unless ncu says otherwise).\n")
     rows = list(csv.reader(open(launches)))
     hdr, data = None, []
