@@ -62,3 +62,56 @@ class PipelinedRunner:
             cap.wait_stream(self.s_front)
             cap.wait_stream(self.s_back)
         return g
+
+    def e2e(self, imp_pin, fr_pin, out_pin, n_steps: int, stream=None) -> float:
+        """End-to-end pipelined throughput through the public calls: per step, H2D of the step's inputs
+        from pinned host memory (copy stream), the index path + bilinear pixels (index stream), the SR
+        pixels (SR stream), and D2H of the step's HR frames into pinned host memory (copy-out stream);
+        step k's copies overlap the compute of steps k-1 / k+1. Double-buffered device inputs and host
+        outputs (out_pin: two pinned tensors shaped like Pipeline.out). Returns device ms per step."""
+        dev = self.dev
+        stream = stream or torch.cuda.current_stream(dev)
+        s_h2d = torch.cuda.Stream(dev)
+        s_d2h = torch.cuda.Stream(dev)
+        imp_d = [torch.empty(imp_pin.shape, dtype=imp_pin.dtype, device=dev) for _ in range(2)]
+        fr_d = [torch.empty(fr_pin.shape, dtype=fr_pin.dtype, device=dev) for _ in range(2)]
+        h2d_done = [torch.cuda.Event() for _ in range(2)]
+        bil_done = [torch.cuda.Event() for _ in range(2)]
+        d2h_done = [torch.cuda.Event() for _ in range(2)]
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        t0.record(stream)
+        for st in (s_h2d, s_d2h, self.s_front, self.s_back):
+            st.wait_stream(stream)
+        for k in range(n_steps):
+            b = k % 2
+            q = self.pipes[b]
+            with torch.cuda.stream(s_h2d):
+                if k >= 2:
+                    s_h2d.wait_event(self.back_done[b])    # step k-2 no longer reads these inputs
+                imp_d[b].copy_(imp_pin, non_blocking=True)
+                fr_d[b].copy_(fr_pin, non_blocking=True)
+                h2d_done[b].record(s_h2d)
+            with torch.cuda.stream(self.s_front):
+                self.s_front.wait_event(h2d_done[b])
+                if k >= 2:
+                    self.s_front.wait_event(d2h_done[b])   # step k-2's frames have left the device
+                q.select(imp_d[b], stream=self.s_front)
+                q.pack_step(imp_d[b], stream=self.s_front)
+                self.front_done[b].record(self.s_front)
+                q.scatter_bilinear(fr_d[b], stream=self.s_front)
+                bil_done[b].record(self.s_front)
+            with torch.cuda.stream(self.s_back):
+                self.s_back.wait_event(self.front_done[b])
+                q.enhance_owned(fr_d[b], stream=self.s_back)
+                self.back_done[b].record(self.s_back)
+            with torch.cuda.stream(s_d2h):
+                s_d2h.wait_event(self.back_done[b])
+                s_d2h.wait_event(bil_done[b])
+                out_pin[b].copy_(q.out, non_blocking=True)
+                d2h_done[b].record(s_d2h)
+        for st in (s_h2d, s_d2h, self.s_front, self.s_back):
+            stream.wait_stream(st)
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+        return t0.elapsed_time(t1) / n_steps
