@@ -406,6 +406,23 @@ def main() -> None:
                      "occupy_ratio_sel_over_box": sel_px / max(box_px, 1),
                      "occupy_ratio_box_over_bin": box_px / max(n_bins * wl.bin_w * wl.bin_h, 1),
                      "sr_network_tflops": flops_step / (stage[2] / 1000.0) / 1e12})
+        # HBM-bound kernels against the measured copy bandwidth: algorithmic bytes per launch / mean
+        # launch time (concurrent replay: includes co-scheduling with the SR stream)
+        es_out = 2 if wl.sr.bf16 else 4
+        s2 = wl.sr.scale * wl.sr.scale
+        lr_bytes = wl.S * wl.F * wl.W * wl.H * 3
+        hbm_alg = {"scatter_bilinear": (s2 * (wl.S * wl.F * wl.W * wl.H - sel_px) * 3 * es_out + lr_bytes,
+                                        "HR bytes of the non-owned pixels written + LR frames read"),
+                   "gather": (box_px * 3 + n_bins * wl.bin_w * wl.bin_h * 16,
+                              "box pixels read (u8 RGB) + packed bins written (8 bf16 channels)")}
+        hbm = {}
+        for name, (nbytes, what) in hbm_alg.items():
+            if name in kern_all:
+                ms = kern_all[name][1] / kern_all[name][0]
+                gbs = nbytes / (ms / 1000.0) / 1e9
+                hbm[name] = {"algorithmic_bytes": int(nbytes), "what": what, "ms_mean": ms, "achieved_gbs": gbs,
+                             "peak_gbs": peaks["hbm_gbs"], "frac": gbs / peaks["hbm_gbs"],
+                             "traffic": load_traffic(name)}
         kernels = {name: {"launches_per_step": n / n_warm, "ms_mean": ms / n,
                           "share": ms / sum(v[1] for v in kern_all.values())} for name, (n, ms) in
                    sorted(kern_all.items(), key=lambda kv: -kv[1][1])}
@@ -426,6 +443,7 @@ def main() -> None:
             "stages_ms": {"select": stage[0], "pack": stage[1], "enhance_scatter": stage[2],
                           "note": "serial instrumented steps, L2 flushed before each"},
             "roofline": roof,
+            "roofline_hbm_kernels": hbm,
             "kernels": kernels,
             "kernels_note": "device ms per launch from a warm replay of the same captured schedule with every libregen "
                             "launch bracketed by CUDA events on its stream (concurrent streams: times include "

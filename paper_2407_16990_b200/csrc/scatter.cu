@@ -282,18 +282,31 @@ __global__ void __launch_bounds__(32 * BL_WARPS) bilinear_kernel(ScatterArgs a, 
         const uint32_t* w0 = reinterpret_cast<const uint32_t*>(r0 + 3 * x0 - 4);
         const uint32_t* w1 = reinterpret_cast<const uint32_t*>(r1 + 3 * x0 - 4);
         uint32_t u0[8], u1[8];
+        if (ly == 0.f) {   // the HR row sits on LR row yl0 (phase fraction 0, or an edge clamp): one row
 #pragma unroll
-        for (int k = 0; k < 8; ++k) { u0[k] = __ldg(w0 + k); u1[k] = __ldg(w1 + k); }
+          for (int k = 0; k < 8; ++k) u0[k] = __ldg(w0 + k);
 #pragma unroll
-        for (int c = 0; c < 10; ++c)
+          for (int c = 0; c < 10; ++c)
 #pragma unroll
-          for (int ch = 0; ch < 3; ++ch) {
-            const int b = 1 + 3 * c + ch;   // byte within the words (compile-time)
-            // u8 -> fp32 exactly: the byte placed under the exponent of 2^23, minus 2^23
-            const float p0 = __uint_as_float(__byte_perm(u0[b >> 2], 0x4B000000u, 0x7650u | (b & 3))) - 8388608.0f;
-            const float p1 = __uint_as_float(__byte_perm(u1[b >> 2], 0x4B000000u, 0x7650u | (b & 3))) - 8388608.0f;
-            vr[c][ch] = __fmul_rn(fmaf(ly, p1 - p0, p0), 1.0f / 255.0f);
-          }
+            for (int ch = 0; ch < 3; ++ch) {
+              const int b = 1 + 3 * c + ch;
+              const float p0 = __uint_as_float(__byte_perm(u0[b >> 2], 0x4B000000u, 0x7650u | (b & 3))) - 8388608.0f;
+              vr[c][ch] = __fmul_rn(p0, 1.0f / 255.0f);   // == fmaf(0, p1 - p0, p0) / 255 exactly
+            }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) { u0[k] = __ldg(w0 + k); u1[k] = __ldg(w1 + k); }
+#pragma unroll
+          for (int c = 0; c < 10; ++c)
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+              const int b = 1 + 3 * c + ch;   // byte within the words (compile-time)
+              // u8 -> fp32 exactly: the byte placed under the exponent of 2^23, minus 2^23
+              const float p0 = __uint_as_float(__byte_perm(u0[b >> 2], 0x4B000000u, 0x7650u | (b & 3))) - 8388608.0f;
+              const float p1 = __uint_as_float(__byte_perm(u1[b >> 2], 0x4B000000u, 0x7650u | (b & 3))) - 8388608.0f;
+              vr[c][ch] = __fmul_rn(fmaf(ly, p1 - p0, p0), 1.0f / 255.0f);
+            }
+        }
       } else {   // first / last group of the row: clamped byte loads
 #pragma unroll
         for (int c = 0; c < 10; ++c) {
