@@ -44,7 +44,7 @@ def _check_index(g, o):
     np.testing.assert_array_equal(g["owner"], o["owner"])
 
 
-@pytest.mark.parametrize("cfg,n_box_sample,n_frame_sample", [("c2", 6, 3), ("c3", 4, 2), ("c5", 2, 2)])
+@pytest.mark.parametrize("cfg,n_box_sample,n_frame_sample", [("c2", 6, 3), ("c3", 4, 2), ("c4g", 3, 2), ("c5", 2, 2)])
 def test_full_size_graph_replay(cfg, n_box_sample, n_frame_sample):
     wl = synth.CONFIGS[cfg]
     seed = 21

@@ -102,6 +102,17 @@ def test_index_path_bit_exact(name, kind, kw):
     _assert_index_equal(g, o)
 
 
+@pytest.mark.parametrize("P", [1, 2, 7])
+def test_index_path_partition_sizes(P):
+    """Block mode (partition_mb = 1: every selected MB its own box, SURVEY §8(f)1 'Block') and the
+    other partition limits of the survey's fill study, bit-exact against the oracle."""
+    wl = dataclasses.replace(synth.small(synth.CONFIGS["c2"], F=3), partition_mb=P)
+    imp = synth.importance_maps(wl.S, wl.F, wl.GH, wl.GW, 13, "noisy")
+    _, g = _run_index(wl, imp, synth.sr_weights(wl.sr, 0))
+    o = _oracle_index(wl, imp)
+    _assert_index_equal(g, o)
+
+
 def test_index_path_small_max_bins_leaves_unplaced():
     wl = dataclasses.replace(synth.small(synth.CONFIGS["c2"], F=3), max_bins=5)
     imp = synth.importance_maps(wl.S, wl.F, wl.GH, wl.GW, 2)
