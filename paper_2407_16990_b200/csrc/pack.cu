@@ -188,6 +188,7 @@ __global__ void __launch_bounds__(256) sort_rank_kernel(regen_box* boxes, const 
 
 constexpr int PACK_POOL = 8192;   // live free areas beyond the register slots (global workspace, L1/L2)
 constexpr int PACK_DIMS = 4096;   // box footprints + indices staged in SMEM in packing order (32 KB)
+constexpr int PACK_SOV = 2048;    // overflow slots 32 .. 32+PACK_SOV-1 in SMEM (32 KB), the rest global
 
 struct PackArgs {
   regen_box* boxes;
@@ -217,11 +218,16 @@ __device__ __forceinline__ bool fits(uint64_t r, int pw, int ph) {
 }
 
 __global__ void __launch_bounds__(32, 1) pack_kernel(PackArgs a) {
-  extern __shared__ uint8_t psm[];
-  uint64_t* key = a.pool;                               // slots >= 32 (rarely used)
-  uint64_t* rect = a.pool + PACK_POOL;
+  extern __shared__ __align__(16) uint8_t psm[];
   uint32_t* dims = (uint32_t*)psm;                      // (w+g) | (h+g)<<16 of the oi-th box in order
   int32_t* ords = (int32_t*)(dims + PACK_DIMS);         // box index of the oi-th box in order
+  uint64_t* skey = (uint64_t*)(ords + PACK_DIMS);       // overflow slots 32 .. 32+PACK_SOV-1 (SMEM)
+  uint64_t* srect = skey + PACK_SOV;
+  uint64_t* gkey = a.pool;                              // overflow slots beyond (global, L1-resident)
+  uint64_t* grect = a.pool + PACK_POOL;
+  // overflow slot i (= pool slot 32 + i)
+  auto ov_key = [&](int i) -> uint64_t& { return i < PACK_SOV ? skey[i] : gkey[i - PACK_SOV]; };
+  auto ov_rect = [&](int i) -> uint64_t& { return i < PACK_SOV ? srect[i] : grect[i - PACK_SOV]; };
   const int lane = threadIdx.x;
   const int64_t n = min(*a.num_boxes, a.max_boxes);
   // placement-invariant pruning bounds: a free area no box fits in (either orientation) is never stored
@@ -271,9 +277,18 @@ __global__ void __launch_bounds__(32, 1) pack_kernel(PackArgs a) {
     uint64_t best = fits(rr, pw, ph) ? rk : ~0ull;
     uint64_t brect = rr;
     int bslot = lane;
-    for (int s = 32 + lane; s < hw; s += 32) {   // overflow slots
-      const uint64_t kk = key[s - 32], rq = rect[s - 32];
-      if (fits(rq, pw, ph) && kk < best) { best = kk; brect = rq; bslot = s; }
+    // overflow slots (only when the pool outgrows the registers): 4 independent loads per lane in flight
+    for (int s0 = 32 + lane; s0 < hw; s0 += 128) {
+      uint64_t kk[4], rq[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int sl = s0 + 32 * u;
+        kk[u] = sl < hw ? ov_key(sl - 32) : ~0ull;
+        rq[u] = sl < hw ? ov_rect(sl - 32) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (fits(rq[u], pw, ph) && kk[u] < best) { best = kk[u]; brect = rq[u]; bslot = s0 + 32 * u; }
     }
     long long t1 = 0;
     if (a.prof) { t1 = clock64(); hw_sum += hw; }
@@ -340,8 +355,8 @@ __global__ void __launch_bounds__(32, 1) pack_kernel(PackArgs a) {
         if (dst < 32) {
           if (lane == dst) { rk = nk; rr = nr; }
         } else if (lane == 0) {
-          key[dst - 32] = nk;
-          rect[dst - 32] = nr;
+          ov_key(dst - 32) = nk;
+          ov_rect(dst - 32) = nr;
         }
       }
       if (free_slot >= 0) {   // nothing refilled the consumed slot: move the last live area into it
@@ -352,14 +367,14 @@ __global__ void __launch_bounds__(32, 1) pack_kernel(PackArgs a) {
             lk = __shfl_sync(0xffffffffu, rk, hw);
             lq = __shfl_sync(0xffffffffu, rr, hw);
           } else {
-            lk = key[hw - 32];
-            lq = rect[hw - 32];
+            lk = ov_key(hw - 32);
+            lq = ov_rect(hw - 32);
           }
           if (free_slot < 32) {
             if (lane == free_slot) { rk = lk; rr = lq; }
           } else if (lane == 0) {
-            key[free_slot - 32] = lk;
-            rect[free_slot - 32] = lq;
+            ov_key(free_slot - 32) = lk;
+            ov_rect(free_slot - 32) = lq;
           }
         }
         if (hw < 32 && lane == hw) { rk = ~0ull; rr = 0ull; }   // the vacated register slot is empty
@@ -503,7 +518,8 @@ extern "C" regen_status regen_pack_regions(const regen_geom* geom, const regen_p
     const char* e = getenv("REGEN_PACK_PROF");
     k.prof = (e && e[0] == '1') ? 1 : 0;
   }
-  const size_t smem = (size_t)PACK_DIMS * 8;   // dims + ords
+  const size_t smem = (size_t)PACK_DIMS * 8 + (size_t)PACK_SOV * 16;   // dims + ords + SMEM overflow slots
+  REGEN_CUDA(cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   {
     REGEN_TRACE("pack", s);
     pack_kernel<<<1, 32, smem, s>>>(k);
