@@ -217,8 +217,34 @@ __device__ __forceinline__ bool fits(uint64_t r, int pw, int ph) {
   return (fw >= pw && fh >= ph) || (fw >= ph && fh >= pw);
 }
 
-__global__ void __launch_bounds__(32, 1) pack_kernel(PackArgs a) {
+// Large pools (thousands of live areas on noisy maps / Block mode / 8-stream groups): when the overflow
+// part of the pool exceeds PACK_BIG slots, warp 0 hands the fit test of that box to all PACK_WARPS warps
+// (named barrier 1: publish the box, each warp scans a strided share of the overflow slots and posts its
+// first fit, warp 0 merges the candidates); small pools keep the single-warp path and the helper warps
+// sleep on the barrier.
+constexpr int PACK_WARPS = 8;
+constexpr int PACK_BIG = 192;
+
+__device__ __forceinline__ void pack_bar() { asm volatile("bar.sync 1, %0;" ::"r"(32 * PACK_WARPS) : "memory"); }
+
+// warp-wide first fit: min key over the lanes' candidates, with the holder's rect and slot
+__device__ __forceinline__ void warp_first_fit(uint64_t best, uint64_t brect, int bslot, uint64_t& wkey,
+                                               uint64_t& wrect, int& wslot) {
+  const uint32_t bhi = (uint32_t)(best >> 32);
+  const uint32_t mhi = __reduce_min_sync(0xffffffffu, bhi);
+  const uint32_t mlo = __reduce_min_sync(0xffffffffu, bhi == mhi ? (uint32_t)best : 0xFFFFFFFFu);
+  wkey = ((uint64_t)mhi << 32) | mlo;
+  const uint32_t hold = __ballot_sync(0xffffffffu, best == wkey);
+  const int hl = hold ? __ffs(hold) - 1 : 0;
+  wrect = __shfl_sync(0xffffffffu, brect, hl);
+  wslot = __shfl_sync(0xffffffffu, bslot, hl);
+}
+
+__global__ void __launch_bounds__(32 * PACK_WARPS, 1) pack_kernel(PackArgs a) {
   extern __shared__ __align__(16) uint8_t psm[];
+  __shared__ int task_hw, task_pw, task_ph;   // the box whose fit test the helper warps join (hw < 0: done)
+  __shared__ uint64_t cand_key[PACK_WARPS], cand_rect[PACK_WARPS];
+  __shared__ int cand_slot[PACK_WARPS];
   uint32_t* dims = (uint32_t*)psm;                      // (w+g) | (h+g)<<16 of the oi-th box in order
   int32_t* ords = (int32_t*)(dims + PACK_DIMS);         // box index of the oi-th box in order
   uint64_t* skey = (uint64_t*)(ords + PACK_DIMS);       // overflow slots 32 .. 32+PACK_SOV-1 (SMEM)
@@ -228,8 +254,35 @@ __global__ void __launch_bounds__(32, 1) pack_kernel(PackArgs a) {
   // overflow slot i (= pool slot 32 + i)
   auto ov_key = [&](int i) -> uint64_t& { return i < PACK_SOV ? skey[i] : gkey[i - PACK_SOV]; };
   auto ov_rect = [&](int i) -> uint64_t& { return i < PACK_SOV ? srect[i] : grect[i - PACK_SOV]; };
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = min(*a.num_boxes, a.max_boxes);
+  if (warp > 0) {
+    // =========== helper warps: join the fit test of large-pool boxes ===========
+    for (;;) {
+      pack_bar();   // B1: a task (or the end) is published
+      const int hw = task_hw, pw = task_pw, ph = task_ph;
+      if (hw < 0) return;
+      uint64_t best = ~0ull, brect = 0;
+      int bslot = -1;
+      for (int s0 = 32 + 32 * warp + lane; s0 < hw; s0 += 128 * PACK_WARPS) {
+        uint64_t kk[4], rq[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int sl = s0 + 32 * PACK_WARPS * u;
+          kk[u] = sl < hw ? ov_key(sl - 32) : ~0ull;
+          rq[u] = sl < hw ? ov_rect(sl - 32) : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (fits(rq[u], pw, ph) && kk[u] < best) { best = kk[u]; brect = rq[u]; bslot = s0 + 32 * PACK_WARPS * u; }
+      }
+      uint64_t wk, wr;
+      int ws;
+      warp_first_fit(best, brect, bslot, wk, wr, ws);
+      if (lane == 0) { cand_key[warp] = wk; cand_rect[warp] = wr; cand_slot[warp] = ws; }
+      pack_bar();   // B2: candidates posted
+    }
+  }
   // placement-invariant pruning bounds: a free area no box fits in (either orientation) is never stored
   int mA = 1 << 30, mB = 1 << 30;
   for (int64_t i = lane; i < n; i += 32) {
@@ -277,36 +330,46 @@ __global__ void __launch_bounds__(32, 1) pack_kernel(PackArgs a) {
     uint64_t best = fits(rr, pw, ph) ? rk : ~0ull;
     uint64_t brect = rr;
     int bslot = lane;
-    // overflow slots (only when the pool outgrows the registers): 4 independent loads per lane in flight
-    for (int s0 = 32 + lane; s0 < hw; s0 += 128) {
+    const bool big = hw - 32 > PACK_BIG;   // warp-uniform
+    if (big) {
+      if (lane == 0) { task_hw = hw; task_pw = pw; task_ph = ph; }
+      pack_bar();   // B1
+    }
+    // overflow slots: this warp's share (all of them on the single-warp path), 4 loads per lane in flight
+    const int ostride = big ? 32 * PACK_WARPS : 32;
+    for (int s0 = 32 + lane; s0 < hw; s0 += 4 * ostride) {
       uint64_t kk[4], rq[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int sl = s0 + 32 * u;
+        const int sl = s0 + ostride * u;
         kk[u] = sl < hw ? ov_key(sl - 32) : ~0ull;
         rq[u] = sl < hw ? ov_rect(sl - 32) : 0ull;
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        if (fits(rq[u], pw, ph) && kk[u] < best) { best = kk[u]; brect = rq[u]; bslot = s0 + 32 * u; }
+        if (fits(rq[u], pw, ph) && kk[u] < best) { best = kk[u]; brect = rq[u]; bslot = s0 + ostride * u; }
     }
     long long t1 = 0;
     if (a.prof) { t1 = clock64(); hw_sum += hw; }
     // 64-bit warp min as two 32-bit REDUX (bin in the high word, sequence in the low word)
-    const uint32_t bhi = (uint32_t)(best >> 32);
-    const uint32_t mhi = __reduce_min_sync(0xffffffffu, bhi);
-    const uint32_t mlo = __reduce_min_sync(0xffffffffu, bhi == mhi ? (uint32_t)best : 0xFFFFFFFFu);
+    uint64_t wkey, wrect;
+    int wslot;
+    warp_first_fit(best, brect, bslot, wkey, wrect, wslot);
+    if (big) {
+      pack_bar();   // B2: the helpers' candidates are posted
+      uint64_t ck = ~0ull, cr = 0;
+      int cs = -1;
+      if (lane == 0) { ck = wkey; cr = wrect; cs = wslot; }
+      else if (lane < PACK_WARPS) { ck = cand_key[lane]; cr = cand_rect[lane]; cs = cand_slot[lane]; }
+      warp_first_fit(ck, cr, cs, wkey, wrect, wslot);
+    }
     int fx, fy, fw, fh, bin, slot = -1;
     bool place = true;
-    if (mhi != 0xFFFFFFFFu || mlo != 0xFFFFFFFFu) {
-      // the lane holding the winner broadcasts its rect and slot
-      const int hl = __ffs(__ballot_sync(0xffffffffu, bhi == mhi && (uint32_t)best == mlo)) - 1;
-      const uint32_t rlo = __shfl_sync(0xffffffffu, (uint32_t)brect, hl);
-      const uint32_t rhi = __shfl_sync(0xffffffffu, (uint32_t)(brect >> 32), hl);
-      slot = __shfl_sync(0xffffffffu, bslot, hl);
-      fx = (int)(rlo & 0xFFFF); fy = (int)(rlo >> 16);
-      fw = (int)(rhi & 0xFFFF); fh = (int)(rhi >> 16);
-      bin = (int)mhi;
+    if (wkey != ~0ull) {
+      slot = wslot;
+      fx = (int)(wrect & 0xFFFF); fy = (int)((wrect >> 16) & 0xFFFF);
+      fw = (int)((wrect >> 32) & 0xFFFF); fh = (int)(wrect >> 48);
+      bin = (int)(wkey >> 32);
     } else if (opened < a.max_bins && ((FW >= pw && FH >= ph) || (FW >= ph && FH >= pw))) {
       bin = opened++;
       fx = 1; fy = 0; fw = FW; fh = FH;
@@ -383,6 +446,8 @@ __global__ void __launch_bounds__(32, 1) pack_kernel(PackArgs a) {
     __syncwarp();   // lane 0's overflow-slot writes are visible to every lane before the next scan
     if (a.prof) c_upd += clock64() - t2;
   }
+  if (lane == 0) task_hw = -1;
+  pack_bar();   // release the helper warps
   if (a.prof && lane == 0)
     printf("[pack-prof] boxes %lld scan %lld dec %lld upd %lld cycles, mean live areas %.1f, bins %d\n", (long long)n,
            c_scan, c_dec, c_upd, n ? (double)hw_sum / n : 0.0, used);
@@ -522,7 +587,7 @@ extern "C" regen_status regen_pack_regions(const regen_geom* geom, const regen_p
   REGEN_CUDA(cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   {
     REGEN_TRACE("pack", s);
-    pack_kernel<<<1, 32, smem, s>>>(k);
+    pack_kernel<<<1, 32 * PACK_WARPS, smem, s>>>(k);
   }
   REGEN_LAUNCH_CHECK();
   if (k.prof) {
