@@ -423,6 +423,17 @@ def main() -> None:
                 hbm[name] = {"algorithmic_bytes": int(nbytes), "what": what, "ms_mean": ms, "achieved_gbs": gbs,
                              "peak_gbs": peaks["hbm_gbs"], "frac": gbs / peaks["hbm_gbs"],
                              "traffic": load_traffic(name)}
+        # whole-step roofline: the slower of the packed-conv FLOPs (box pixels x FLOP per LR
+        # pixel) at the sustained tensor peak and the algorithmic bytes (LR frames + importance read, HR
+        # frames written) at the copy bandwidth
+        bytes_alg = wl.S * wl.F * (wl.W * wl.H * 3 + 4 * wl.GH * wl.GW + s2 * wl.W * wl.H * 3 * es_out)
+        t_tc = flops_step / (peak * 1e12) * 1e3
+        t_hbm = bytes_alg / (peaks["hbm_gbs"] * 1e9) * 1e3
+        t_roof = max(t_tc, t_hbm)
+        step_roof = {"bound": "tensor" if t_tc >= t_hbm else "hbm", "flops_per_step": flops_step,
+                     "bytes_alg_per_step": bytes_alg, "t_tensor_ms": t_tc, "t_hbm_ms": t_hbm,
+                     "roof_value": frames_step * world / (t_roof / 1e3),
+                     "frac": t_roof / (total_ms / args.steps)}
         kernels = {name: {"launches_per_step": n / n_warm, "ms_mean": ms / n,
                           "share": ms / sum(v[1] for v in kern_all.values())} for name, (n, ms) in
                    sorted(kern_all.items(), key=lambda kv: -kv[1][1])}
@@ -444,6 +455,7 @@ def main() -> None:
                           "note": "serial instrumented steps, L2 flushed before each"},
             "roofline": roof,
             "roofline_hbm_kernels": hbm,
+            "roofline_step": step_roof,
             "kernels": kernels,
             "kernels_note": "device ms per launch from a warm replay of the same captured schedule with every libregen "
                             "launch bracketed by CUDA events on its stream (concurrent streams: times include "
