@@ -156,10 +156,53 @@ __device__ __forceinline__ uint64_t box_key(const regen_box& b, int order) {
   return order == REGEN_ORDER_AREA ? (uint64_t)((int64_t)b.w * b.h) : density_ord(b.density);
 }
 
+// n <= SORT_SMEM: one CTA bitonic-sorts (key, index) pairs in SMEM (the order is total: keys tie-broken by
+// the unique index), else every box counts the boxes ahead of it (O(n^2) tiles, large n only)
+constexpr int SORT_SMEM = 4096;   // 48 KB of SMEM: fits beside a resident SR CTA
+
+__device__ __forceinline__ bool sort_before(uint64_t ka, uint32_t ia, uint64_t kb, uint32_t ib) {
+  return ka > kb || (ka == kb && ia < ib);   // density (or area) descending, index ascending
+}
+
+__global__ void __launch_bounds__(1024) sort_bitonic_kernel(regen_box* boxes, const int64_t* num_boxes,
+                                                            int64_t max_boxes, int order, int32_t* out_order) {
+  extern __shared__ __align__(16) uint64_t sk[];
+  uint32_t* si = reinterpret_cast<uint32_t*>(sk + SORT_SMEM);
+  const int64_t n64 = min(*num_boxes, max_boxes);
+  if (n64 <= 0 || n64 > SORT_SMEM) return;
+  const int n = (int)n64;
+  int N = 2;
+  while (N < n) N <<= 1;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    sk[i] = i < n ? box_key(boxes[i], order) : 0ull;          // padding sorts last (key 0, index max)
+    si[i] = i < n ? (uint32_t)i : 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  for (int k = 2; k <= N; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const uint64_t ka = sk[i], kb = sk[l];
+          const uint32_t ia = si[i], ib = si[l];
+          const bool sw = (i & k) == 0 ? sort_before(kb, ib, ka, ia) : sort_before(ka, ia, kb, ib);
+          if (sw) { sk[i] = kb; sk[l] = ka; si[i] = ib; si[l] = ia; }
+        }
+      }
+      __syncthreads();
+    }
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    const uint32_t i = si[p];
+    out_order[p] = (int32_t)i;
+    boxes[i].rank = p;
+  }
+}
+
 __global__ void __launch_bounds__(256) sort_rank_kernel(regen_box* boxes, const int64_t* num_boxes, int64_t max_boxes,
                                                         int order, int32_t* out_order) {
   __shared__ uint64_t tile[1024];
   const int64_t n = min(*num_boxes, max_boxes);
+  if (n <= SORT_SMEM) return;   // sort_bitonic_kernel
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if ((int64_t)blockIdx.x * blockDim.x >= n) return;
   const uint64_t ki = i < n ? box_key(boxes[i], order) : 0;
@@ -188,7 +231,7 @@ __global__ void __launch_bounds__(256) sort_rank_kernel(regen_box* boxes, const 
 
 constexpr int PACK_POOL = 8192;   // live free areas beyond the register slots (global workspace, L1/L2)
 constexpr int PACK_DIMS = 4096;   // box footprints + indices staged in SMEM in packing order (32 KB)
-constexpr int PACK_SOV = 2048;    // overflow slots 32 .. 32+PACK_SOV-1 in SMEM (32 KB), the rest global
+constexpr int PACK_SOV = 1024;    // overflow slots 32 .. 32+PACK_SOV-1 in SMEM (16 KB; 48 KB total so the CTA fits beside a resident SR CTA), the rest global
 
 struct PackArgs {
   regen_box* boxes;
@@ -563,8 +606,12 @@ extern "C" regen_status regen_pack_regions(const regen_geom* geom, const regen_p
   REGEN_LAUNCH_CHECK();
   {
     REGEN_TRACE("sort_rank", s);
-    sort_rank_kernel<<<(unsigned)((max_boxes + 255) / 256), 256, 0, s>>>(d_boxes, d_num_boxes, max_boxes, p->order,
-                                                                         d_order);
+    const size_t ssm = (size_t)SORT_SMEM * 12;
+    REGEN_CUDA(cudaFuncSetAttribute(sort_bitonic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
+    sort_bitonic_kernel<<<1, 1024, ssm, s>>>(d_boxes, d_num_boxes, max_boxes, p->order, d_order);
+    if (max_boxes > SORT_SMEM)
+      sort_rank_kernel<<<(unsigned)((max_boxes + 255) / 256), 256, 0, s>>>(d_boxes, d_num_boxes, max_boxes, p->order,
+                                                                           d_order);
   }
   REGEN_LAUNCH_CHECK();
   PackArgs k;
