@@ -388,16 +388,17 @@ __global__ void __launch_bounds__(ROLE == ROLE_FOLDF ? NTHREADS + 256 : NTHREADS
       const int v = u / p.nchunk, chunk = u - v * p.nchunk;
       const int bin = v / p.nbands, y0 = (v - bin * p.nbands) * S::BSTR + S::ROFF;
       const int nrows = min(S::BRS, p.Hr - y0);
-      // ROLE_FOLDF: the occupancy words of all 66 rows for this warp's 32 pixels, fetched once per
-      // unit (3 per lane) and handed to each row by a shuffle: the epilogue is this kernel's critical
-      // path, so no per-row global-load latency may sit on it
+      // one tile per row (T == 1): the occupancy words of all the band's rows for this warp's 32 pixels
+      // (one word: 32 pixels at res 1, 64 at res 2) are fetched once per unit, <= 3 per lane, and handed
+      // to each row by a shuffle, so no per-row global-load latency sits on the epilogue's path
       uint32_t occ_pre[3] = {0u, 0u, 0u};
-      if constexpr (S::FF) {
+      if constexpr (T == 1) {
+        const int wq = ((32 * q4) / p.res) / 32;
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
           const int r = 32 * q + lane;
           const int y = min(max(y0 + r, 0), p.Hr - 1);
-          if (r < S::BRS) occ_pre[q] = __ldg(p.mbits + ((size_t)bin * p.bin_h + y) * words + q4);
+          if (r < S::BRS) occ_pre[q] = __ldg(p.mbits + ((size_t)bin * p.bin_h + y / p.res) * words + wq);
         }
       }
       for (int k = 0; k < S::NG_OUT; ++k) {
@@ -411,7 +412,7 @@ __global__ void __launch_bounds__(ROLE == ROLE_FOLDF ? NTHREADS + 256 : NTHREADS
         for (int jj = 0; jj < G; ++jj) {
           const int y = min(max(ybase + jj, 0), p.Hr - 1);
           const uint32_t* mrow = p.mbits + ((size_t)bin * p.bin_h + y / p.res) * words;
-          if constexpr (S::FF) {
+          if constexpr (T == 1) {
             const int r = G * k + jj;   // band-local row; shuffle the prefetched word (warp-uniform r)
             const uint32_t w01 = r < 32 ? occ_pre[0] : occ_pre[1];
             occw[jj][0] = __shfl_sync(0xffffffffu, r < 64 ? w01 : occ_pre[2], r & 31);
