@@ -182,11 +182,11 @@ __global__ void __launch_bounds__(ROLE == ROLE_FOLDF ? NTHREADS + 256 : NTHREADS
     for (int i = 0; i < S::OGR; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
     for (int i = 0; i < 2; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
     for (int i = 0; i < 4; ++i) { mbar_init(&unit_full[i], 1); mbar_init(&unit_empty[i], S::FF ? 17 : 9); }
-    // a partial-sum row is written by one epilogue quad (4 warp arrivals) and read by the three
-    // combines of rows r-1, r, r+1 (3 x 4 warp arrivals; band-edge rows get the missing ones from
-    // the edge combines)
+    // a partial-sum row is written by one epilogue quad (128 lane arrivals, each lane releasing its own
+    // stores) and read by the three combines of rows r-1, r, r+1 (3 x 128 lane arrivals; band-edge
+    // rows get the missing ones from the edge combines)
     if (S::FF)
-      for (int i = 0; i < FF_NPR; ++i) { mbar_init(&prow_full[i], 4); mbar_init(&prow_empty[i], 12); }
+      for (int i = 0; i < FF_NPR; ++i) { mbar_init(&prow_full[i], 128); mbar_init(&prow_empty[i], 3 * 128); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -475,8 +475,7 @@ __global__ void __launch_bounds__(ROLE == ROLE_FOLDF ? NTHREADS + 256 : NTHREADS
 #pragma unroll
               for (int g = 0; g < CP / 8; ++g) *reinterpret_cast<uint4*>(rowp + g * FF_W * 16) = make_uint4(0, 0, 0, 0);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&prow_full[sl]);
+            mbar_arrive(&prow_full[sl]);   // every writer lane releases its own row stores
           } else if (j < nrows) {
 #pragma unroll
             for (int t = 0; t < T; ++t) {
@@ -601,8 +600,7 @@ __global__ void __launch_bounds__(ROLE == ROLE_FOLDF ? NTHREADS + 256 : NTHREADS
                 acc);
             fold::store_frame<PS>(acc, b0, b1, b2, dst, 1, x, y, p.fOW, p.fout, p.fout_fp32);
           }
-          __syncwarp();
-          if (lane == 0) {
+          {   // every combiner lane releases its own reads of the three rows
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
               // row c-1+d read once by this combine; the band-edge rows 0, 1, 64, 65 also take the

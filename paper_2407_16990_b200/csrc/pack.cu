@@ -268,7 +268,11 @@ __device__ __forceinline__ bool fits(uint64_t r, int pw, int ph) {
 constexpr int PACK_WARPS = 8;
 constexpr int PACK_BIG = 192;
 
-__device__ __forceinline__ void pack_bar() { asm volatile("bar.sync 1, %0;" ::"r"(32 * PACK_WARPS) : "memory"); }
+// non-.aligned named barrier, entered by whole warps after a __syncwarp (lane-0 branches precede it)
+__device__ __forceinline__ void pack_bar() {
+  __syncwarp();
+  asm volatile("barrier.sync 1, %0;" ::"r"(32 * PACK_WARPS) : "memory");
+}
 
 // warp-wide first fit: min key over the lanes' candidates, with the holder's rect and slot
 __device__ __forceinline__ void warp_first_fit(uint64_t best, uint64_t brect, int bslot, uint64_t& wkey,
