@@ -233,6 +233,28 @@ __global__ void __launch_bounds__(SC_THREADS, 8) scatter_rows_kernel(ScatterArgs
 // columns: a group never straddles one). The first and last group of a row take a clamped path.
 constexpr int BL_WARPS = 4;
 
+// packed fp32x2 arithmetic (sm_100: FADD2 / FFMA2 / FMUL2), round-to-nearest per element
+__device__ __forceinline__ unsigned long long f2pack(float lo, float hi) {
+  return (unsigned long long)__float_as_uint(lo) | ((unsigned long long)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ float f2lo(unsigned long long v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float f2hi(unsigned long long v) { return __uint_as_float((uint32_t)(v >> 32)); }
+__device__ __forceinline__ unsigned long long f2sub(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long f2mul(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long f2fma(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
 template <int S, typename TO>
 struct BL {
   static constexpr int VALS = 8 * S * 3;                        // values per group
@@ -296,16 +318,23 @@ __global__ void __launch_bounds__(32 * BL_WARPS) bilinear_kernel(ScatterArgs a, 
         } else {
 #pragma unroll
           for (int k = 0; k < 8; ++k) { u0[k] = __ldg(w0 + k); u1[k] = __ldg(w1 + k); }
+          // the 30 values as 15 pairs, each step one packed fp32x2 instruction (FADD2/FFMA2/FMUL2:
+          // per-element IEEE round-to-nearest, bit-identical to the scalar chain of the row kernel)
+          float* vf = &vr[0][0];
+          const unsigned long long m23 = f2pack(8388608.0f, 8388608.0f), k255 = f2pack(1.0f / 255.0f, 1.0f / 255.0f);
+          const unsigned long long ly2 = f2pack(ly, ly);
 #pragma unroll
-          for (int c = 0; c < 10; ++c)
-#pragma unroll
-            for (int ch = 0; ch < 3; ++ch) {
-              const int b = 1 + 3 * c + ch;   // byte within the words (compile-time)
-              // u8 -> fp32 exactly: the byte placed under the exponent of 2^23, minus 2^23
-              const float p0 = __uint_as_float(__byte_perm(u0[b >> 2], 0x4B000000u, 0x7650u | (b & 3))) - 8388608.0f;
-              const float p1 = __uint_as_float(__byte_perm(u1[b >> 2], 0x4B000000u, 0x7650u | (b & 3))) - 8388608.0f;
-              vr[c][ch] = __fmul_rn(fmaf(ly, p1 - p0, p0), 1.0f / 255.0f);
-            }
+          for (int e = 0; e < 30; e += 2) {
+            const int b0 = 1 + e, b1 = 2 + e;   // bytes within the words (compile-time)
+            const unsigned long long q0 = f2pack(__uint_as_float(__byte_perm(u0[b0 >> 2], 0x4B000000u, 0x7650u | (b0 & 3))),
+                                                 __uint_as_float(__byte_perm(u0[b1 >> 2], 0x4B000000u, 0x7650u | (b1 & 3))));
+            const unsigned long long q1 = f2pack(__uint_as_float(__byte_perm(u1[b0 >> 2], 0x4B000000u, 0x7650u | (b0 & 3))),
+                                                 __uint_as_float(__byte_perm(u1[b1 >> 2], 0x4B000000u, 0x7650u | (b1 & 3))));
+            const unsigned long long p0 = f2sub(q0, m23), p1 = f2sub(q1, m23);
+            const unsigned long long r = f2mul(f2fma(ly2, f2sub(p1, p0), p0), k255);
+            vf[e] = f2lo(r);
+            vf[e + 1] = f2hi(r);
+          }
         }
       } else {   // first / last group of the row: clamped byte loads
 #pragma unroll
