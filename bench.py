@@ -255,7 +255,7 @@ def main() -> None:
     # two pipelines (double-buffered state) so that the index path (select + pack) of batch k+1 runs
     # on one CUDA stream while the SR (enhance + scatter) of batch k runs on another (schedule.py: the
     # same runner the full-size parity test drives)
-    runner = PipelinedRunner(make_pipe, dev, bilinear_on_front=os.environ.get("REGEN_BILINEAR_BACK") != "1")
+    runner = PipelinedRunner(make_pipe, dev, bilinear=os.environ.get("REGEN_BILINEAR", "side"))
     pipes = runner.pipes
     p = pipes[0]
     imp = torch.from_numpy(imp_h).to(dev)
@@ -448,7 +448,7 @@ def main() -> None:
                        "l2": "timed steps run back to back; each step's working set (~2 GB of packed activations "
                              "and HR intermediates) is >10x the 126 MB L2, so no step finds the previous one's data",
                        "schedule": "index path (select+pack) of batch k+1 overlapped with SR (enhance+scatter) of batch k "
-                                   "on two CUDA streams, double-buffered pipeline state"
+                                   "on two CUDA streams (bilinear pass on a third, lowest-priority stream), double-buffered pipeline state"
                                    + ("; the K steps replayed as one captured CUDA graph" if graph is not None else ""),
                        "parallelism": f"weak dp{world} (streams sharded by rank, no data-path collective)"},
             "stages_ms": {"select": stage[0], "pack": stage[1], "enhance_scatter": stage[2],

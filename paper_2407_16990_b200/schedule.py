@@ -12,16 +12,24 @@ from . import Pipeline
 
 
 class PipelinedRunner:
-    def __init__(self, make_pipe, device, bilinear_on_front: bool = True):
-        self.bilinear_on_front = bilinear_on_front
+    def __init__(self, make_pipe, device, bilinear: str = "side"):
+        """bilinear: where regen_scatter_bilinear of a batch runs — "side" (its own lowest-priority
+        stream after the batch's index path), "front" (the index stream) or "back" (the SR stream)."""
+        assert bilinear in ("side", "front", "back")
+        self.bilinear = bilinear
         self.dev = torch.device(device)
         self.pipes: list[Pipeline] = [make_pipe(), make_pipe()]
-        # the index path is a chain of small latency-bound kernels: give its stream the higher priority
-        # so its CTAs are dispatched as soon as the SR kernels' CTAs free an SM
-        self.s_front = torch.cuda.Stream(self.dev, priority=-1)
-        self.s_back = torch.cuda.Stream(self.dev, priority=0)
+        # priorities: the index path (a chain of small latency-bound kernels) highest, so its CTAs are
+        # dispatched as soon as the SR kernels' CTAs free an SM; the SR stream next; the bilinear pass
+        # (HBM filler that co-runs beside the persistent SR CTAs) lowest
+        least, greatest = torch.cuda.Stream.priority_range()
+        mid = min(least, greatest + 1)
+        self.s_front = torch.cuda.Stream(self.dev, priority=greatest)
+        self.s_back = torch.cuda.Stream(self.dev, priority=mid)
+        self.s_side = torch.cuda.Stream(self.dev, priority=least)
         self.front_done = [torch.cuda.Event() for _ in range(2)]
         self.back_done = [torch.cuda.Event() for _ in range(2)]
+        self.side_done = [torch.cuda.Event() for _ in range(2)]
 
     def steps(self, imp, frames, n_steps: int, capturing: bool = False):
         """Enqueue n_steps pipelined steps (each: one batch through select -> pack -> enhance+scatter)."""
@@ -30,25 +38,32 @@ class PipelinedRunner:
             with torch.cuda.stream(self.s_front):
                 if not (capturing and k < 2):
                     self.s_front.wait_event(self.back_done[k % 2])   # buffers of batch k-2 are free
+                    if self.bilinear == "side":
+                        self.s_front.wait_event(self.side_done[k % 2])
                 q.select(imp, stream=self.s_front)
                 q.pack_step(imp, stream=self.s_front)
                 self.front_done[k % 2].record(self.s_front)
-                if self.bilinear_on_front:
+                if self.bilinear == "front":
                     q.scatter_bilinear(frames, stream=self.s_front)
+            if self.bilinear == "side":
+                with torch.cuda.stream(self.s_side):
+                    self.s_side.wait_event(self.front_done[k % 2])
+                    q.scatter_bilinear(frames, stream=self.s_side)
+                    self.side_done[k % 2].record(self.s_side)
             with torch.cuda.stream(self.s_back):
                 self.s_back.wait_event(self.front_done[k % 2])
                 q.enhance_owned(frames, stream=self.s_back)
-                if not self.bilinear_on_front:
+                if self.bilinear == "back":
                     q.scatter_bilinear(frames, stream=self.s_back)
                 self.back_done[k % 2].record(self.s_back)
 
     def run_eager(self, imp, frames, n_steps: int, stream=None):
         stream = stream or torch.cuda.current_stream(self.dev)
-        self.s_front.wait_stream(stream)
-        self.s_back.wait_stream(stream)
+        for st in (self.s_front, self.s_back, self.s_side):
+            st.wait_stream(stream)
         self.steps(imp, frames, n_steps)
-        stream.wait_stream(self.s_front)
-        stream.wait_stream(self.s_back)
+        for st in (self.s_front, self.s_back, self.s_side):
+            stream.wait_stream(st)
 
     def capture(self, imp, frames, n_steps: int) -> torch.cuda.CUDAGraph:
         """One CUDA graph holding n_steps pipelined steps (fork/join on a capture stream)."""
@@ -56,11 +71,11 @@ class PipelinedRunner:
         cap.wait_stream(torch.cuda.current_stream(self.dev))
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=cap):
-            self.s_front.wait_stream(cap)
-            self.s_back.wait_stream(cap)
+            for st in (self.s_front, self.s_back, self.s_side):
+                st.wait_stream(cap)
             self.steps(imp, frames, n_steps, capturing=True)
-            cap.wait_stream(self.s_front)
-            cap.wait_stream(self.s_back)
+            for st in (self.s_front, self.s_back, self.s_side):
+                cap.wait_stream(st)
         return g
 
     def e2e(self, imp_pin, fr_pin, out_pin, n_steps: int, stream=None) -> float:
