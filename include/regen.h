@@ -48,7 +48,16 @@ typedef enum {
 
 enum { REGEN_MODE_TOPK = 0, REGEN_MODE_THRESHOLD = 1 };
 enum { REGEN_SCOPE_GLOBAL = 0, REGEN_SCOPE_PER_STREAM = 1, REGEN_SCOPE_PER_FRAME = 2 };
-enum { REGEN_ORDER_DENSITY = 0, REGEN_ORDER_AREA = 1 };
+enum { REGEN_ORDER_DENSITY = 0, REGEN_ORDER_AREA = 1, REGEN_ORDER_HEIGHT = 2 };
+/* placement policy of the packer (regen_pack_params.policy): GUILLOTINE = Alg. 1 with InnerFree read
+ * as a guillotine split (D6, default); MAXRECT = Alg. 2 literally: one free area per bin, the maximal
+ * empty rectangle of the bin's free cells (histogram-stack method), re-computed after
+ * every placement (D14); SKYLINE = bottom-left skyline per bin (D15); SHELF = first-fit shelves per
+ * bin (D16). The last two are the survey's comparison policies. */
+enum { REGEN_POLICY_GUILLOTINE = 0, REGEN_POLICY_MAXRECT = 1, REGEN_POLICY_SKYLINE = 2, REGEN_POLICY_SHELF = 3 };
+/* importance density of a box (Alg. 1 l.6): SPAN = mean over every MB of the box's MB span (P:751
+ * "all MBs in it", D4, default); MEMBERS = mean over its member MBs only (P:691's set notation). */
+enum { REGEN_DENSITY_SPAN = 0, REGEN_DENSITY_MEMBERS = 1 };
 enum { REGEN_DTYPE_BF16 = 0, REGEN_DTYPE_FP32 = 1 };
 enum { REGEN_CALL_SELECT = 0, REGEN_CALL_PACK = 1, REGEN_CALL_ENHANCE = 2, REGEN_CALL_SCATTER = 3,
        REGEN_CALL_ENHANCE_SCATTER = 4 };
@@ -74,6 +83,8 @@ typedef struct {
   int64_t k;             /* TOPK: count per scope segment (>= 0). THRESHOLD: cap (-1 = none) */
   float tau;             /* THRESHOLD only; must not be NaN */
   int32_t connectivity;  /* 8 (default, D3) or 4 */
+  int64_t cap;           /* capacity cap N of P:663 (MB_size*N <= H*W*B: regen_capacity_mbs), applied to
+                            every scope segment in both modes on top of k; -1 = none */
 } regen_select_params;
 
 /* Region-aware bin packing, Alg. 1 P:677-719 (D4-D8, D12). */
@@ -83,7 +94,10 @@ typedef struct {
   int32_t expand;          /* pixels of expansion around a box, 3 */
   int32_t partition_mb;    /* Partition preset size in MBs (D5): 4 for 128-px bins, 3 for 64-px */
   int32_t gutter;          /* zero gutter right/below each box (D8), 1 */
-  int32_t order;           /* REGEN_ORDER_DENSITY (Alg. 1 l.6) or REGEN_ORDER_AREA (max-area-first) */
+  int32_t order;           /* REGEN_ORDER_DENSITY (Alg. 1 l.6), REGEN_ORDER_AREA (max-area-first) or
+                              REGEN_ORDER_HEIGHT (box height desc, for shelves); ties by box index */
+  int32_t policy;          /* REGEN_POLICY_* (placement rule, default GUILLOTINE) */
+  int32_t density;         /* REGEN_DENSITY_SPAN (default) or REGEN_DENSITY_MEMBERS */
 } regen_pack_params;
 
 /* SR network (D11): EDSR-baseline, or the tiny 2-conv model when n_resblocks == 0. */
@@ -93,6 +107,12 @@ typedef struct {
   int32_t n_resblocks;  /* 0 => tiny model: conv 3->C, ReLU, conv C->3s^2, PixelShuffle(s) */
   int32_t dtype;        /* REGEN_DTYPE_BF16 (tcgen05, bf16 storage, fp32 accumulate) or REGEN_DTYPE_FP32 */
   float res_scale;      /* residual scaling, 1.0 */
+  int32_t bin_w;        /* bin width the handle is planned for (BF16: every conv's tcgen05 plan and B
+                           image are built by regen_sr_create for it; enhance calls with another
+                           bin_w return REGEN_E_INVALID). BF16 requires channels % 16 == 0,
+                           bin_w % 128 == 0 and n_resblocks > 0: there is no silent fallback to a
+                           CUDA-core kernel, other BF16 configs return REGEN_E_UNSUPPORTED. FP32 runs
+                           every conv on the fp32 CUDA-core kernel (the C1 model). */
 } regen_sr_config;
 
 /* Region record (Alg. 1 l.3): id order = (stream, frame, smallest raster index) (D3). 32 bytes. */
@@ -125,6 +145,8 @@ typedef struct {
  *   d_labels      [S][F][GH][GW] int32 region id of each selected MB, -1 otherwise (out)
  *   d_regions     [max_regions] region records (out); d_num_regions: int64 count (out, may exceed
  *                 max_regions => REGEN_ST_REGION_OVERFLOW and records truncated)
+ *   d_status      reset to 0 on `stream` first (this is the first call of a batch; the later calls
+ *                 of the batch OR their overflow bits into it)
  * ------------------------------------------------------------------------------------------- */
 REGEN_API regen_status regen_select_mbs(const regen_geom* geom, const regen_select_params* params,
                               const float* d_importance, uint32_t* d_sel_bitmap, int32_t* d_labels,
@@ -150,7 +172,10 @@ REGEN_API regen_status regen_pack_regions(const regen_geom* geom, const regen_pa
  * SR network handle. h_weights: host fp32, per conv W[Cout][Cin][3][3] then bias[Cout], in
  * network order (D11): head, 2 per resblock, body, upsampler conv(s), tail; tiny: conv0, conv1.
  * n_weights must equal the sum. Weights are repacked once (bf16 per-tap tensor-core layout for
- * BF16) and copied to the device; the caller's buffer may be freed afterwards. Not stream-ordered.
+ * BF16, planned for cfg->bin_w) and copied to the device with synchronous copies; the caller's
+ * buffer may be freed afterwards. Not stream-ordered: call it before capturing or launching work.
+ * After create, every enhance call is free of host synchronisation and allocation, and a handle may
+ * be used from several host threads (it is read-only after create).
  * ------------------------------------------------------------------------------------------- */
 REGEN_API regen_status regen_sr_create(const regen_sr_config* cfg, const float* h_weights, size_t n_weights,
                              void** out_handle);
@@ -252,7 +277,7 @@ REGEN_API regen_status regen_trace_read(char* names, float* ms, int32_t cap, int
 REGEN_API int64_t regen_capacity_mbs(int32_t bin_w, int32_t bin_h, int32_t n_bins, int32_t mb);  /* floor(H*W*B/mb^2) */
 REGEN_API const char* regen_status_string(regen_status s);
 REGEN_API const char* regen_last_error(void);
-REGEN_API int32_t regen_abi_version(void);   /* 1 */
+REGEN_API int32_t regen_abi_version(void);   /* 2 */
 
 #ifdef __cplusplus
 }

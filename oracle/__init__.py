@@ -23,14 +23,15 @@ _lib = None
 
 MODE_TOPK, MODE_THRESHOLD = 0, 1
 SCOPE_GLOBAL, SCOPE_PER_STREAM, SCOPE_PER_FRAME = 0, 1, 2
-ORDER_DENSITY, ORDER_AREA = 0, 1
+ORDER_DENSITY, ORDER_AREA, ORDER_HEIGHT = 0, 1, 2
+DENSITY_SPAN, DENSITY_MEMBERS = 0, 1
 
 
 def build(force: bool = False) -> str:
     """Compile liboracle.so (gcc, no fast-math, no FMA contraction)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off",
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-pthread", "-ffp-contract=off",
                                "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
@@ -64,12 +65,13 @@ def round_bf16(x: np.ndarray) -> np.ndarray:
 # ----------------------------------------------------------------------------------- steps
 
 def select(importance: np.ndarray, W: int, H: int, mode: int, k: int, tau: float = 0.0,
-           scope: int = SCOPE_GLOBAL, mb: int = 16) -> np.ndarray:
-    """O2: uint8 [S][F][GH][GW] selection mask."""
+           scope: int = SCOPE_GLOBAL, mb: int = 16, cap: int = -1) -> np.ndarray:
+    """O2: uint8 [S][F][GH][GW] selection mask (cap >= 0: capacity N of P:663)."""
     imp = np.ascontiguousarray(importance, np.float32)
     S, F = imp.shape[:2]
     sel = np.zeros(imp.shape, np.uint8)
-    rc = lib().ref_select(S, F, W, H, mb, mode, ctypes.c_int64(k), ctypes.c_float(tau), scope, _p(imp), _p(sel))
+    rc = lib().ref_select(S, F, W, H, mb, mode, ctypes.c_int64(k), ctypes.c_float(tau), scope, ctypes.c_int64(cap),
+                          _p(imp), _p(sel))
     assert rc == 0
     return sel
 
@@ -88,7 +90,7 @@ def regions(sel: np.ndarray, W: int, H: int, conn: int = 8, mb: int = 16):
 
 
 def boxes(importance: np.ndarray, labels: np.ndarray, regs: np.ndarray, W: int, H: int,
-          expand: int = 3, partition_mb: int = 4, mb: int = 16):
+          expand: int = 3, partition_mb: int = 4, mb: int = 16, density_mode: int = DENSITY_SPAN):
     """O4 (Alg.1 l.4-6): boxes int32 [n][12], density f64 [n], box_of_mb int32 [S][F][GH][GW]."""
     imp = np.ascontiguousarray(importance, np.float32)
     labels = np.ascontiguousarray(labels, np.int32)
@@ -99,7 +101,7 @@ def boxes(importance: np.ndarray, labels: np.ndarray, regs: np.ndarray, W: int, 
     dens = np.zeros(cap, np.float64)
     owner = np.empty(labels.shape, np.int32)
     n = _i64p()
-    rc = lib().ref_boxes(S, F, W, H, mb, expand, partition_mb, _p(imp), _p(labels), _p(regs),
+    rc = lib().ref_boxes(S, F, W, H, mb, expand, partition_mb, density_mode, _p(imp), _p(labels), _p(regs),
                          ctypes.c_int64(len(regs)), _p(bx), _p(dens), ctypes.c_int64(cap), ctypes.byref(n), _p(owner))
     assert rc == 0
     return bx[: n.value].copy(), dens[: n.value].copy(), owner
@@ -202,25 +204,36 @@ def sr_crop(cfg, w64: np.ndarray, crop: np.ndarray) -> np.ndarray:
     return out
 
 
+def host_cores() -> int:
+    """Host cores this process may run on (the thread count of the multi-threaded entries)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
 def enhance(cfg, w64: np.ndarray, lr: np.ndarray, bx: np.ndarray, placement: np.ndarray,
-            box_lo: int = 0, box_hi: int | None = None) -> np.ndarray:
-    """O7b: HR bins fp64 [num_bins][s bin_h][s bin_w][3] (boxes [box_lo, box_hi) only)."""
+            box_lo: int = 0, box_hi: int | None = None, threads: int = 1) -> np.ndarray:
+    """O7b: HR bins fp64 [num_bins][s bin_h][s bin_w][3] (boxes [box_lo, box_hi) only).
+    threads > 1: ref_enhance_mt (the same per-box function over POSIX threads, bit-identical)."""
     nb, bh, bw = lr.shape[:3]
     s = cfg.scale
     hr = np.zeros((nb, s * bh, s * bw, 3), np.float64)
     box_hi = len(bx) if box_hi is None else box_hi
-    rc = lib().ref_enhance(s, cfg.channels, cfg.n_resblocks, ctypes.c_double(cfg.res_scale),
-                           _p(np.ascontiguousarray(w64, np.float64)), _p(np.ascontiguousarray(lr, np.float64)),
-                           bw, bh, nb, ctypes.c_int64(len(bx)), _p(np.ascontiguousarray(bx, np.int32)),
-                           _p(np.ascontiguousarray(placement, np.int32)), ctypes.c_int64(box_lo),
-                           ctypes.c_int64(box_hi), _p(hr))
+    args = [s, cfg.channels, cfg.n_resblocks, ctypes.c_double(cfg.res_scale),
+            _p(np.ascontiguousarray(w64, np.float64)), _p(np.ascontiguousarray(lr, np.float64)),
+            bw, bh, nb, ctypes.c_int64(len(bx)), _p(np.ascontiguousarray(bx, np.int32)),
+            _p(np.ascontiguousarray(placement, np.int32)), ctypes.c_int64(box_lo), ctypes.c_int64(box_hi), _p(hr)]
+    rc = lib().ref_enhance_mt(*args, int(threads)) if threads > 1 else lib().ref_enhance(*args)
     assert rc == 0
     return hr
 
 
 def scatter(frames: np.ndarray, bx: np.ndarray, placement: np.ndarray, owner: np.ndarray, hr: np.ndarray,
-            scale: int, bin_w: int, bin_h: int, f_lo: int = 0, f_hi: int | None = None, mb: int = 16) -> np.ndarray:
-    """O8: HR frames fp64 [f_hi-f_lo][s H][s W][3] of the flat (stream, frame) range."""
+            scale: int, bin_w: int, bin_h: int, f_lo: int = 0, f_hi: int | None = None, mb: int = 16,
+            threads: int = 1) -> np.ndarray:
+    """O8: HR frames fp64 [f_hi-f_lo][s H][s W][3] of the flat (stream, frame) range.
+    threads > 1: ref_scatter_mt (same per-frame function over POSIX threads, bit-identical)."""
     fr = np.ascontiguousarray(frames, np.uint8)
     S, F, H, W = fr.shape[:4]
     f_hi = S * F if f_hi is None else f_hi
@@ -228,9 +241,13 @@ def scatter(frames: np.ndarray, bx: np.ndarray, placement: np.ndarray, owner: np
     hr = np.ascontiguousarray(hr, np.float64)
     if hr.size == 0:
         hr = np.zeros(1, np.float64)
-    lib().ref_scatter(S, F, W, H, mb, scale, _p(fr), _p(np.ascontiguousarray(bx, np.int32)),
-                      _p(np.ascontiguousarray(placement, np.int32)), _p(np.ascontiguousarray(owner, np.int32)),
-                      _p(hr), bin_w, bin_h, ctypes.c_int64(f_lo), ctypes.c_int64(f_hi), _p(out))
+    args = [S, F, W, H, mb, scale, _p(fr), _p(np.ascontiguousarray(bx, np.int32)),
+            _p(np.ascontiguousarray(placement, np.int32)), _p(np.ascontiguousarray(owner, np.int32)),
+            _p(hr), bin_w, bin_h, ctypes.c_int64(f_lo), ctypes.c_int64(f_hi), _p(out)]
+    if threads > 1:
+        lib().ref_scatter_mt(*args, int(threads))
+    else:
+        lib().ref_scatter(*args)
     return out
 
 
@@ -239,11 +256,11 @@ def scatter(frames: np.ndarray, bx: np.ndarray, placement: np.ndarray, owner: np
 def index_path(importance: np.ndarray, W: int, H: int, k: int, *, mode: int = MODE_TOPK, tau: float = 0.0,
                scope: int = SCOPE_GLOBAL, conn: int = 8, expand: int = 3, partition_mb: int = 4,
                bin_w: int = 128, bin_h: int = 128, max_bins: int = 4096, gutter: int = 1,
-               order_policy: int = ORDER_DENSITY) -> dict:
+               order_policy: int = ORDER_DENSITY, cap: int = -1, density_mode: int = DENSITY_SPAN) -> dict:
     """Selection -> regions -> boxes -> sort -> pack, in Alg. 1's order."""
-    sel = select(importance, W, H, mode, k, tau, scope)
+    sel = select(importance, W, H, mode, k, tau, scope, cap=cap)
     labels, regs = regions(sel, W, H, conn)
-    bx, dens, box_of = boxes(importance, labels, regs, W, H, expand, partition_mb)
+    bx, dens, box_of = boxes(importance, labels, regs, W, H, expand, partition_mb, density_mode=density_mode)
     order = sort(bx, dens, order_policy)
     pl, nbins = pack(bx, order, bin_w, bin_h, max_bins, gutter)
     return dict(sel=sel, labels=labels, regions=regs, boxes=bx, density=dens, box_of_mb=box_of,

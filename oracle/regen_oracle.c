@@ -5,7 +5,7 @@
  * --impl reference legs may load this library. The product path (paper_2407_16990_b200/) never
  * links, imports or calls it, and shares no header, helper, table or constant generator with it.
  *
- * Plain, slow, single-threaded, written from the paper (arXiv 2407.16990, /root/reference/PAPER.md,
+ * Plain, slow, written from the paper (arXiv 2407.16990, /root/reference/PAPER.md,
  * cited as P:<line>) in the paper's order. Floating point is fp64 except where a stated reading
  * fixes a lower precision (input quantisation to bf16, bf16-rounded conv weights).
  * Readings of the paper's gaps are D1..D12 in DESIGN.md §3; each function names the ones it uses.
@@ -15,13 +15,18 @@
  * pinned to torch fp64 library routines and closed forms, the end-to-end SR is pinned only through
  * those steps plus the isolation invariant ("parity pinned via steps").
  *
- * Build: gcc -O2 -std=c11 -fPIC -shared -ffp-contract=off -o liboracle.so regen_oracle.c
+ * Every step is a single-threaded function; ref_enhance_mt / ref_scatter_mt only distribute the same
+ * per-box / per-frame functions over POSIX threads (bit-identical results, for the all-box parity
+ * checks and the all-cores CPU baseline).
+ *
+ * Build: gcc -O2 -std=c11 -fPIC -shared -pthread -ffp-contract=off -o liboracle.so regen_oracle.c
  * (no -ffast-math: fp64 sums in the stated order; no FMA contraction).
  */
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 #include <math.h>
+#include <pthread.h>
 
 /* ------------------------------------------------------------------------------------------ */
 /* Geometry. P:454 "frames are divided into an array of 16x16-pixel MBs"; P:535 1920x1080 ->   */
@@ -35,7 +40,8 @@ static int grid_h(int H, int mb) { return (H + mb - 1) / mb; }
 /* "constructs a global queue that aggregates and sorts MBs from all streams in order of the    */
 /* importance" and "selects the top N MBs". Reading D2: the queue order is      */
 /* importance descending, ties by linear MB id ascending, id = ((s*F+f)*GH+y)*GW+x; the         */
-/* importance order is IEEE order with -0 == +0 and NaN lowest.                                */
+/* importance order is IEEE order with -0 == +0 and NaN lowest. cap >= 0: the capacity N of     */
+/* P:663 ("max N: MB_size * N <= H * W * B") bounds every scope segment's selection as well.    */
 /* mode 0 = TOPK (k largest), mode 1 = THRESHOLD (score >= tau, P:1352 baseline; if k >= 0 the  */
 /* result is capped to its k first queue entries). scope 0 = GLOBAL (the whole call),    */
 /* 1 = PER_STREAM (Uniform baseline P:1352: k per stream), 2 = PER_FRAME (k per frame).         */
@@ -58,7 +64,7 @@ static int cmp_queue(const void* a, const void* b) {
   return 0;
 }
 
-int ref_select(int S, int F, int W, int H, int mb, int mode, int64_t k, float tau, int scope,
+int ref_select(int S, int F, int W, int H, int mb, int mode, int64_t k, float tau, int scope, int64_t cap,
                const float* score, uint8_t* sel) {
   const int GW = grid_w(W, mb), GH = grid_h(H, mb);
   const int64_t per_frame = (int64_t)GH * GW;
@@ -78,7 +84,8 @@ int ref_select(int S, int F, int W, int H, int mb, int mode, int64_t k, float ta
     }
     qsort(q, (size_t)n, sizeof(sel_item), cmp_queue);          /* the global queue */
     int64_t take = n;
-    if (mode == 0 || k >= 0) take = k < n ? k : n;            /* top-N / cap */
+    if (mode == 0 || k >= 0) take = k < n ? k : n;            /* top-N / threshold cap */
+    if (cap >= 0 && take > cap) take = cap;                   /* capacity N */
     if (take < 0) take = 0;
     for (int64_t i = 0; i < take; ++i) sel[q[i].id] = 1;
   }
@@ -154,7 +161,8 @@ int ref_regions(int S, int F, int W, int H, int mb, int conn, const uint8_t* sel
 /* ------------------------------------------------------------------------------------------ */
 /* O4. Bound + Partition + density, Alg. 1 lines 4-6, footnote P:735    */
 /* (3-pixel expansion). Readings: D4 density = mean importance of ALL MBs in the box's  */
-/* MB span ("average importance of all MBs in it"), fp64, raster order; D5 partition:    */
+/* MB span ("average importance of all MBs in it"), fp64, raster order (density_mode 1:  */
+/* the mean over the box's member MBs only, P:691's set notation); D5 partition:                */
 /* a region whose MB span is wider/taller than P MBs is cut into ceil(n/P) near-equal           */
 /* MB-aligned pieces per axis (the first n mod pieces get one extra MB), pieces are visited in  */
 /* raster order, each piece keeps only the region's member MBs and is re-bounded to them; empty */
@@ -168,7 +176,7 @@ static int piece_start(int n, int pieces, int i) {
   return i * base + (i < rem ? i : rem);
 }
 
-int ref_boxes(int S, int F, int W, int H, int mb, int expand, int partition_mb,
+int ref_boxes(int S, int F, int W, int H, int mb, int expand, int partition_mb, int density_mode,
               const float* score, const int32_t* labels, const int32_t* regions, int64_t num_regions,
               int32_t* boxes, double* density, int64_t max_boxes, int64_t* num_boxes, int32_t* box_of_mb) {
   const int GW = grid_w(W, mb), GH = grid_h(H, mb);
@@ -211,8 +219,9 @@ int ref_boxes(int S, int F, int W, int H, int mb, int expand, int partition_mb,
         /* importance density (line 6 order key) over the full MB span, raster order */
         double sum = 0.0;
         for (int y = my0; y < my1; ++y)
-          for (int x = mx0; x < mx1; ++x) sum += (double)score[base + y * GW + x];
-        density[b] = sum / (double)((mx1 - mx0) * (my1 - my0));
+          for (int x = mx0; x < mx1; ++x)
+            if (density_mode == 0 || labels[base + y * GW + x] == (int32_t)r) sum += (double)score[base + y * GW + x];
+        density[b] = sum / (double)(density_mode == 0 ? (mx1 - mx0) * (my1 - my0) : cnt);
         int32_t* bx = boxes + 12 * b;
         bx[0] = s; bx[1] = f; bx[2] = mx0; bx[3] = my0; bx[4] = mx1; bx[5] = my1;
         bx[6] = x0; bx[7] = y0; bx[8] = x1 - x0; bx[9] = y1 - y0; bx[10] = cnt; bx[11] = (int32_t)r;
@@ -228,7 +237,8 @@ int ref_boxes(int S, int F, int W, int H, int mb, int expand, int partition_mb,
 /* ------------------------------------------------------------------------------------------ */
 /* O5a. Sort, Alg. 1 line 6: boxes in descending importance density; ties   */
 /* by creation index (reading D2 applied to boxes). order 1 = max-area-first baseline (P:753,   */
-/* `fig:Puzzle`): area w*h descending, ties by index. NaN densities sort last.                  */
+/* `fig:Puzzle`): area w*h descending, ties by index; order 2 = box height h descending (shelf  */
+/* packing's usual order), ties by index. NaN densities sort last.                              */
 /* ------------------------------------------------------------------------------------------ */
 static const double* g_sort_density;
 static const int32_t* g_sort_boxes;
@@ -240,6 +250,9 @@ static int cmp_boxes(const void* a, const void* b) {
     const int64_t ai = (int64_t)g_sort_boxes[12 * i + 8] * g_sort_boxes[12 * i + 9];
     const int64_t aj = (int64_t)g_sort_boxes[12 * j + 8] * g_sort_boxes[12 * j + 9];
     if (ai != aj) return ai > aj ? -1 : 1;
+  } else if (g_sort_policy == 2) {
+    const int32_t hi = g_sort_boxes[12 * i + 9], hj = g_sort_boxes[12 * j + 9];
+    if (hi != hj) return hi > hj ? -1 : 1;
   } else {
     const double di = g_sort_density[i], dj = g_sort_density[j];
     const int ni = di != di, nj = dj != dj;
@@ -493,33 +506,95 @@ int ref_sr_crop(int scale, int C, int n_resblocks, double res_scale, const doubl
 /* SR(crop) at (s*bx, s*by) for each placed box (crop = its rotated footprint, read back from    */
 /* lr), zeros elsewhere. Boxes with index in [box_lo, box_hi) only (sampling for large sizes).   */
 /* ------------------------------------------------------------------------------------------ */
+static int enhance_box(int scale, int C, int n_resblocks, double res_scale, const double* weights,
+                       const double* lr, int bin_w, int bin_h, const int32_t* bx, const int32_t* pl, double* hr) {
+  const int HW = scale * bin_w, HH = scale * bin_h;
+  const int rot = pl[3];
+  const int fw = rot ? bx[9] : bx[8], fh = rot ? bx[8] : bx[9];
+  double* in = (double*)malloc(sizeof(double) * 3 * (size_t)fw * fh);
+  double* out = (double*)malloc(sizeof(double) * 3 * (size_t)fw * fh * scale * scale);
+  if (!in || !out) { free(in); free(out); return -1; }
+  for (int c = 0; c < 3; ++c)
+    for (int q = 0; q < fh; ++q)
+      for (int p = 0; p < fw; ++p)
+        in[((int64_t)c * fh + q) * fw + p] = lr[(((int64_t)pl[0] * bin_h + pl[2] + q) * bin_w + pl[1] + p) * 3 + c];
+  const int rc = ref_sr_crop(scale, C, n_resblocks, res_scale, weights, in, fh, fw, out);
+  for (int c = 0; c < 3; ++c)
+    for (int q = 0; q < fh * scale; ++q)
+      for (int p = 0; p < fw * scale; ++p)
+        hr[(((int64_t)pl[0] * HH + scale * pl[2] + q) * HW + scale * pl[1] + p) * 3 + c] =
+            out[((int64_t)c * fh * scale + q) * fw * scale + p];
+  free(in);
+  free(out);
+  return rc;
+}
+
 int ref_enhance(int scale, int C, int n_resblocks, double res_scale, const double* weights,
                 const double* lr, int bin_w, int bin_h, int num_bins, int64_t num_boxes, const int32_t* boxes,
                 const int32_t* placement, int64_t box_lo, int64_t box_hi, double* hr) {
   const int HW = scale * bin_w, HH = scale * bin_h;
   memset(hr, 0, sizeof(double) * (size_t)num_bins * HH * HW * 3);
   for (int64_t b = box_lo; b < box_hi && b < num_boxes; ++b) {
-    const int32_t* bx = boxes + 12 * b;
-    const int32_t* pl = placement + 4 * b;
-    if (pl[0] < 0) continue;
-    const int rot = pl[3];
-    const int fw = rot ? bx[9] : bx[8], fh = rot ? bx[8] : bx[9];
-    double* in = (double*)malloc(sizeof(double) * 3 * (size_t)fw * fh);
-    double* out = (double*)malloc(sizeof(double) * 3 * (size_t)fw * fh * scale * scale);
-    for (int c = 0; c < 3; ++c)
-      for (int q = 0; q < fh; ++q)
-        for (int p = 0; p < fw; ++p)
-          in[((int64_t)c * fh + q) * fw + p] = lr[(((int64_t)pl[0] * bin_h + pl[2] + q) * bin_w + pl[1] + p) * 3 + c];
-    ref_sr_crop(scale, C, n_resblocks, res_scale, weights, in, fh, fw, out);
-    for (int c = 0; c < 3; ++c)
-      for (int q = 0; q < fh * scale; ++q)
-        for (int p = 0; p < fw * scale; ++p)
-          hr[(((int64_t)pl[0] * HH + scale * pl[2] + q) * HW + scale * pl[1] + p) * 3 + c] =
-              out[((int64_t)c * fh * scale + q) * fw * scale + p];
-    free(in);
-    free(out);
+    if (placement[4 * b] < 0) continue;
+    if (enhance_box(scale, C, n_resblocks, res_scale, weights, lr, bin_w, bin_h, boxes + 12 * b, placement + 4 * b,
+                    hr) != 0)
+      return -1;
   }
   return 0;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* Multi-threaded entries (for the all-box parity checks and the all-cores CPU baseline): the   */
+/* same per-box / per-frame functions as the single-threaded ones, distributed round-robin over */
+/* POSIX threads. Boxes occupy disjoint HR-bin footprints and frames disjoint outputs, so the   */
+/* results are bit-identical to ref_enhance / ref_scatter.                                       */
+/* ------------------------------------------------------------------------------------------ */
+typedef struct {
+  int scale, C, n_resblocks, bin_w, bin_h;
+  double res_scale;
+  const double *weights, *lr;
+  const int32_t *boxes, *placement;
+  int64_t lo, hi, stride, first;
+  double* hr;
+  int rc;
+} enhance_job;
+
+static void* enhance_worker(void* arg) {
+  enhance_job* j = (enhance_job*)arg;
+  j->rc = 0;
+  for (int64_t b = j->lo + j->first; b < j->hi; b += j->stride) {
+    if (j->placement[4 * b] < 0) continue;
+    if (enhance_box(j->scale, j->C, j->n_resblocks, j->res_scale, j->weights, j->lr, j->bin_w, j->bin_h,
+                    j->boxes + 12 * b, j->placement + 4 * b, j->hr) != 0)
+      j->rc = -1;
+  }
+  return NULL;
+}
+
+int ref_enhance_mt(int scale, int C, int n_resblocks, double res_scale, const double* weights,
+                   const double* lr, int bin_w, int bin_h, int num_bins, int64_t num_boxes, const int32_t* boxes,
+                   const int32_t* placement, int64_t box_lo, int64_t box_hi, double* hr, int nthreads) {
+  const int HW = scale * bin_w, HH = scale * bin_h;
+  memset(hr, 0, sizeof(double) * (size_t)num_bins * HH * HW * 3);
+  if (box_hi > num_boxes) box_hi = num_boxes;
+  if (nthreads < 1) nthreads = 1;
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)nthreads);
+  enhance_job* jobs = (enhance_job*)malloc(sizeof(enhance_job) * (size_t)nthreads);
+  if (!th || !jobs) { free(th); free(jobs); return -1; }
+  for (int t = 0; t < nthreads; ++t) {
+    enhance_job j = {scale, C, n_resblocks, bin_w, bin_h, res_scale, weights, lr, boxes, placement,
+                     box_lo, box_hi, nthreads, t, hr, 0};
+    jobs[t] = j;
+    pthread_create(&th[t], NULL, enhance_worker, &jobs[t]);
+  }
+  int rc = 0;
+  for (int t = 0; t < nthreads; ++t) {
+    pthread_join(th[t], NULL);
+    if (jobs[t].rc) rc = -1;
+  }
+  free(th);
+  free(jobs);
+  return rc;
 }
 
 /* ------------------------------------------------------------------------------------------ */
@@ -540,44 +615,89 @@ static double lerp_src(int d, int scale, int n, int* i0, int* i1) {
   return src - (double)a;
 }
 
-int ref_scatter(int S, int F, int W, int H, int mb, int scale, const uint8_t* frames, const int32_t* boxes,
-                const int32_t* placement, const int32_t* mb_owner, const double* hr_bins, int bin_w, int bin_h,
-                int64_t f_lo, int64_t f_hi, double* out) {
+static void scatter_frame(int F, int W, int H, int mb, int scale, const uint8_t* frames, const int32_t* boxes,
+                          const int32_t* placement, const int32_t* mb_owner, const double* hr_bins, int bin_w,
+                          int bin_h, int64_t sf, double* o) {
+  (void)F;
   const int GW = grid_w(W, mb), GH = grid_h(H, mb);
   const int OW = W * scale, OH = H * scale;
   const int HW = scale * bin_w, HH = scale * bin_h;
-  for (int64_t sf = f_lo; sf < f_hi && sf < (int64_t)S * F; ++sf) {
-    const uint8_t* img = frames + sf * (int64_t)H * W * 3;
-    double* o = out + (sf - f_lo) * (int64_t)OH * OW * 3;
-    for (int Y = 0; Y < OH; ++Y) {
-      int y0, y1;
-      const double ly = lerp_src(Y, scale, H, &y0, &y1);
-      for (int X = 0; X < OW; ++X) {
-        const int mx = X / (mb * scale), my = Y / (mb * scale);
-        const int32_t b = mb_owner[sf * GH * GW + (int64_t)my * GW + mx];
-        double* px = o + ((int64_t)Y * OW + X) * 3;
-        if (b >= 0) {
-          const int32_t* bx = boxes + 12 * b;
-          const int32_t* pl = placement + 4 * b;
-          const int u = X - scale * bx[6], v = Y - scale * bx[7];
-          int bxp, byp;
-          if (pl[3]) { bxp = scale * pl[1] + (scale * bx[9] - 1 - v); byp = scale * pl[2] + u; }
-          else { bxp = scale * pl[1] + u; byp = scale * pl[2] + v; }
-          const double* src = hr_bins + (((int64_t)pl[0] * HH + byp) * HW + bxp) * 3;
-          px[0] = src[0]; px[1] = src[1]; px[2] = src[2];
-        } else {
-          int x0, x1;
-          const double lx = lerp_src(X, scale, W, &x0, &x1);
-          for (int c = 0; c < 3; ++c) {
-            const double p00 = img[((int64_t)y0 * W + x0) * 3 + c] / 255.0;
-            const double p01 = img[((int64_t)y0 * W + x1) * 3 + c] / 255.0;
-            const double p10 = img[((int64_t)y1 * W + x0) * 3 + c] / 255.0;
-            const double p11 = img[((int64_t)y1 * W + x1) * 3 + c] / 255.0;
-            px[c] = (1.0 - ly) * ((1.0 - lx) * p00 + lx * p01) + ly * ((1.0 - lx) * p10 + lx * p11);
-          }
+  const uint8_t* img = frames + sf * (int64_t)H * W * 3;
+  for (int Y = 0; Y < OH; ++Y) {
+    int y0, y1;
+    const double ly = lerp_src(Y, scale, H, &y0, &y1);
+    for (int X = 0; X < OW; ++X) {
+      const int mx = X / (mb * scale), my = Y / (mb * scale);
+      const int32_t b = mb_owner[sf * GH * GW + (int64_t)my * GW + mx];
+      double* px = o + ((int64_t)Y * OW + X) * 3;
+      if (b >= 0) {
+        const int32_t* bx = boxes + 12 * b;
+        const int32_t* pl = placement + 4 * b;
+        const int u = X - scale * bx[6], v = Y - scale * bx[7];
+        int bxp, byp;
+        if (pl[3]) { bxp = scale * pl[1] + (scale * bx[9] - 1 - v); byp = scale * pl[2] + u; }
+        else { bxp = scale * pl[1] + u; byp = scale * pl[2] + v; }
+        const double* src = hr_bins + (((int64_t)pl[0] * HH + byp) * HW + bxp) * 3;
+        px[0] = src[0]; px[1] = src[1]; px[2] = src[2];
+      } else {
+        int x0, x1;
+        const double lx = lerp_src(X, scale, W, &x0, &x1);
+        for (int c = 0; c < 3; ++c) {
+          const double p00 = img[((int64_t)y0 * W + x0) * 3 + c] / 255.0;
+          const double p01 = img[((int64_t)y0 * W + x1) * 3 + c] / 255.0;
+          const double p10 = img[((int64_t)y1 * W + x0) * 3 + c] / 255.0;
+          const double p11 = img[((int64_t)y1 * W + x1) * 3 + c] / 255.0;
+          px[c] = (1.0 - ly) * ((1.0 - lx) * p00 + lx * p01) + ly * ((1.0 - lx) * p10 + lx * p11);
         }
       }
     }
   }
+}
+
+int ref_scatter(int S, int F, int W, int H, int mb, int scale, const uint8_t* frames, const int32_t* boxes,
+                const int32_t* placement, const int32_t* mb_owner, const double* hr_bins, int bin_w, int bin_h,
+                int64_t f_lo, int64_t f_hi, double* out) {
+  const int64_t frame_px = (int64_t)H * scale * W * scale * 3;
+  for (int64_t sf = f_lo; sf < f_hi && sf < (int64_t)S * F; ++sf)
+    scatter_frame(F, W, H, mb, scale, frames, boxes, placement, mb_owner, hr_bins, bin_w, bin_h, sf,
+                  out + (sf - f_lo) * frame_px);
+  return 0;
+}
+
+typedef struct {
+  int F, W, H, mb, scale, bin_w, bin_h;
+  const uint8_t* frames;
+  const int32_t *boxes, *placement, *mb_owner;
+  const double* hr_bins;
+  int64_t lo, hi, stride, first;
+  double* out;
+} scatter_job;
+
+static void* scatter_worker(void* arg) {
+  scatter_job* j = (scatter_job*)arg;
+  const int64_t frame_px = (int64_t)j->H * j->scale * j->W * j->scale * 3;
+  for (int64_t sf = j->lo + j->first; sf < j->hi; sf += j->stride)
+    scatter_frame(j->F, j->W, j->H, j->mb, j->scale, j->frames, j->boxes, j->placement, j->mb_owner, j->hr_bins,
+                  j->bin_w, j->bin_h, sf, j->out + (sf - j->lo) * frame_px);
+  return NULL;
+}
+
+int ref_scatter_mt(int S, int F, int W, int H, int mb, int scale, const uint8_t* frames, const int32_t* boxes,
+                   const int32_t* placement, const int32_t* mb_owner, const double* hr_bins, int bin_w, int bin_h,
+                   int64_t f_lo, int64_t f_hi, double* out, int nthreads) {
+  if (f_hi > (int64_t)S * F) f_hi = (int64_t)S * F;
+  if (nthreads < 1) nthreads = 1;
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)nthreads);
+  scatter_job* jobs = (scatter_job*)malloc(sizeof(scatter_job) * (size_t)nthreads);
+  if (!th || !jobs) { free(th); free(jobs); return -1; }
+  for (int t = 0; t < nthreads; ++t) {
+    scatter_job j = {F, W, H, mb, scale, bin_w, bin_h, frames, boxes, placement, mb_owner, hr_bins,
+                     f_lo, f_hi, nthreads, t, out};
+    jobs[t] = j;
+    pthread_create(&th[t], NULL, scatter_worker, &jobs[t]);
+  }
+  for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+  free(th);
+  free(jobs);
   return 0;
 }

@@ -19,7 +19,9 @@ LIB_PATH = os.path.join(_HERE, "libregen.so")
 REGEN_OK, REGEN_E_INVALID, REGEN_E_CAPACITY, REGEN_E_CUDA, REGEN_E_UNSUPPORTED = range(5)
 MODE_TOPK, MODE_THRESHOLD = 0, 1
 SCOPE_GLOBAL, SCOPE_PER_STREAM, SCOPE_PER_FRAME = 0, 1, 2
-ORDER_DENSITY, ORDER_AREA = 0, 1
+ORDER_DENSITY, ORDER_AREA, ORDER_HEIGHT = 0, 1, 2
+POLICY_GUILLOTINE, POLICY_MAXRECT, POLICY_SKYLINE, POLICY_SHELF = 0, 1, 2, 3
+DENSITY_SPAN, DENSITY_MEMBERS = 0, 1
 DTYPE_BF16, DTYPE_FP32 = 0, 1
 CALL_SELECT, CALL_PACK, CALL_ENHANCE, CALL_SCATTER, CALL_ENHANCE_SCATTER = 0, 1, 2, 3, 4
 ST_REGION_OVERFLOW, ST_BOX_OVERFLOW, ST_FREELIST_OVERFLOW = 1, 2, 4
@@ -38,18 +40,18 @@ class Geom(ctypes.Structure):
 
 class SelectParams(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int32), ("scope", ctypes.c_int32), ("k", ctypes.c_int64), ("tau", ctypes.c_float),
-                ("connectivity", ctypes.c_int32)]
+                ("connectivity", ctypes.c_int32), ("cap", ctypes.c_int64)]
 
 
 class PackParams(ctypes.Structure):
     _fields_ = [("bin_w", ctypes.c_int32), ("bin_h", ctypes.c_int32), ("max_bins", ctypes.c_int32),
                 ("expand", ctypes.c_int32), ("partition_mb", ctypes.c_int32), ("gutter", ctypes.c_int32),
-                ("order", ctypes.c_int32)]
+                ("order", ctypes.c_int32), ("policy", ctypes.c_int32), ("density", ctypes.c_int32)]
 
 
 class SRConfig(ctypes.Structure):
     _fields_ = [("scale", ctypes.c_int32), ("channels", ctypes.c_int32), ("n_resblocks", ctypes.c_int32),
-                ("dtype", ctypes.c_int32), ("res_scale", ctypes.c_float)]
+                ("dtype", ctypes.c_int32), ("res_scale", ctypes.c_float), ("bin_w", ctypes.c_int32)]
 
 
 REGION_DTYPE = np.dtype([("stream", "<i4"), ("frame", "<i4"), ("root", "<i4"), ("mx0", "<i4"), ("my0", "<i4"),
@@ -218,8 +220,8 @@ class SRNet:
     """Owns a regen_sr_create handle (weights repacked on the device)."""
 
     def __init__(self, scale: int, channels: int, n_resblocks: int, weights: np.ndarray, bf16: bool = True,
-                 res_scale: float = 1.0):
-        self.cfg = SRConfig(scale, channels, n_resblocks, DTYPE_BF16 if bf16 else DTYPE_FP32, res_scale)
+                 res_scale: float = 1.0, bin_w: int = 128):
+        self.cfg = SRConfig(scale, channels, n_resblocks, DTYPE_BF16 if bf16 else DTYPE_FP32, res_scale, bin_w)
         w = np.ascontiguousarray(weights, np.float32)
         h = ctypes.c_void_p(0)
         _check(lib.regen_sr_create(ctypes.byref(self.cfg), w.ctypes.data_as(ctypes.c_void_p), w.size,
@@ -242,13 +244,14 @@ class Pipeline:
 
     def __init__(self, *, S, F, W, H, k, bin_w, bin_h, max_bins, partition_mb, scale, channels, n_resblocks,
                  weights, bf16=True, res_scale=1.0, mode=MODE_TOPK, tau=0.0, scope=SCOPE_GLOBAL, connectivity=8,
-                 expand=3, gutter=1, order=ORDER_DENSITY, max_boxes=None, out_dtype=None, device="cuda"):
+                 expand=3, gutter=1, order=ORDER_DENSITY, max_boxes=None, out_dtype=None, device="cuda", cap=-1,
+                 policy=POLICY_GUILLOTINE, density=DENSITY_SPAN):
         import torch
         self.torch = torch
         self.geom = Geom(S, F, W, H, 16)
-        self.sel = SelectParams(mode, scope, k, tau, connectivity)
-        self.pack = PackParams(bin_w, bin_h, max_bins, expand, partition_mb, gutter, order)
-        self.sr = SRNet(scale, channels, n_resblocks, weights, bf16, res_scale)
+        self.sel = SelectParams(mode, scope, k, tau, connectivity, cap)
+        self.pack = PackParams(bin_w, bin_h, max_bins, expand, partition_mb, gutter, order, policy, density)
+        self.sr = SRNet(scale, channels, n_resblocks, weights, bf16, res_scale, bin_w)
         self.scale = scale
         self.GW, self.GH = (W + 15) // 16, (H + 15) // 16
         self.n_mbs = S * F * self.GH * self.GW
@@ -266,8 +269,8 @@ class Pipeline:
         self.boxes = torch.empty(self.max_boxes * 80, dtype=u8, device=dev)
         self.order = torch.empty(self.max_boxes, dtype=i32, device=dev)
         self.owner = torch.empty(self.n_mbs, dtype=i32, device=dev)
+        # the workspace of the calls run() makes; the separate enhance call (HR bins) grows it on first use
         ws = max(workspace_size(CALL_SELECT, self.geom), workspace_size(CALL_PACK, self.geom),
-                 workspace_size(CALL_ENHANCE, self.geom, self.pack, self.sr.handle),
                  workspace_size(CALL_ENHANCE_SCATTER, self.geom, self.pack, self.sr.handle))
         self.ws = torch.empty(ws, dtype=u8, device=dev)
         self.hr_dtype = DTYPE_BF16 if bf16 else DTYPE_FP32
@@ -294,7 +297,7 @@ class Pipeline:
         return self.counts[1:2]
 
     def select(self, importance, stream=None):
-        self.status.zero_()
+        # regen_select_mbs resets the status word on `stream` (the first call of a batch)
         select_mbs(self.geom, self.sel, importance, self.bitmap, self.labels, self.regions, self.max_regions,
                    self.counts[0:1], self.status, self.ws, stream)
 
@@ -304,6 +307,9 @@ class Pipeline:
                      stream)
 
     def enhance(self, frames, stream=None):
+        need = workspace_size(CALL_ENHANCE, self.geom, self.pack, self.sr.handle)
+        if self.ws.numel() < need:
+            self.ws = self.torch.empty(need, dtype=self.torch.uint8, device=self.out.device)
         enhance_packed(self.sr, self.geom, self.pack, frames, self.boxes, self.max_boxes, self.counts[1:2],
                        self.num_bins, self.hr_bins, self.status, self.ws, stream)
 

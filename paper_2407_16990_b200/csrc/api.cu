@@ -83,4 +83,4 @@ extern "C" const char* regen_status_string(regen_status s) {
 
 extern "C" const char* regen_last_error(void) { return g_err; }
 
-extern "C" int32_t regen_abi_version(void) { return 1; }
+extern "C" int32_t regen_abi_version(void) { return 2; }

@@ -20,6 +20,14 @@ void set_error(const char* fmt, ...);
     }                                   \
   } while (0)
 
+#define REGEN_UNSUPPORTED_IF(cond, ...)  \
+  do {                                  \
+    if (cond) {                         \
+      ::regen::set_error(__VA_ARGS__);  \
+      return REGEN_E_UNSUPPORTED;       \
+    }                                   \
+  } while (0)
+
 #define REGEN_CUDA(call)                                                              \
   do {                                                                                \
     cudaError_t e_ = (call);                                                          \

@@ -854,66 +854,62 @@ void conv_tc_release(SRNet* net) {
   net->tc_plans = nullptr;
 }
 
-// Plans are built lazily per (conv, bin_w) the first time a conv is launched with that bin width.
-static tc::Plan* get_plan(SRNet* net, const ConvDesc& cv, int bin_w) {
+// Every conv's plan and B image for the handle's bin width are built once, by regen_sr_create
+// (conv_tc_plan_all); launches only read them (the handle is immutable afterwards).
+regen_status conv_tc_plan_all(SRNet* net, int bin_w) {
   using namespace tc;
   NetPlans* np = (NetPlans*)net->tc_plans;
-  const size_t idx = &cv - net->convs.data();
-  if (np->plans.size() != net->convs.size()) np->plans.assign(net->convs.size(), Plan());
-  Plan& pl = np->plans[idx];
-  if (pl.ok || pl.cp < 0) {
-    if (pl.ok && net->tc_bin_w == bin_w) return &pl;
-    if (pl.cp < 0 && net->tc_bin_w == bin_w) return nullptr;
-  }
-  if (net->tc_bin_w != bin_w) {   // (re)plan every conv for this bin width
-    for (auto& q : np->plans) q = Plan();
-    net->tc_bin_w = bin_w;
-    std::vector<uint8_t> all;
-    for (size_t i = 0; i < net->convs.size(); ++i) {
-      ConvDesc& d = net->convs[i];
-      std::vector<float> W((size_t)d.cout * d.cin * 9);
-      for (int co = 0; co < d.cout; ++co)
-        for (int ci = 0; ci < d.cin; ++ci)
-          for (int t = 0; t < 9; ++t)
-            W[((size_t)co * d.cin + ci) * 9 + t] = net->tc_weights[d.w_off + ((size_t)co * d.cin8 * 8 + ci) * 9 + t];
-      Plan q;
-      std::vector<uint16_t> img;
-      if (plan_conv(d, net->cfg.channels, d.res, bin_w, q, img, W.data()) &&
-          lookup(d.role, net->cfg.channels, q.cp, q.R, q.G, q.T, d.ps) != nullptr) {
-        all.resize((all.size() + 1023) / 1024 * 1024);
-        d.tc_off = all.size();
-        const uint8_t* b = reinterpret_cast<const uint8_t*>(img.data());
-        all.insert(all.end(), b, b + img.size() * 2);
-        np->plans[i] = q;
-      } else {
-        np->plans[i].cp = -1;
-      }
+  REGEN_REQUIRE(np != nullptr, "tcgen05 weights not prepared");
+  np->plans.assign(net->convs.size(), Plan());
+  net->tc_bin_w = bin_w;
+  std::vector<uint8_t> all;
+  for (size_t i = 0; i < net->convs.size(); ++i) {
+    ConvDesc& d = net->convs[i];
+    std::vector<float> W((size_t)d.cout * d.cin * 9);
+    for (int co = 0; co < d.cout; ++co)
+      for (int ci = 0; ci < d.cin; ++ci)
+        for (int t = 0; t < 9; ++t)
+          W[((size_t)co * d.cin + ci) * 9 + t] = net->tc_weights[d.w_off + ((size_t)co * d.cin8 * 8 + ci) * 9 + t];
+    Plan q;
+    std::vector<uint16_t> img;
+    if (plan_conv(d, net->cfg.channels, d.res, bin_w, q, img, W.data()) &&
+        lookup(d.role, net->cfg.channels, q.cp, q.R, q.G, q.T, d.ps) != nullptr) {
+      all.resize((all.size() + 1023) / 1024 * 1024);
+      d.tc_off = all.size();
+      const uint8_t* bb = reinterpret_cast<const uint8_t*>(img.data());
+      all.insert(all.end(), bb, bb + img.size() * 2);
+      np->plans[i] = q;
+    } else {
+      np->plans[i].cp = -1;
     }
-    cudaFree(net->d_wtc);
-    net->d_wtc = nullptr;
-    if (!all.empty()) {
-      if (cudaMalloc(&net->d_wtc, all.size()) != cudaSuccess ||
-          cudaMemcpy(net->d_wtc, all.data(), all.size(), cudaMemcpyHostToDevice) != cudaSuccess)
-        return nullptr;
-    }
-    net->wtc_bytes = all.size();
   }
-  Plan& q = np->plans[idx];
+  cudaFree(net->d_wtc);
+  net->d_wtc = nullptr;
+  if (!all.empty()) {
+    REGEN_CUDA(cudaMalloc(&net->d_wtc, all.size()));
+    REGEN_CUDA(cudaMemcpy(net->d_wtc, all.data(), all.size(), cudaMemcpyHostToDevice));
+  }
+  net->wtc_bytes = all.size();
+  return REGEN_OK;
+}
+
+static const tc::Plan* tc_plan_of(const SRNet* net, const ConvDesc& cv, int bin_w) {
+  const tc::NetPlans* np = (const tc::NetPlans*)net->tc_plans;
+  if (np == nullptr || net->tc_bin_w != bin_w || np->plans.size() != net->convs.size()) return nullptr;
+  const tc::Plan& q = np->plans[&cv - net->convs.data()];
   return q.ok ? &q : nullptr;
 }
 
-static const tc::Plan* tc_plan_of(SRNet* net, const ConvDesc& cv, int bin_w) { return get_plan(net, cv, bin_w); }
-
 bool conv_tc_supported(const SRNet* net, const ConvDesc& cv, int bin_w) {
   if (!net->use_tc) return false;
-  return get_plan(const_cast<SRNet*>(net), cv, bin_w) != nullptr;
+  return tc_plan_of(net, cv, bin_w) != nullptr;
 }
 
 regen_status conv_tc_launch(const SRNet* net, const ConvDesc& cv, const void* in, void* out, const void* skip,
                             const uint32_t* mbits, int max_bins, const int32_t* d_num_bins, int bin_w, int bin_h,
                             int* counter, cudaStream_t s, int reverse) {
   using namespace tc;
-  const Plan* pl = get_plan(const_cast<SRNet*>(net), cv, bin_w);
+  const Plan* pl = tc_plan_of(net, cv, bin_w);
   REGEN_REQUIRE(pl != nullptr, "no tcgen05 plan for conv");
   Params p;
   memset(&p, 0, sizeof(p));
@@ -951,12 +947,7 @@ regen_status conv_tc_launch(const SRNet* net, const ConvDesc& cv, const void* in
   KernFn kern = lookup(cv.role, net->cfg.channels, pl->cp, pl->R, pl->G, pl->T, cv.ps);
   REGEN_REQUIRE(kern != nullptr, "no tcgen05 kernel instance");
   REGEN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  static int nsm = 0;
-  if (nsm == 0) {
-    int dev;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int nsm = net->n_sm;
   const int units = max_bins * p.nbands * pl->nchunk;
   const int grid = std::min(units, nsm);
   static unsigned long long* d_prof = nullptr;
@@ -999,7 +990,7 @@ namespace regen {
 static const tc::Plan* foldf_plan(const SRNet* net, int bin_w, int& ps) {
   if (!net->use_tc || net->fold_conv < 0) return nullptr;
   const ConvDesc& cv = net->convs[net->fold_conv];
-  const tc::Plan* pl = tc_plan_of(const_cast<SRNet*>(net), cv, bin_w);
+  const tc::Plan* pl = tc_plan_of(net, cv, bin_w);
   if (pl == nullptr || pl->T != 1 || cv.res != 1 || pl->nchunk != 1) return nullptr;
   ps = net->convs[net->fold_conv - 2].ps;
   if (tc::lookup(ROLE_FOLDF, net->cfg.channels, pl->cp, 6, 1, 1, ps) == nullptr) return nullptr;
@@ -1011,8 +1002,7 @@ static const tc::Plan* foldf_plan(const SRNet* net, int bin_w, int& ps) {
 
 bool fold_fused_supported(const SRNet* net, int bin_w) {
   int ps = 0;
-  const char* off = getenv("REGEN_NO_FOLDF");   // A/B aid: the fold conv + standalone combine
-  if (off && off[0] == '1') return false;
+  if (net->no_foldf) return false;   // REGEN_NO_FOLDF=1 at create: the fold conv + standalone combine (A/B aid)
   return foldf_plan(net, bin_w, ps) != nullptr;
 }
 
@@ -1066,10 +1056,7 @@ regen_status fold_fused_launch(const SRNet* net, const void* in, const uint32_t*
   KernFn kern = lookup(ROLE_FOLDF, net->cfg.channels, pl->cp, 6, 1, 1, ps);
   REGEN_REQUIRE(kern != nullptr, "no fused fold kernel instance");
   REGEN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int dev, nsm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = std::min(max_bins * p.nbands, nsm);
+  const int grid = std::min(max_bins * p.nbands, net->n_sm);
   static unsigned long long* d_prof = nullptr;
   static int prof_on = -1;
   if (prof_on < 0) {

@@ -73,6 +73,41 @@ float round_bf16_host(float f) {
 
 using namespace regen;
 
+namespace regen {
+static bool fold_enabled(const SRNet* net, int bin_w);
+
+// The BF16 model runs every conv it executes on the tcgen05 kernels; a configuration with a conv the
+// tensor-core kernels do not tile is rejected here (REGEN_E_UNSUPPORTED) instead of silently running
+// on a CUDA-core kernel. REGEN_FORCE_SIMT=1 (debug/A-B aid, read at create) is the one explicit way to
+// run a BF16 model on the CUDA-core kernel.
+static regen_status check_bf16_kernels(const SRNet* net) {
+  const char* force = getenv("REGEN_FORCE_SIMT");
+  if (force && force[0] == '1') return REGEN_OK;
+  const int bw = net->cfg.bin_w, n = net->cfg.n_resblocks;
+  REGEN_UNSUPPORTED_IF(!net->use_tc, "BF16 model needs channels %% 16 == 0 (got %d)", net->cfg.channels);
+  REGEN_UNSUPPORTED_IF(n == 0, "BF16 tiny model: its C -> 3s^2 conv has no tcgen05 kernel (use FP32)");
+  auto planned = [&](size_t i) { return conv_tc_supported(net, net->convs[i], bw); };
+  REGEN_UNSUPPORTED_IF(!planned(0), "BF16: no tcgen05 plan for the head conv at bin_w %d", bw);
+  if (!resblock_tc_supported(net, bw))
+    for (int i = 1; i <= 2 * n; ++i)
+      REGEN_UNSUPPORTED_IF(!planned(i), "BF16: no tcgen05 plan for residual conv %d at bin_w %d", i, bw);
+  size_t i = 2 * n + 1;
+  REGEN_UNSUPPORTED_IF(!planned(i), "BF16: no tcgen05 plan for the body conv at bin_w %d", bw);
+  ++i;
+  if (net->cfg.scale == 4) {
+    REGEN_UNSUPPORTED_IF(!planned(i), "BF16: no tcgen05 plan for the first x2 upsampler at bin_w %d", bw);
+    ++i;
+  }
+  if (!fold_enabled(net, bw)) {
+    REGEN_UNSUPPORTED_IF(!planned(i), "BF16: no tcgen05 plan for the upsampler conv at bin_w %d", bw);
+    REGEN_UNSUPPORTED_IF(!planned(i + 1), "BF16: no tcgen05 plan for the tail conv at bin_w %d", bw);
+  }
+  return REGEN_OK;
+}
+}  // namespace regen
+
+extern "C" regen_status regen_sr_destroy(void* handle);
+
 extern "C" regen_status regen_sr_create(const regen_sr_config* cfg, const float* h_weights, size_t n_weights,
                                         void** out_handle) {
   REGEN_REQUIRE(cfg && h_weights && out_handle, "null argument");
@@ -82,8 +117,17 @@ extern "C" regen_status regen_sr_create(const regen_sr_config* cfg, const float*
   REGEN_REQUIRE(cfg->n_resblocks >= 0 && cfg->n_resblocks <= 64, "bad n_resblocks");
   REGEN_REQUIRE(cfg->dtype == REGEN_DTYPE_BF16 || cfg->dtype == REGEN_DTYPE_FP32, "bad dtype");
   REGEN_REQUIRE(!(cfg->res_scale != cfg->res_scale), "res_scale is NaN");
+  REGEN_REQUIRE(cfg->bin_w >= 4 && cfg->bin_w <= 4096, "bad bin_w %d", cfg->bin_w);
   SRNet* net = new SRNet();
   net->cfg = *cfg;
+  {
+    auto flag = [](const char* name) { const char* e = getenv(name); return e != nullptr && e[0] == '1'; };
+    net->no_fold = flag("REGEN_NO_FOLD");
+    net->no_foldf = flag("REGEN_NO_FOLDF");
+    net->no_fused_rb = flag("REGEN_NO_FUSED_RESBLOCK");
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&net->n_sm, cudaDevAttrMultiProcessorCount, dev);
+  }
   build_convs(net);
   size_t need = 0;
   for (auto& d : net->convs) need += (size_t)d.cout * d.cin * 9 + d.cout;
@@ -121,9 +165,11 @@ extern "C" regen_status regen_sr_create(const regen_sr_config* cfg, const float*
   }
   if (cfg->dtype == REGEN_DTYPE_BF16) {
     regen_status st = conv_tc_prepare(net);
+    if (st == REGEN_OK && net->use_tc) st = conv_tc_plan_all(net, cfg->bin_w);
+    if (st == REGEN_OK && resblock_tc_supported(net, cfg->bin_w)) st = resblock_tc_prepare(net);
+    if (st == REGEN_OK) st = check_bf16_kernels(net);
     if (st != REGEN_OK) {
-      cudaFree(net->d_w32);
-      delete net;
+      regen_sr_destroy(net);
       return st;
     }
   }
@@ -380,7 +426,9 @@ regen_status conv_simt_launch(const SRNet* net, const ConvDesc& cv, const void* 
 
 // ------------------------------------------------------------------------------------ buffers
 
-EnhanceBufs enhance_bufs(const SRNet* net, const regen_pack_params& p, void* base) {
+// frames_out: the buffers of the frame-output calls (regen_enhance_scatter / _owned); with the fused
+// fold + combine the HR-resolution partial-sum buffer `u` is never touched and is not carved
+EnhanceBufs enhance_bufs(const SRNet* net, const regen_pack_params& p, void* base, bool frames_out) {
   Carver c(base);
   const size_t es = net->cfg.dtype == REGEN_DTYPE_BF16 ? 2 : 4;
   const int C8 = net->cfg.channels / 8, s = net->cfg.scale;
@@ -396,7 +444,8 @@ EnhanceBufs enhance_bufs(const SRNet* net, const regen_pack_params& p, void* bas
     e.a1 = c.take<uint8_t>(px * C8 * 8 * es);
     e.a2 = c.take<uint8_t>(px * C8 * 8 * es);
     e.u1 = s == 4 ? (void*)c.take<uint8_t>(px * 4 * C8 * 8 * es) : nullptr;
-    e.u = c.take<uint8_t>(px * s * s * C8 * 8 * es);
+    const bool fused_fold = frames_out && fold_enabled(net, p.bin_w) && fold_fused_supported(net, p.bin_w);
+    e.u = fused_fold ? nullptr : (void*)c.take<uint8_t>(px * s * s * C8 * 8 * es);
   } else {
     e.a1 = e.a2 = e.u1 = e.u = nullptr;
   }
@@ -406,10 +455,12 @@ EnhanceBufs enhance_bufs(const SRNet* net, const regen_pack_params& p, void* bas
 
 // `order` alternates along the conv chain: a conv hands out its units in the reverse order of the one
 // before it, so it starts on the bins its producer wrote last (still in L2).
+// BF16 handles run every conv on tcgen05 (regen_sr_create guarantees a plan for each executed conv);
+// FP32 handles (and BF16 under the explicit REGEN_FORCE_SIMT=1 debug switch) on the CUDA-core kernel
 static regen_status run_conv(const SRNet* net, const ConvDesc& cv, const void* in, void* out, const void* skip,
                              const EnhanceBufs& e, const regen_pack_params& p, const int32_t* d_num_bins,
                              cudaStream_t s, int order = 0) {
-  if (net->use_tc && conv_tc_supported(net, cv, p.bin_w))
+  if (net->use_tc)
     return conv_tc_launch(net, cv, in, out, skip, e.mbits, p.max_bins, d_num_bins, p.bin_w, p.bin_h,
                           e.counters + (&cv - net->convs.data()), s, order & 1);
   return conv_simt_launch(net, cv, in, out, skip, e.map, p.max_bins, d_num_bins, p.bin_w, p.bin_h, s);
@@ -418,16 +469,16 @@ static regen_status run_conv(const SRNet* net, const ConvDesc& cv, const void* i
 // the UP∘TAIL fold runs when the folded conv has a tcgen05 plan (REGEN_NO_FOLD=1 forces the literal
 // upsampler + tail, for A/B checks)
 static bool fold_enabled(const SRNet* net, int bin_w) {
-  if (net->fold_conv < 0 || !net->use_tc) return false;
-  const char* off = getenv("REGEN_NO_FOLD");
-  if (off && off[0] == '1') return false;
+  if (net->fold_conv < 0 || !net->use_tc || net->no_fold) return false;
   return conv_tc_supported(net, net->convs[net->fold_conv], bin_w);
 }
 
-static regen_status validate_pack(const regen_pack_params* p) {
+static regen_status validate_pack(const regen_pack_params* p, const SRNet* net = nullptr) {
   REGEN_REQUIRE(p != nullptr, "pack params null");
   REGEN_REQUIRE(p->bin_w >= 4 && p->bin_h >= 1 && p->bin_w <= 4096 && p->bin_h <= 4096 && p->max_bins >= 1,
                 "bad bin geometry");
+  REGEN_REQUIRE(net == nullptr || !net->use_tc || p->bin_w == net->cfg.bin_w,
+                "bin_w %d differs from the SR handle's planned bin_w %d", p->bin_w, net ? net->cfg.bin_w : 0);
   return REGEN_OK;
 }
 
@@ -597,7 +648,7 @@ static size_t hr_bins_bytes(const SRNet* net, const regen_pack_params& p) {
 
 // workspace of regen_enhance_scatter: the enhance buffers, plus the HR bins when the fold is off
 size_t enhance_scatter_ws_bytes(const SRNet* net, const regen_pack_params& p) {
-  const size_t e = (enhance_bufs(net, p, nullptr).bytes + 255) / 256 * 256;
+  const size_t e = (enhance_bufs(net, p, nullptr, true).bytes + 255) / 256 * 256;
   return fold_enabled(net, p.bin_w) ? e : e + hr_bins_bytes(net, p) + 256;
 }
 
@@ -615,6 +666,8 @@ extern "C" regen_status regen_enhance_packed(void* sr, const regen_geom* geom, c
   REGEN_REQUIRE(d_frames && d_boxes && d_num_boxes && d_num_bins && d_hr_bins && d_status, "null device pointer");
   REGEN_REQUIRE(max_boxes >= 1 && max_boxes < (1ll << 31), "bad max_boxes");
   const SRNet* net = (const SRNet*)sr;
+  st = validate_pack(p, net);
+  if (st != REGEN_OK) return st;
   EnhanceBufs e = enhance_bufs(net, *p, nullptr);
   REGEN_REQUIRE(d_ws && ws_bytes >= e.bytes, "workspace too small (%zu < %zu)", ws_bytes, e.bytes);
   e = enhance_bufs(net, *p, d_ws);
@@ -639,10 +692,12 @@ static regen_status enhance_scatter_parts(void* sr, const regen_geom* geom, cons
   REGEN_REQUIRE(max_boxes >= 1 && max_boxes < (1ll << 31), "bad max_boxes");
   REGEN_REQUIRE(out_dtype == REGEN_DTYPE_BF16 || out_dtype == REGEN_DTYPE_FP32, "bad out dtype");
   const SRNet* net = (const SRNet*)sr;
+  st = validate_pack(p, net);
+  if (st != REGEN_OK) return st;
   REGEN_REQUIRE(net->cfg.scale >= 2, "scale must be >= 2");
   const size_t need = enhance_scatter_ws_bytes(net, *p);
   REGEN_REQUIRE(d_ws && ws_bytes >= need, "workspace too small (%zu < %zu)", ws_bytes, need);
-  EnhanceBufs e = enhance_bufs(net, *p, d_ws);
+  EnhanceBufs e = enhance_bufs(net, *p, d_ws, true);
   if (fold_enabled(net, p->bin_w)) {
     FoldFrameArgs fa;
     fa.geom = *geom;

@@ -49,6 +49,10 @@ struct SRNet {
   int tc_bin_w = -1;             // bin width the B images were planned for
   void* rb_images = nullptr;     // fused-resblock B images (resblock_tc.cu)
   int fold_conv = -1;            // index of the ROLE_FOLD conv in convs (-1: none)
+  int n_sm = 148;                // SMs of the device the handle was created on (persistent grids)
+  // A/B switches, read from the environment once by regen_sr_create (REGEN_NO_FOLD, REGEN_NO_FOLDF,
+  // REGEN_NO_FUSED_RESBLOCK): measurement aids, every default is the fastest path
+  bool no_fold = false, no_foldf = false, no_fused_rb = false;
 };
 
 constexpr int N_COUNTERS = 256, RB_COUNTER0 = 160;   // convs <= 2*64 + 6, residual blocks <= 64
@@ -71,7 +75,7 @@ struct EnhanceBufs {
   size_t bytes;
 };
 
-EnhanceBufs enhance_bufs(const SRNet* net, const regen_pack_params& p, void* base);
+EnhanceBufs enhance_bufs(const SRNet* net, const regen_pack_params& p, void* base, bool frames_out = false);
 
 // conv launchers
 regen_status conv_simt_launch(const SRNet* net, const ConvDesc& cv, const void* in, void* out, const void* skip,
@@ -79,6 +83,8 @@ regen_status conv_simt_launch(const SRNet* net, const ConvDesc& cv, const void* 
                               cudaStream_t s);
 bool conv_tc_supported(const SRNet* net, const ConvDesc& cv, int bin_w);
 regen_status conv_tc_prepare(SRNet* net);
+regen_status conv_tc_plan_all(SRNet* net, int bin_w);
+regen_status resblock_tc_prepare(SRNet* net);
 void conv_tc_release(SRNet* net);
 bool resblock_tc_supported(const SRNet* net, int bin_w);
 void fold_prepare(SRNet* net, std::vector<float>& w32);

@@ -35,6 +35,7 @@ struct BoxArgs {
   int32_t* box_of_mb;        // [frames][GH][GW] (d_mb_owner, pre-filled with -1)
   int32_t* status;
   int GW, GH, W, H, F, mb, expand, P;
+  int density;   // REGEN_DENSITY_SPAN / REGEN_DENSITY_MEMBERS
 };
 
 __device__ __forceinline__ int piece_start(int n, int pieces, int i) {
@@ -80,8 +81,10 @@ __device__ int region_pieces(const BoxArgs& a, int64_t r, int64_t box_base) {
           if (lane == 0) {
             double sum = 0.0;
             const float* sc = a.imp + frame * a.GW * a.GH;
+            const bool members = a.density == REGEN_DENSITY_MEMBERS;
             for (int y = my0; y < my1; ++y)
-              for (int x = mx0; x < mx1; ++x) sum = __dadd_rn(sum, (double)sc[y * a.GW + x]);
+              for (int x = mx0; x < mx1; ++x)
+                if (!members || lab[y * a.GW + x] == (int32_t)r) sum = __dadd_rn(sum, (double)sc[y * a.GW + x]);
             regen_box bx;
             bx.stream = rg.stream;
             bx.frame = rg.frame;
@@ -91,7 +94,7 @@ __device__ int region_pieces(const BoxArgs& a, int64_t r, int64_t box_base) {
             bx.x0 = x0; bx.y0 = y0; bx.w = x1 - x0; bx.h = y1 - y0;
             bx.n_members = cnt;
             bx.region = (int32_t)r;
-            bx.density = __ddiv_rn(sum, (double)((mx1 - mx0) * (my1 - my0)));
+            bx.density = __ddiv_rn(sum, (double)(members ? cnt : (mx1 - mx0) * (my1 - my0)));
             bx.bin = -1; bx.bx = 0; bx.by = 0; bx.rotated = 0; bx.rank = 0; bx.reserved = 0;
             a.boxes[b] = bx;
           }
@@ -153,7 +156,8 @@ __global__ void scan_counts64_kernel(const int32_t* counts, const int64_t* n_ptr
 // ------------------------------------------------------------------------------------ sort
 
 __device__ __forceinline__ uint64_t box_key(const regen_box& b, int order) {
-  return order == REGEN_ORDER_AREA ? (uint64_t)((int64_t)b.w * b.h) : density_ord(b.density);
+  return order == REGEN_ORDER_AREA ? (uint64_t)((int64_t)b.w * b.h)
+         : order == REGEN_ORDER_HEIGHT ? (uint64_t)b.h : density_ord(b.density);
 }
 
 // n <= SORT_SMEM: one CTA bitonic-sorts (key, index) pairs in SMEM (the order is total: keys tie-broken by
@@ -243,6 +247,8 @@ struct PackArgs {
   int32_t* status;
   int bin_w, bin_h, max_bins, gutter;
   int prof;   // REGEN_PACK_PROF=1: print per-phase cycle counts
+  int pool_limit;   // live free-area capacity (PACK_POOL + 32; REGEN_PACK_POOL_LIMIT=n lowers it: a test
+                    // aid that makes REGEN_ST_FREELIST_OVERFLOW reachable on small inputs)
 };
 
 // One warp. The live free areas of the opened bins form a compact pool: key = bin << 32 | creation
@@ -410,6 +416,7 @@ __global__ void __launch_bounds__(32 * PACK_WARPS, 1) pack_kernel(PackArgs a) {
       else if (lane < PACK_WARPS) { ck = cand_key[lane]; cr = cand_rect[lane]; cs = cand_slot[lane]; }
       warp_first_fit(ck, cr, cs, wkey, wrect, wslot);
     }
+    __syncwarp();   // every lane's overflow-slot reads of this box's scan precede lane 0's writes below
     int fx, fy, fw, fh, bin, slot = -1;
     bool place = true;
     if (wkey != ~0ull) {
@@ -458,7 +465,7 @@ __global__ void __launch_bounds__(32 * PACK_WARPS, 1) pack_kernel(PackArgs a) {
         if (min(rw, rh) < mA || max(rw, rh) < mB) continue;   // unusable: never stored
         int dst;
         if (free_slot >= 0) { dst = free_slot; free_slot = -1; }
-        else if (hw < PACK_POOL + 32) dst = hw++;
+        else if (hw < a.pool_limit) dst = hw++;
         else { overflow = true; continue; }
         const uint64_t nk = ((uint64_t)bin << 32) | sq;
         const uint64_t nr = (uint64_t)(uint32_t)(rx | (ry << 16)) | ((uint64_t)(uint32_t)(rw | (rh << 16)) << 32);
@@ -551,7 +558,10 @@ extern "C" regen_status regen_pack_regions(const regen_geom* geom, const regen_p
   REGEN_REQUIRE(p->expand >= 0 && p->expand <= 64, "bad expand");
   REGEN_REQUIRE(p->partition_mb >= 1 && p->partition_mb <= 64, "bad partition_mb");
   REGEN_REQUIRE(p->gutter >= 0 && p->gutter <= 8, "bad gutter");
-  REGEN_REQUIRE(p->order == REGEN_ORDER_DENSITY || p->order == REGEN_ORDER_AREA, "bad order");
+  REGEN_REQUIRE(p->order == REGEN_ORDER_DENSITY || p->order == REGEN_ORDER_AREA || p->order == REGEN_ORDER_HEIGHT,
+                "bad order");
+  REGEN_REQUIRE(p->density == REGEN_DENSITY_SPAN || p->density == REGEN_DENSITY_MEMBERS, "bad density mode");
+  REGEN_REQUIRE(p->policy == REGEN_POLICY_GUILLOTINE, "policy %d not built", p->policy);
   REGEN_REQUIRE(d_importance && d_labels && d_num_regions && d_num_boxes && d_num_bins && d_mb_owner && d_status,
                 "null device pointer");
   REGEN_REQUIRE(max_boxes >= 1 && max_boxes < (1ll << 31) && d_boxes && d_order, "bad boxes buffer");
@@ -586,6 +596,7 @@ extern "C" regen_status regen_pack_regions(const regen_geom* geom, const regen_p
   a.mb = g.mb;
   a.expand = p->expand;
   a.P = p->partition_mb;
+  a.density = p->density;
   const int warps_per_block = 4;   // 128 threads x <= 56 registers: fits beside a resident SR conv CTA
   const unsigned nblk = (unsigned)std::min<int64_t>((max_regions + warps_per_block - 1) / warps_per_block, 148 * 4);
   {
@@ -633,6 +644,9 @@ extern "C" regen_status regen_pack_regions(const regen_geom* geom, const regen_p
   {
     const char* e = getenv("REGEN_PACK_PROF");
     k.prof = (e && e[0] == '1') ? 1 : 0;
+    const char* lim = getenv("REGEN_PACK_POOL_LIMIT");
+    k.pool_limit = PACK_POOL + 32;
+    if (lim && atoi(lim) > 0) k.pool_limit = std::min(atoi(lim), PACK_POOL + 32);
   }
   const size_t smem = (size_t)PACK_DIMS * 8 + (size_t)PACK_SOV * 16;   // dims + ords + SMEM overflow slots
   REGEN_CUDA(cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -438,8 +438,7 @@ static void rb_pack(const std::vector<float>& w32, const ConvDesc& d, int C, std
 }
 
 bool resblock_tc_supported(const SRNet* net, int bin_w) {
-  const char* e = getenv("REGEN_NO_FUSED_RESBLOCK");
-  if (e && e[0] == '1') return false;
+  if (net->no_fused_rb) return false;   // REGEN_NO_FUSED_RESBLOCK=1 at create (A/B aid)
   return net->use_tc && bin_w == 128 && (net->cfg.channels == 32 || net->cfg.channels == 16) &&
          net->cfg.n_resblocks > 0 && !net->tc_weights.empty();
 }
@@ -450,6 +449,7 @@ struct RbImages {
   uint8_t* d = nullptr;
 };
 
+// built once by regen_sr_create (resblock_tc_prepare); launches only read them
 static RbImages* rb_images(SRNet* net) {
   if (net->rb_images) return (RbImages*)net->rb_images;
   auto* im = new RbImages();
@@ -472,6 +472,11 @@ static RbImages* rb_images(SRNet* net) {
   return im;
 }
 
+regen_status resblock_tc_prepare(SRNet* net) {
+  REGEN_REQUIRE(rb_images(net) != nullptr, "fused resblock B images: upload failed");
+  return REGEN_OK;
+}
+
 void resblock_tc_release(SRNet* net) {
   if (!net->rb_images) return;
   auto* im = (RbImages*)net->rb_images;
@@ -484,9 +489,9 @@ regen_status resblock_tc_launch(const SRNet* cnet, int block, const void* in, vo
                                 int max_bins, const int32_t* d_num_bins, int bin_w, int bin_h, int* counter,
                                 cudaStream_t s, int reverse) {
   using namespace tc::rb;
-  SRNet* net = const_cast<SRNet*>(cnet);
-  RbImages* im = rb_images(net);
-  REGEN_REQUIRE(im != nullptr, "resblock B images");
+  const SRNet* net = cnet;
+  const RbImages* im = (const RbImages*)net->rb_images;
+  REGEN_REQUIRE(im != nullptr, "resblock B images not prepared");
   const int C = net->cfg.channels;
   Params p;
   memset(&p, 0, sizeof(p));
@@ -518,13 +523,7 @@ regen_status resblock_tc_launch(const SRNet* cnet, int block, const void* in, vo
   const size_t smem = 1024 + 2ull * NSLOT * G * (C / 8) * 128 * 16 + 2ull * p.b_bytes;
   REGEN_REQUIRE(smem <= 227 * 1024, "fused resblock SMEM %zu", smem);
   REGEN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  static int nsm = 0;
-  if (nsm == 0) {
-    int dev;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  }
-  const int grid = std::min(max_bins * p.nbands, nsm);
+  const int grid = std::min(max_bins * p.nbands, net->n_sm);
   static unsigned long long* d_prof = nullptr;
   const char* pe = getenv("REGEN_TC_PROF");
   const bool prof = pe && pe[0] == '1';

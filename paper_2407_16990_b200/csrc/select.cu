@@ -8,6 +8,8 @@
 //                 point to the smaller raster index, so every root is its component's minimum),
 //                 regions ranked by root in raster order, SMEM atomics for bbox/count.
 // region_write    globalises frame-local region ids with the scanned per-frame offsets.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace regen {
@@ -336,6 +338,7 @@ extern "C" regen_status regen_select_mbs(const regen_geom* geom, const regen_sel
   REGEN_REQUIRE(p->connectivity == 8 || p->connectivity == 4, "connectivity must be 4 or 8");
   REGEN_REQUIRE(p->mode == REGEN_MODE_THRESHOLD || p->k >= 0, "k must be >= 0 for TOPK");
   REGEN_REQUIRE(!(p->tau != p->tau), "tau is NaN");
+  REGEN_REQUIRE(p->cap >= -1, "cap must be -1 (none) or >= 0");
   REGEN_REQUIRE(d_importance && d_sel_bitmap && d_labels && d_num_regions && d_status, "null device pointer");
   REGEN_REQUIRE(max_regions >= 0 && (max_regions == 0 || d_regions), "bad regions buffer");
   const regen_geom g = *geom;
@@ -351,6 +354,7 @@ extern "C" regen_status regen_select_mbs(const regen_geom* geom, const regen_sel
   int64_t* foff;
   select_ws(g, d_ws, &stage, &fcount, &foff);
 
+  REGEN_CUDA(cudaMemsetAsync(d_status, 0, sizeof(int32_t), s));   // a batch starts with a clean status word
   REGEN_CUDA(cudaMemsetAsync(d_sel_bitmap, 0, sizeof(uint32_t) * (size_t)nf * GH * W32, s));
   SelArgs a;
   a.imp = d_importance;
@@ -361,7 +365,8 @@ extern "C" regen_status regen_select_mbs(const regen_geom* geom, const regen_sel
   a.W32 = W32;
   a.GH = GH;
   a.mode = p->mode;
-  a.k = p->k;
+  // the capacity cap N applies on top of k in both modes
+  a.k = p->cap < 0 ? p->k : ((p->mode == REGEN_MODE_THRESHOLD && p->k < 0) ? p->cap : std::min(p->k, p->cap));
   a.tau = p->tau;
   const int nseg = (int)(M / a.seg_len);
   {

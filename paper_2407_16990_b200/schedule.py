@@ -31,30 +31,42 @@ class PipelinedRunner:
         self.back_done = [torch.cuda.Event() for _ in range(2)]
         self.side_done = [torch.cuda.Event() for _ in range(2)]
 
+    @staticmethod
+    def _inputs(imp, frames):
+        """One (importance, frames) pair or lists of them (the selection groups of a rank): batch k of
+        a run uses pair k % len."""
+        if isinstance(imp, (list, tuple)):
+            assert len(imp) == len(frames) and len(imp) > 0
+            return list(zip(imp, frames))
+        return [(imp, frames)]
+
     def steps(self, imp, frames, n_steps: int, capturing: bool = False):
-        """Enqueue n_steps pipelined steps (each: one batch through select -> pack -> enhance+scatter)."""
-        for k in range(n_steps):
+        """Enqueue n_steps pipelined steps; a step is one batch of every input pair (each batch: select
+        -> pack -> enhance+scatter of one selection group)."""
+        ins = self._inputs(imp, frames)
+        for k in range(n_steps * len(ins)):
             q = self.pipes[k % 2]
+            imp_k, fr_k = ins[k % len(ins)]
             with torch.cuda.stream(self.s_front):
                 if not (capturing and k < 2):
                     self.s_front.wait_event(self.back_done[k % 2])   # buffers of batch k-2 are free
                     if self.bilinear == "side":
                         self.s_front.wait_event(self.side_done[k % 2])
-                q.select(imp, stream=self.s_front)
-                q.pack_step(imp, stream=self.s_front)
+                q.select(imp_k, stream=self.s_front)
+                q.pack_step(imp_k, stream=self.s_front)
                 self.front_done[k % 2].record(self.s_front)
                 if self.bilinear == "front":
-                    q.scatter_bilinear(frames, stream=self.s_front)
+                    q.scatter_bilinear(fr_k, stream=self.s_front)
             if self.bilinear == "side":
                 with torch.cuda.stream(self.s_side):
                     self.s_side.wait_event(self.front_done[k % 2])
-                    q.scatter_bilinear(frames, stream=self.s_side)
+                    q.scatter_bilinear(fr_k, stream=self.s_side)
                     self.side_done[k % 2].record(self.s_side)
             with torch.cuda.stream(self.s_back):
                 self.s_back.wait_event(self.front_done[k % 2])
-                q.enhance_owned(frames, stream=self.s_back)
+                q.enhance_owned(fr_k, stream=self.s_back)
                 if self.bilinear == "back":
-                    q.scatter_bilinear(frames, stream=self.s_back)
+                    q.scatter_bilinear(fr_k, stream=self.s_back)
                 self.back_done[k % 2].record(self.s_back)
 
     def run_eager(self, imp, frames, n_steps: int, stream=None):
@@ -80,30 +92,34 @@ class PipelinedRunner:
 
     def e2e(self, imp_pin, fr_pin, out_pin, n_steps: int, stream=None) -> float:
         """End-to-end pipelined throughput through the public calls: per step, H2D of the step's inputs
-        from pinned host memory (copy stream), the index path + bilinear pixels (index stream), the SR
-        pixels (SR stream), and D2H of the step's HR frames into pinned host memory (copy-out stream);
+        from pinned host memory (copy stream), the index path (index stream), the bilinear pixels (on
+        the stream `self.bilinear` names, as in steps()), the SR pixels (SR stream), and D2H of the step's HR frames into pinned host memory (copy-out stream);
         step k's copies overlap the compute of steps k-1 / k+1. Double-buffered device inputs and host
         outputs (out_pin: two pinned tensors shaped like Pipeline.out). Returns device ms per step."""
         dev = self.dev
         stream = stream or torch.cuda.current_stream(dev)
         s_h2d = torch.cuda.Stream(dev)
         s_d2h = torch.cuda.Stream(dev)
-        imp_d = [torch.empty(imp_pin.shape, dtype=imp_pin.dtype, device=dev) for _ in range(2)]
-        fr_d = [torch.empty(fr_pin.shape, dtype=fr_pin.dtype, device=dev) for _ in range(2)]
+        ins = self._inputs(imp_pin, fr_pin)   # pinned host inputs of every selection group of the rank
+        imp_d = [torch.empty(ins[0][0].shape, dtype=ins[0][0].dtype, device=dev) for _ in range(2)]
+        fr_d = [torch.empty(ins[0][1].shape, dtype=ins[0][1].dtype, device=dev) for _ in range(2)]
         h2d_done = [torch.cuda.Event() for _ in range(2)]
         bil_done = [torch.cuda.Event() for _ in range(2)]
         d2h_done = [torch.cuda.Event() for _ in range(2)]
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize(dev)
         t0.record(stream)
-        for st in (s_h2d, s_d2h, self.s_front, self.s_back):
+        for st in (s_h2d, s_d2h, self.s_front, self.s_back, self.s_side):
             st.wait_stream(stream)
-        for k in range(n_steps):
+        for k in range(n_steps * len(ins)):
             b = k % 2
             q = self.pipes[b]
+            imp_pin, fr_pin = ins[k % len(ins)]
             with torch.cuda.stream(s_h2d):
                 if k >= 2:
-                    s_h2d.wait_event(self.back_done[b])    # step k-2 no longer reads these inputs
+                    # step k-2 no longer reads these inputs: its SR (back) and its bilinear pass
+                    s_h2d.wait_event(self.back_done[b])
+                    s_h2d.wait_event(bil_done[b])
                 imp_d[b].copy_(imp_pin, non_blocking=True)
                 fr_d[b].copy_(fr_pin, non_blocking=True)
                 h2d_done[b].record(s_h2d)
@@ -114,18 +130,27 @@ class PipelinedRunner:
                 q.select(imp_d[b], stream=self.s_front)
                 q.pack_step(imp_d[b], stream=self.s_front)
                 self.front_done[b].record(self.s_front)
-                q.scatter_bilinear(fr_d[b], stream=self.s_front)
-                bil_done[b].record(self.s_front)
+                if self.bilinear == "front":
+                    q.scatter_bilinear(fr_d[b], stream=self.s_front)
+                    bil_done[b].record(self.s_front)
+            if self.bilinear == "side":
+                with torch.cuda.stream(self.s_side):
+                    self.s_side.wait_event(self.front_done[b])
+                    q.scatter_bilinear(fr_d[b], stream=self.s_side)
+                    bil_done[b].record(self.s_side)
             with torch.cuda.stream(self.s_back):
                 self.s_back.wait_event(self.front_done[b])
                 q.enhance_owned(fr_d[b], stream=self.s_back)
+                if self.bilinear == "back":
+                    q.scatter_bilinear(fr_d[b], stream=self.s_back)
+                    bil_done[b].record(self.s_back)
                 self.back_done[b].record(self.s_back)
             with torch.cuda.stream(s_d2h):
                 s_d2h.wait_event(self.back_done[b])
                 s_d2h.wait_event(bil_done[b])
                 out_pin[b].copy_(q.out, non_blocking=True)
                 d2h_done[b].record(s_d2h)
-        for st in (s_h2d, s_d2h, self.s_front, self.s_back):
+        for st in (s_h2d, s_d2h, self.s_front, self.s_back, self.s_side):
             stream.wait_stream(st)
         t1.record(stream)
         torch.cuda.synchronize(dev)

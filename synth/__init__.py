@@ -123,6 +123,7 @@ class Workload:
     partition_mb: int
     sr: SRConfig
     max_bins: int
+    groups: int = 0   # selection groups in the whole job (S streams each); 0 = one per rank (weak scaling)
 
     @property
     def GW(self) -> int:
@@ -142,19 +143,27 @@ class Workload:
         return (round(self.pct * 100) * self.n_mbs) // 10000
 
 
-# BASELINE.json configs (frame count F=30 where unstated: 1-s chunk).
+# BASELINE.json configs (frame count F=30 where unstated: 1-s chunk). A Workload is one
+# selection group (the scope of the cross-stream top-N); `groups` > 0 fixes the job's stream count
+# (groups x S streams, sharded over the ranks: strong scaling), 0 gives every rank one group (weak).
 CONFIGS = {
     "c1": Workload("c1_320x180_x2_tiny_fp32", 1, 8, 320, 180, 10.0, 64, 64, 3,
                    SRConfig(2, 16, 0, 1.0, bf16=False), 64),
     "c2": Workload("c2_360p_x3_edsr8x32_bf16", 1, 30, 640, 360, 20.0, 128, 128, 4,
                    SRConfig(3, 32, 8, 1.0, bf16=True), 512),
     "c3": Workload("c3_8x360p_x3_edsr8x32_bf16", 8, 30, 640, 360, 20.0, 128, 128, 4,
-                   SRConfig(3, 32, 8, 1.0, bf16=True), 4096),
+                   SRConfig(3, 32, 8, 1.0, bf16=True), 2048),
+    # C4: 64 streams = 8 selection groups of 8 streams (one paper edge server's load)
+    "c4": Workload("c4_64x360p_x3_top15_8groups", 8, 30, 640, 360, 15.0, 128, 128, 4,
+                   SRConfig(3, 32, 8, 1.0, bf16=True), 2048, groups=8),
     "c4g": Workload("c4_group8_360p_x3_top15", 8, 30, 640, 360, 15.0, 128, 128, 4,
-                    SRConfig(3, 32, 8, 1.0, bf16=True), 4096),
-    "c5": Workload("c5_720p_x2_edsr16x64_bf16", 2, 30, 1280, 720, 5.0, 128, 128, 4,
-                   SRConfig(2, 64, 16, 1.0, bf16=True), 4096),
+                    SRConfig(3, 32, 8, 1.0, bf16=True), 2048),
+    # C5: 16 streams of 720p in 8 selection groups of 2 streams (a 2-stream group at the 50% end of
+    # the ratio sweep already needs ~3k bins of C=64 activations); ratio set per run (5..50%)
+    "c5": Workload("c5_16x720p_x2_edsr16x64_bf16", 2, 30, 1280, 720, 5.0, 128, 128, 4,
+                   SRConfig(2, 64, 16, 1.0, bf16=True), 4096, groups=8),
 }
+C5_RATIOS = (5.0, 10.0, 15.0, 20.0, 25.0, 35.0, 50.0)
 
 
 def small(w: Workload, F: int | None = None, S: int | None = None) -> Workload:

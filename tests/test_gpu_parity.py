@@ -76,6 +76,10 @@ INDEX_CASES = [
     ("c2f4", "blobs", {"order": 1}),
     ("c3f2", "blobs", {}),
     ("c5f2", "noisy", {}),
+    ("c2f4", "levels", {"cap": 700}),                       # capacity N below k
+    ("c2f4", "blobs", {"mode": 1, "tau": 0.3, "k": -1, "cap": 450}),
+    ("c2f4", "noisy", {"density": 1}),                      # REGEN_DENSITY_MEMBERS
+    ("c2f4", "blobs", {"order": 2}),                        # REGEN_ORDER_HEIGHT
 ]
 
 
@@ -97,8 +101,9 @@ def test_index_path_bit_exact(name, kind, kw):
     okw = dict(kw)
     conv = okw.pop("connectivity", 8)
     order = okw.pop("order", 0)
+    dens = okw.pop("density", 0)
     _, g = _run_index(wl, imp, w, **kw)
-    o = _oracle_index(wl, imp, conn=conv, order_policy=order, **okw)
+    o = _oracle_index(wl, imp, conn=conv, order_policy=order, density_mode=dens, **okw)
     _assert_index_equal(g, o)
 
 
@@ -212,9 +217,20 @@ def test_pixels_c2_bf16_small():
     _check_pixels(synth.small(synth.CONFIGS["c2"], F=2), box_sample=lambda n: range(0, n, max(1, n // 12)))
 
 
-def test_pixels_tiny_bf16_x3_full_frames():
-    wl = dataclasses.replace(synth.small(synth.CONFIGS["c2"], F=2), sr=synth.SRConfig(3, 16, 0, 1.0, True))
+def test_pixels_tiny_fp32_x3_full_frames():
+    wl = dataclasses.replace(synth.small(synth.CONFIGS["c2"], F=2), sr=synth.SRConfig(3, 16, 0, 1.0, False))
     _check_pixels(wl)
+
+
+@pytest.mark.parametrize("sr,bin_w", [(synth.SRConfig(3, 16, 0, 1.0, True), 128),   # tiny model: no tcgen05 tail
+                                      (synth.SRConfig(3, 8, 1, 1.0, True), 128),    # C % 16 != 0
+                                      (synth.SRConfig(3, 32, 1, 1.0, True), 96)])   # bin_w % 128 != 0
+def test_bf16_configs_without_tensor_core_kernels_fail_loudly(sr, bin_w):
+    """No silent dispatch: a BF16 model with a conv the tcgen05 kernels do not tile is rejected by
+    regen_sr_create with REGEN_E_UNSUPPORTED instead of running on the CUDA-core kernel."""
+    rg = _rg()
+    with pytest.raises(rg.RegenError, match="unsupported"):
+        rg.SRNet(sr.scale, sr.channels, sr.n_resblocks, synth.sr_weights(sr, 0), True, 1.0, bin_w)
 
 
 def test_pixels_small_edsr_bf16_full_frames():
@@ -236,11 +252,41 @@ def test_pixels_bf16_tensor_core_shapes(s, C, nres):
     _check_pixels(wl, kind="noisy", box_sample=lambda n: range(0, n, max(1, n // 6)))
 
 
-def test_sr_tensor_core_matches_simt_path():
-    """Same packed batch through the tcgen05 kernels and through the SIMT kernels (separate process
-    with REGEN_FORCE_SIMT=1 is not needed: compare both against the oracle on a shared box set)."""
+def _kernels_of(fn):
+    rg = _rg()
+    rg.trace_read()
+    rg.trace_enable(True)
+    try:
+        fn()
+        torch.cuda.synchronize()
+    finally:
+        rg.trace_enable(False)
+    return {name for name, _ in rg.trace_read()}
+
+
+def test_sr_tensor_core_matches_simt_path(monkeypatch):
+    """The same batch through the tcgen05 kernels and, in a handle created under the explicit
+    REGEN_FORCE_SIMT=1 switch, through the CUDA-core kernel: the launched kernels prove which path
+    ran, both stay within the bf16 tolerance of the oracle and of each other."""
     wl = synth.small(synth.CONFIGS["c2"], F=2)
-    _check_pixels(wl, seed=9, box_sample=lambda n: range(1, n, max(1, n // 5)))
+    sample = lambda n: range(1, n, max(1, n // 5))  # noqa: E731
+    imp = synth.importance_maps(wl.S, wl.F, wl.GH, wl.GW, 9)
+    fr = torch.from_numpy(synth.frames_rgb8(wl.S, wl.F, wl.H, wl.W, 9)).cuda()
+    w = synth.sr_weights(wl.sr, 9)
+    outs = {}
+    for mode in ("tc", "simt"):
+        if mode == "simt":
+            monkeypatch.setenv("REGEN_FORCE_SIMT", "1")
+        p = _pipeline(wl, w)
+        d_imp = torch.from_numpy(imp).cuda()
+        names = _kernels_of(lambda: p.run(d_imp, fr))
+        if mode == "tc":
+            assert "resblock" in names and "conv_fold_frames" in names and "conv_simt" not in names, names
+        else:
+            assert "conv_simt" in names and not any(n.startswith(("resblock", "conv_fold", "conv_head")) for n in names), names
+        outs[mode] = p.out.float().clone()
+        assert _check_pixels(wl, seed=9, box_sample=sample) <= TOL[True]
+    assert float((outs["tc"] - outs["simt"]).abs().max()) <= TOL[True]
 
 
 @pytest.mark.parametrize("s,C", [(3, 32), (2, 32), (4, 16), (3, 64)])

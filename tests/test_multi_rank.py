@@ -98,3 +98,29 @@ def test_group_maps_are_slices_of_the_global_workload():
     for s0, s1 in shard.group_bounds(N_STREAMS, GROUP):
         np.testing.assert_array_equal(synth.importance_maps(s1 - s0, F, GH, GW, 3, "blobs", s0=s0), full[s0:s1])
         np.testing.assert_array_equal(synth.frames_rgb8(s1 - s0, F, 8, 8, 3, s0=s0), frames[s0:s1])
+
+
+def _bench_dry_run(*args):
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--dry-run", *args], capture_output=True,
+                         text=True, timeout=300, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    return json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+
+
+def test_bench_launcher_spawns_its_own_ranks():
+    """`bench.py --gpus 2` without a torchrun environment re-launches itself as 2 ranks (gloo in the
+    dry run): C4's 8 selection groups split 4/4 (strong scaling), C2 gives each rank one group (weak),
+    and the MAX/SUM reductions see both ranks."""
+    d = _bench_dry_run("--gpus", "2", "--config", "c4")
+    assert d["n_gpus"] == 2 and d["rank0_groups"] == [[0, 8], [8, 16], [16, 24], [24, 32]]
+    assert d["max_ms"] == 2.0 and d["frames"] == 64 * 30
+    d = _bench_dry_run("--gpus", "2")
+    assert d["n_gpus"] == 2 and d["rank0_groups"] == [[0, 1]] and d["frames"] == 2 * 30
+    d = _bench_dry_run("--config", "c5")
+    assert d["n_gpus"] == 1 and len(d["rank0_groups"]) == 8 and d["frames"] == 16 * 30

@@ -78,6 +78,25 @@ def test_select_threshold(cap):
     assert np.array_equal(sel, ref)
 
 
+@pytest.mark.parametrize("k,cap", [(100, 40), (40, 100), (0, 5), (300, 0)])
+def test_select_capacity_cap_topk(k, cap):
+    # the capacity N bounds the selection on top of the configured k
+    imp = _maps("levels")
+    sel = oracle.select(imp, 320, 180, oracle.MODE_TOPK, k, cap=cap)
+    assert np.array_equal(sel, _brute_topk(imp, min(k, cap)))
+
+
+def test_select_capacity_cap_threshold_and_scope():
+    imp = _maps("blobs")
+    sel = oracle.select(imp, 320, 180, oracle.MODE_THRESHOLD, -1, tau=0.3, cap=25)
+    masked = np.where(imp >= 0.3, imp, -np.inf)
+    assert np.array_equal(sel, _brute_topk(masked, 25))
+    sel = oracle.select(imp, 320, 180, oracle.MODE_TOPK, 30, scope=oracle.SCOPE_PER_FRAME, cap=7)
+    for s in range(imp.shape[0]):
+        for f in range(imp.shape[1]):
+            assert np.array_equal(sel[s, f], _brute_topk(imp[s:s + 1, f:f + 1], 7)[0, 0])
+
+
 @pytest.mark.parametrize("scope", [oracle.SCOPE_PER_STREAM, oracle.SCOPE_PER_FRAME])
 def test_select_scopes(scope):
     imp = _maps("levels")
@@ -209,6 +228,24 @@ def test_boxes_partition_members_exactly_once(kind, P):
         assert math.isclose(dens[b], math.fsum(span.reshape(-1)) / span.size, rel_tol=1e-14)
 
 
+def test_density_members_mode_is_mean_over_members():
+    # P:691's set notation read as the member MBs of the box (REGEN_DENSITY_MEMBERS)
+    imp = _maps("noisy", S=1, F=2, GH=23, GW=40)
+    sel = oracle.select(imp, 640, 360, 0, int(0.3 * imp.size))
+    labels, regs = oracle.regions(sel, 640, 360, 8)
+    bx, dens, own = oracle.boxes(imp, labels, regs, 640, 360, 3, 3, density_mode=oracle.DENSITY_MEMBERS)
+    bx0, dens0, own0 = oracle.boxes(imp, labels, regs, 640, 360, 3, 3)
+    assert np.array_equal(bx, bx0) and np.array_equal(own, own0)
+    differs = 0
+    for b, rec in enumerate(bx):
+        s, f = rec[0], rec[1]
+        vals = imp[s, f][own[s, f] == b].astype(np.float64)
+        assert len(vals) == rec[10]
+        assert math.isclose(dens[b], math.fsum(vals) / len(vals), rel_tol=1e-14)
+        differs += dens[b] != dens0[b]
+    assert differs > 0     # boxes that bound unselected MBs get a different density
+
+
 def test_region_ids_and_box_order_are_creation_order():
     imp = _maps("blobs", S=2, F=2, GH=23, GW=40)
     sel = oracle.select(imp, 640, 360, 0, int(0.2 * imp.size))
@@ -231,6 +268,8 @@ def test_sort_density_then_index_and_area_policy():
     assert order.tolist() == sorted(range(n), key=lambda i: (-dens[i], i))
     order = oracle.sort(bx, dens, oracle.ORDER_AREA)
     assert order.tolist() == sorted(range(n), key=lambda i: (-int(bx[i, 8]) * int(bx[i, 9]), i))
+    order = oracle.sort(bx, dens, oracle.ORDER_HEIGHT)
+    assert order.tolist() == sorted(range(n), key=lambda i: (-int(bx[i, 9]), i))
 
 
 # ------------------------------------------------------------------------------------ pack
