@@ -66,7 +66,8 @@ enum { REGEN_CALL_SELECT = 0, REGEN_CALL_PACK = 1, REGEN_CALL_ENHANCE = 2, REGEN
 enum {
   REGEN_ST_REGION_OVERFLOW = 1,   /* num_regions > max_regions */
   REGEN_ST_BOX_OVERFLOW = 2,      /* num_boxes > max_boxes */
-  REGEN_ST_FREELIST_OVERFLOW = 4  /* packer free-area pool full: remaining boxes left unplaced */
+  REGEN_ST_FREELIST_OVERFLOW = 4, /* packer free-area pool full: remaining boxes left unplaced */
+  REGEN_ST_TOPK_INCOMPLETE = 8    /* regen_select_mbs_global before the 4 digit rounds: nothing selected */
 };
 
 /* Frame geometry. MB grid GW = ceil(frame_w/mb), GH = ceil(frame_h/mb) (D1); mb = 16. */
@@ -251,6 +252,42 @@ REGEN_API regen_status regen_enhance_owned(void* sr, const regen_geom* geom, con
                                  int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream);
 REGEN_API regen_status regen_scatter_bilinear(const regen_geom* geom, int32_t scale, const uint8_t* d_frames,
                                     const int32_t* d_mb_owner, void* d_out, int32_t out_dtype, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * exact cross-rank global top-N. The paper's queue "aggregates and sorts MBs from all
+ * streams" (§3.3.1); when the streams are sharded over ranks (one process per GPU),
+ * the top-N must be taken over every rank's MBs. Reading D2 with a GLOBAL MB id: key = ord(score)
+ * << 32 | (0xFFFFFFFF - gid), gid = ((stream0 + s) * F + f) * GH * GW + y * GW + x (stream0 = the
+ * global index of this call's first stream; ids must fit 32 bits); the N largest keys are selected,
+ * i.e. every key >= the N-th largest. Protocol, identical on every rank (D17):
+ *   regen_topk_init(N, state)                                  N = the job-wide k
+ *   for round in 0..3:
+ *     zero hist; regen_topk_histogram(geom_i, stream0_i, imp_i, state, hist) for each of the rank's
+ *       calls (it ADDS the 16-bit digit `round` of the keys matching the prefix into hist[65536]);
+ *     all-reduce(hist, SUM) over the ranks (the caller's collective, e.g. NCCL over NVLink);
+ *     regen_topk_pick(hist, state)                             same sums -> same digit everywhere
+ *   regen_select_mbs_global(geom_i, params, stream0_i, imp_i, state, ...) for each call: the bitmap
+ *     of the MBs with key >= the N-th key, then regions exactly as regen_select_mbs (a2).
+ * d_state: 24-byte device struct; d_hist: 65536 uint32 counts. N >= total MBs selects every MB, N =
+ * 0 none. params: only `connectivity` is used. Errors as regen_select_mbs; selecting before the 4
+ * rounds sets REGEN_ST_TOPK_INCOMPLETE. All calls stream-ordered, graph-capturable.
+ * ------------------------------------------------------------------------------------------- */
+enum { REGEN_TOPK_SEARCH = 0, REGEN_TOPK_ALL = 1, REGEN_TOPK_NONE = 2 };
+typedef struct {
+  uint64_t prefix;   /* digits found so far (after round 4: the N-th largest key) */
+  int64_t k_rem;     /* rank of the N-th key among the keys matching the prefix */
+  int32_t round;     /* digits found, 0..4 */
+  int32_t flag;      /* REGEN_TOPK_SEARCH / ALL (N >= every MB) / NONE (N == 0) */
+} regen_topk_state;
+REGEN_API regen_status regen_topk_init(int64_t k, regen_topk_state* d_state, void* stream);
+REGEN_API regen_status regen_topk_histogram(const regen_geom* geom, int64_t stream0, const float* d_importance,
+                                  const regen_topk_state* d_state, uint32_t* d_hist, void* stream);
+REGEN_API regen_status regen_topk_pick(const uint32_t* d_hist, regen_topk_state* d_state, void* stream);
+REGEN_API regen_status regen_select_mbs_global(const regen_geom* geom, const regen_select_params* params,
+                                     int64_t stream0, const float* d_importance,
+                                     const regen_topk_state* d_state, uint32_t* d_sel_bitmap, int32_t* d_labels,
+                                     regen_region* d_regions, int64_t max_regions, int64_t* d_num_regions,
+                                     int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream);
 
 /* Workspace bytes for a call (which = REGEN_CALL_*; params = the call's params struct;
  * sr = SR handle for ENHANCE, else NULL). */

@@ -24,13 +24,15 @@ POLICY_GUILLOTINE, POLICY_MAXRECT, POLICY_SKYLINE, POLICY_SHELF = 0, 1, 2, 3
 DENSITY_SPAN, DENSITY_MEMBERS = 0, 1
 DTYPE_BF16, DTYPE_FP32 = 0, 1
 CALL_SELECT, CALL_PACK, CALL_ENHANCE, CALL_SCATTER, CALL_ENHANCE_SCATTER = 0, 1, 2, 3, 4
-ST_REGION_OVERFLOW, ST_BOX_OVERFLOW, ST_FREELIST_OVERFLOW = 1, 2, 4
+ST_REGION_OVERFLOW, ST_BOX_OVERFLOW, ST_FREELIST_OVERFLOW, ST_TOPK_INCOMPLETE = 1, 2, 4, 8
+TOPK_STATE_BYTES, TOPK_DIGITS = 24, 1 << 16
 
 EXPORTED = ["regen_select_mbs", "regen_pack_regions", "regen_sr_create", "regen_sr_destroy", "regen_stitch_bins",
             "regen_enhance_packed", "regen_scatter_blend", "regen_workspace_size", "regen_capacity_mbs",
             "regen_status_string", "regen_last_error", "regen_abi_version", "regen_enhance_kernel_count",
             "regen_enhance_scatter", "regen_trace_enable", "regen_trace_read", "regen_trace_filter",
-            "regen_enhance_owned", "regen_scatter_bilinear"]
+            "regen_enhance_owned", "regen_scatter_bilinear", "regen_topk_init", "regen_topk_histogram",
+            "regen_topk_pick", "regen_select_mbs_global"]
 
 
 class Geom(ctypes.Structure):
@@ -87,6 +89,10 @@ def _load():
     lib.regen_enhance_owned.argtypes = list(lib.regen_enhance_scatter.argtypes)
     lib.regen_scatter_bilinear.argtypes = [P(Geom), i32, vp, vp, vp, i32, vp]
     lib.regen_workspace_size.argtypes = [i32, P(Geom), vp, vp, P(sz)]
+    lib.regen_topk_init.argtypes = [i64, vp, vp]
+    lib.regen_topk_histogram.argtypes = [P(Geom), i64, vp, vp, vp, vp]
+    lib.regen_topk_pick.argtypes = [vp, vp, vp]
+    lib.regen_select_mbs_global.argtypes = [P(Geom), P(SelectParams), i64, vp, vp, vp, vp, vp, i64, vp, vp, vp, sz, vp]
     lib.regen_enhance_kernel_count.argtypes = [vp, P(PackParams), P(i32)]
     lib.regen_trace_enable.argtypes = [i32]
     lib.regen_trace_read.argtypes = [vp, vp, i32, P(i32)]
@@ -99,7 +105,8 @@ def _load():
     for name in ["regen_select_mbs", "regen_pack_regions", "regen_sr_create", "regen_sr_destroy",
                  "regen_stitch_bins", "regen_enhance_packed", "regen_scatter_blend", "regen_workspace_size",
                  "regen_enhance_kernel_count", "regen_enhance_scatter", "regen_trace_enable", "regen_trace_read", "regen_trace_filter",
-                 "regen_enhance_owned", "regen_scatter_bilinear"]:
+                 "regen_enhance_owned", "regen_scatter_bilinear", "regen_topk_init", "regen_topk_histogram",
+            "regen_topk_pick", "regen_select_mbs_global"]:
         getattr(lib, name).restype = ctypes.c_int
     return lib
 
@@ -175,6 +182,27 @@ def pack_regions(geom, params, importance, labels, regions, num_regions, boxes, 
                                   _ptr(regions), _ptr(num_regions), _ptr(boxes), max_boxes, _ptr(num_boxes),
                                   _ptr(order), _ptr(num_bins), _ptr(mb_owner), _ptr(status), _ptr(ws),
                                   ws.numel() * ws.element_size(), _stream(stream)), "regen_pack_regions")
+
+
+def topk_init(k, state, stream=None):
+    _check(lib.regen_topk_init(k, _ptr(state), _stream(stream)), "regen_topk_init")
+
+
+def topk_histogram(geom, stream0, importance, state, hist, stream=None):
+    _check(lib.regen_topk_histogram(ctypes.byref(geom), stream0, _ptr(importance), _ptr(state), _ptr(hist),
+                                    _stream(stream)), "regen_topk_histogram")
+
+
+def topk_pick(hist, state, stream=None):
+    _check(lib.regen_topk_pick(_ptr(hist), _ptr(state), _stream(stream)), "regen_topk_pick")
+
+
+def select_mbs_global(geom, params, stream0, importance, state, sel_bitmap, labels, regions, max_regions, num_regions,
+                      status, ws, stream=None):
+    _check(lib.regen_select_mbs_global(ctypes.byref(geom), ctypes.byref(params), stream0, _ptr(importance), _ptr(state),
+                                       _ptr(sel_bitmap), _ptr(labels), _ptr(regions), max_regions, _ptr(num_regions),
+                                       _ptr(status), _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)),
+           "regen_select_mbs_global")
 
 
 def stitch_bins(geom, params, dtype, frames, boxes, max_boxes, num_boxes, num_bins, lr_bins, ws, stream=None):
@@ -300,6 +328,11 @@ class Pipeline:
         # regen_select_mbs resets the status word on `stream` (the first call of a batch)
         select_mbs(self.geom, self.sel, importance, self.bitmap, self.labels, self.regions, self.max_regions,
                    self.counts[0:1], self.status, self.ws, stream)
+
+    def select_global(self, importance, state, stream0, stream=None):
+        """a1+a2 with the selection of a finished cross-rank top-N (regen_select_mbs_global; global_topk.py)."""
+        select_mbs_global(self.geom, self.sel, stream0, importance, state, self.bitmap, self.labels, self.regions,
+                          self.max_regions, self.counts[0:1], self.status, self.ws, stream)
 
     def pack_step(self, importance, stream=None):
         pack_regions(self.geom, self.pack, importance, self.labels, self.regions, self.counts[0:1], self.boxes,

@@ -322,59 +322,17 @@ static size_t select_ws(const regen_geom& g, void* base, int32_t** stage, int32_
 
 size_t select_workspace_bytes(const regen_geom& g) { return select_ws(g, nullptr, nullptr, nullptr, nullptr); }
 
-}  // namespace regen
-
-using namespace regen;
-
-extern "C" regen_status regen_select_mbs(const regen_geom* geom, const regen_select_params* p,
-                                         const float* d_importance, uint32_t* d_sel_bitmap, int32_t* d_labels,
-                                         regen_region* d_regions, int64_t max_regions, int64_t* d_num_regions,
-                                         int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream) {
-  regen_status st = validate_geom(geom);
-  if (st != REGEN_OK) return st;
-  REGEN_REQUIRE(p != nullptr, "params is null");
-  REGEN_REQUIRE(p->mode == REGEN_MODE_TOPK || p->mode == REGEN_MODE_THRESHOLD, "bad mode %d", p->mode);
-  REGEN_REQUIRE(p->scope >= 0 && p->scope <= 2, "bad scope %d", p->scope);
-  REGEN_REQUIRE(p->connectivity == 8 || p->connectivity == 4, "connectivity must be 4 or 8");
-  REGEN_REQUIRE(p->mode == REGEN_MODE_THRESHOLD || p->k >= 0, "k must be >= 0 for TOPK");
-  REGEN_REQUIRE(!(p->tau != p->tau), "tau is NaN");
-  REGEN_REQUIRE(p->cap >= -1, "cap must be -1 (none) or >= 0");
-  REGEN_REQUIRE(d_importance && d_sel_bitmap && d_labels && d_num_regions && d_status, "null device pointer");
-  REGEN_REQUIRE(max_regions >= 0 && (max_regions == 0 || d_regions), "bad regions buffer");
-  const regen_geom g = *geom;
-  REGEN_REQUIRE(ws_bytes >= select_workspace_bytes(g) && d_ws, "workspace too small (%zu < %zu)", ws_bytes,
-                select_workspace_bytes(g));
-  cudaStream_t s = (cudaStream_t)stream;
+// a2: regions of the selected-MB bitmap (CCL per frame, region table in (s, f, min raster) order);
+// shared by regen_select_mbs and regen_select_mbs_global
+regen_status launch_regions(const regen_geom& g, int connectivity, const uint32_t* d_sel_bitmap, int32_t* d_labels,
+                            regen_region* d_regions, int64_t max_regions, int64_t* d_num_regions, int32_t* d_status,
+                            void* d_ws, cudaStream_t s) {
   const int GW = grid_w(g), GH = grid_h(g), W32 = words_per_row(g);
   const int pf = GW * GH;
   const int64_t nf = n_frames(g);
-  const int64_t M = nf * pf;
-  REGEN_REQUIRE(M < (1ll << 31), "too many MBs in one call");
   int32_t *stage, *fcount;
   int64_t* foff;
   select_ws(g, d_ws, &stage, &fcount, &foff);
-
-  REGEN_CUDA(cudaMemsetAsync(d_status, 0, sizeof(int32_t), s));   // a batch starts with a clean status word
-  REGEN_CUDA(cudaMemsetAsync(d_sel_bitmap, 0, sizeof(uint32_t) * (size_t)nf * GH * W32, s));
-  SelArgs a;
-  a.imp = d_importance;
-  a.bitmap = d_sel_bitmap;
-  a.seg_len = p->scope == REGEN_SCOPE_GLOBAL ? M : (p->scope == REGEN_SCOPE_PER_STREAM ? (int64_t)g.F * pf : pf);
-  a.per_frame = pf;
-  a.GW = GW;
-  a.W32 = W32;
-  a.GH = GH;
-  a.mode = p->mode;
-  // the capacity cap N (P:663) applies on top of k in both modes
-  a.k = p->cap < 0 ? p->k : ((p->mode == REGEN_MODE_THRESHOLD && p->k < 0) ? p->cap : std::min(p->k, p->cap));
-  a.tau = p->tau;
-  const int nseg = (int)(M / a.seg_len);
-  {
-    REGEN_TRACE("select", s);
-    select_kernel<<<nseg, 1024, 0, s>>>(a);
-  }
-  REGEN_LAUNCH_CHECK();
-
   CclArgs c;
   c.bitmap = d_sel_bitmap;
   c.labels = d_labels;
@@ -384,7 +342,7 @@ extern "C" regen_status regen_select_mbs(const regen_geom* geom, const regen_sel
   c.GH = GH;
   c.W32 = W32;
   c.per_frame = pf;
-  c.conn = p->connectivity;
+  c.conn = connectivity;
   const size_t smem = sizeof(int) * 7 * (size_t)pf;
   REGEN_REQUIRE(smem <= 227 * 1024, "frame MB grid too large for the CCL kernel (%d MBs)", pf);
   REGEN_CUDA(cudaFuncSetAttribute(ccl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -414,4 +372,57 @@ extern "C" regen_status regen_select_mbs(const regen_geom* geom, const regen_sel
   }
   REGEN_LAUNCH_CHECK();
   return REGEN_OK;
+}
+
+}  // namespace regen
+
+using namespace regen;
+
+extern "C" regen_status regen_select_mbs(const regen_geom* geom, const regen_select_params* p,
+                                         const float* d_importance, uint32_t* d_sel_bitmap, int32_t* d_labels,
+                                         regen_region* d_regions, int64_t max_regions, int64_t* d_num_regions,
+                                         int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream) {
+  regen_status st = validate_geom(geom);
+  if (st != REGEN_OK) return st;
+  REGEN_REQUIRE(p != nullptr, "params is null");
+  REGEN_REQUIRE(p->mode == REGEN_MODE_TOPK || p->mode == REGEN_MODE_THRESHOLD, "bad mode %d", p->mode);
+  REGEN_REQUIRE(p->scope >= 0 && p->scope <= 2, "bad scope %d", p->scope);
+  REGEN_REQUIRE(p->connectivity == 8 || p->connectivity == 4, "connectivity must be 4 or 8");
+  REGEN_REQUIRE(p->mode == REGEN_MODE_THRESHOLD || p->k >= 0, "k must be >= 0 for TOPK");
+  REGEN_REQUIRE(!(p->tau != p->tau), "tau is NaN");
+  REGEN_REQUIRE(p->cap >= -1, "cap must be -1 (none) or >= 0");
+  REGEN_REQUIRE(d_importance && d_sel_bitmap && d_labels && d_num_regions && d_status, "null device pointer");
+  REGEN_REQUIRE(max_regions >= 0 && (max_regions == 0 || d_regions), "bad regions buffer");
+  const regen_geom g = *geom;
+  REGEN_REQUIRE(ws_bytes >= select_workspace_bytes(g) && d_ws, "workspace too small (%zu < %zu)", ws_bytes,
+                select_workspace_bytes(g));
+  cudaStream_t s = (cudaStream_t)stream;
+  const int GW = grid_w(g), GH = grid_h(g), W32 = words_per_row(g);
+  const int pf = GW * GH;
+  const int64_t nf = n_frames(g);
+  const int64_t M = nf * pf;
+  REGEN_REQUIRE(M < (1ll << 31), "too many MBs in one call");
+  REGEN_CUDA(cudaMemsetAsync(d_status, 0, sizeof(int32_t), s));   // a batch starts with a clean status word
+  REGEN_CUDA(cudaMemsetAsync(d_sel_bitmap, 0, sizeof(uint32_t) * (size_t)nf * GH * W32, s));
+  SelArgs a;
+  a.imp = d_importance;
+  a.bitmap = d_sel_bitmap;
+  a.seg_len = p->scope == REGEN_SCOPE_GLOBAL ? M : (p->scope == REGEN_SCOPE_PER_STREAM ? (int64_t)g.F * pf : pf);
+  a.per_frame = pf;
+  a.GW = GW;
+  a.W32 = W32;
+  a.GH = GH;
+  a.mode = p->mode;
+  // the capacity cap N (P:663) applies on top of k in both modes
+  a.k = p->cap < 0 ? p->k : ((p->mode == REGEN_MODE_THRESHOLD && p->k < 0) ? p->cap : std::min(p->k, p->cap));
+  a.tau = p->tau;
+  const int nseg = (int)(M / a.seg_len);
+  {
+    REGEN_TRACE("select", s);
+    select_kernel<<<nseg, 1024, 0, s>>>(a);
+  }
+  REGEN_LAUNCH_CHECK();
+
+  return launch_regions(g, p->connectivity, d_sel_bitmap, d_labels, d_regions, max_regions, d_num_regions, d_status,
+                        d_ws, s);
 }

@@ -124,3 +124,76 @@ def test_bench_launcher_spawns_its_own_ranks():
     assert d["n_gpus"] == 2 and d["rank0_groups"] == [[0, 1]] and d["frames"] == 2 * 30
     d = _bench_dry_run("--config", "c5")
     assert d["n_gpus"] == 1 and len(d["rank0_groups"]) == 8 and d["frames"] == 16 * 30
+
+
+# ------------------------------------------------------------------ exact cross-rank global top-N
+
+def _keys(imp: np.ndarray, stream0: int) -> np.ndarray:
+    """Reading D2/D17 keys with global ids: ord(score) << 32 | (0xFFFFFFFF - gid), written out in numpy
+    (the protocol's CPU stand-in for the libregen histogram kernel)."""
+    b = imp.astype(np.float32).reshape(-1).copy()
+    b[b == 0] = 0.0                                     # -0 == +0
+    u = b.view(np.uint32).astype(np.uint64)
+    ordv = np.where(u & 0x80000000, (~u) & 0xFFFFFFFF, u | 0x80000000)
+    ordv = np.where(np.isnan(b), 0, ordv).astype(np.uint64)
+    gid = np.arange(b.size, dtype=np.uint64) + np.uint64(stream0 * imp[0].size)
+    return (ordv << np.uint64(32)) | (np.uint64(0xFFFFFFFF) - gid)
+
+
+def _topk_worker(rank, world, port, q, k_total):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+    try:
+        GW, GH = synth.grid(W, H)
+        s0, s1 = shard.rank_slice(N_STREAMS, world, rank)
+        imp = synth.importance_maps(s1 - s0, F, GH, GW, 7, "levels", s0=s0)
+        keys = _keys(imp, s0)
+        prefix, k_rem, flag = 0, k_total, "search" if k_total > 0 else "none"
+        for rnd in range(4):
+            sh, hs = 48 - 16 * rnd, 64 - 16 * rnd
+            m = keys if hs == 64 else keys[(keys >> np.uint64(hs)) == np.uint64(prefix >> hs)]
+            hist = torch.from_numpy(np.bincount(((m >> np.uint64(sh)) & np.uint64(0xFFFF)).astype(np.int64),
+                                                minlength=1 << 16).astype(np.int32))
+            dist.all_reduce(hist, op=dist.ReduceOp.SUM)        # the one exchange of the round
+            h = hist.numpy().astype(np.int64)
+            if flag == "search" and rnd == 0 and k_rem >= h.sum():
+                flag = "all"
+            if flag == "search":
+                above = np.concatenate([np.cumsum(h[::-1])[::-1][1:], [0]])   # keys with a larger digit
+                d = int(np.flatnonzero((above < k_rem) & (k_rem <= above + h))[0])
+                prefix |= d << sh
+                k_rem -= int(above[d])
+        sel = (np.ones(keys.size, bool) if flag == "all" else np.zeros(keys.size, bool) if flag == "none"
+               else keys >= np.uint64(prefix))
+        out = [None] * world
+        dist.all_gather_object(out, (s0, sel.reshape(imp.shape).astype(np.uint8)))
+        if rank == 0:
+            q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,k_frac", [(2, 0.2), (3, 0.05), (2, 0.0), (2, 1.5)])
+def test_global_topk_protocol_is_exact_over_ranks(world, k_frac):
+    """The 4-round 16-bit-digit histogram protocol of SURVEY §8(f)2 (gloo all-reduce between the rounds)
+    selects exactly the oracle's GLOBAL top-k over the union of all ranks' streams, with
+    massive ties (10 importance levels), for any world size."""
+    GW, GH = synth.grid(W, H)
+    k_total = int(k_frac * N_STREAMS * F * GH * GW)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_topk_worker, args=(r, world, port, q, k_total)) for r in range(world)]
+    for p in ps:
+        p.start()
+    parts = q.get(timeout=120)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    sel = np.concatenate([s for _, s in sorted(parts, key=lambda t: t[0])], 0)
+    imp = synth.importance_maps(N_STREAMS, F, GH, GW, 7, "levels")
+    ref = oracle.select(imp, W, H, oracle.MODE_TOPK, k_total)
+    np.testing.assert_array_equal(sel, ref)
+    assert sel.sum() == min(k_total, imp.size)
