@@ -60,7 +60,7 @@ enum { REGEN_POLICY_GUILLOTINE = 0, REGEN_POLICY_MAXRECT = 1, REGEN_POLICY_SKYLI
 enum { REGEN_DENSITY_SPAN = 0, REGEN_DENSITY_MEMBERS = 1 };
 enum { REGEN_DTYPE_BF16 = 0, REGEN_DTYPE_FP32 = 1 };
 enum { REGEN_CALL_SELECT = 0, REGEN_CALL_PACK = 1, REGEN_CALL_ENHANCE = 2, REGEN_CALL_SCATTER = 3,
-       REGEN_CALL_ENHANCE_SCATTER = 4 };
+       REGEN_CALL_ENHANCE_SCATTER = 4, REGEN_CALL_TEMPORAL = 5 };
 
 /* asynchronous status bits (*d_status) */
 enum {
@@ -288,6 +288,35 @@ REGEN_API regen_status regen_select_mbs_global(const regen_geom* geom, const reg
                                      const regen_topk_state* d_state, uint32_t* d_sel_bitmap, int32_t* d_labels,
                                      regen_region* d_regions, int64_t max_regions, int64_t* d_num_regions,
                                      int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * temporal MB-importance reuse, §3.2.2 P:584-609 (the step before a1: which frames of
+ * a chunk get a fresh importance prediction). One call = one chunk of F frames of S streams.
+ *   d_residual_y   [S][F][frame_h][frame_w] int16: the Y-channel residual of each frame
+ *   threshold      foreground = |residual| > threshold (D18)
+ *   budget         frames to predict over the S streams (from the execution plan); every
+ *                  stream keeps its anchor frame 0, the rest is shared by the ratio
+ *                  sum_i |dPhi_ij| / sum_j sum_i |dPhi_ij| with the largest-remainder rule
+ *                  (ties: lower stream), capped at F per stream (D18)
+ *   d_phi          [S][F] fp64 out: Phi = sum over the 4-connected foreground components of 1/area
+ *                  (the 1/Area operator), the exact sum of the correctly rounded terms
+ *   d_selected     [S][F] uint8 out: 1 = predict this frame: frame 0, and for N = budget_j - 1 even
+ *                  intervals of the y axis of the CDF of S = Norm(|dPhi|) (L1) the smallest
+ *                  frame k >= 1 whose CDF sum_{i<k} S_i reaches the interval's midpoint (t+0.5)/N
+ *                  (dPhi_i = Phi_{i+1} - Phi_i belongs to frame i+1)
+ *   d_reuse        [S][F] int32 out: the selected frame whose prediction frame f reuses (the nearest
+ *                  selected frame at or before f)
+ *   d_frames_per_stream [S] int32 out: each stream's budget
+ * Workspace: regen_workspace_size(REGEN_CALL_TEMPORAL, geom, NULL, NULL, &bytes). Frames must have
+ * fewer than 2^28 pixels, S <= 1024. fp64 decisions are taken in the oracle's order (bit-exact).
+ * regen_reuse_importance: d_out[s][f] = d_pred[s][d_reuse[s][f]] for the [S][F][GH][GW] fp32 maps
+ * (the predictor ran on the selected frames only); d_out must not alias d_pred.
+ * ------------------------------------------------------------------------------------------- */
+REGEN_API regen_status regen_temporal_select(const regen_geom* geom, const int16_t* d_residual_y, int32_t threshold,
+                                   int64_t budget, double* d_phi, uint8_t* d_selected, int32_t* d_reuse,
+                                   int32_t* d_frames_per_stream, void* d_ws, size_t ws_bytes, void* stream);
+REGEN_API regen_status regen_reuse_importance(const regen_geom* geom, const float* d_pred, const int32_t* d_reuse,
+                                    float* d_out, void* stream);
 
 /* Workspace bytes for a call (which = REGEN_CALL_*; params = the call's params struct;
  * sr = SR handle for ENHANCE, else NULL). */

@@ -9,6 +9,7 @@ the steps in the paper's order (Alg. 1, §3.3).
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import subprocess
 import threading
@@ -280,3 +281,94 @@ def run_workload(wl, importance: np.ndarray, frames: np.ndarray, weights: np.nda
     out = scatter(frames, ip["boxes"], ip["placement"], ip["owner"], hr, wl.sr.scale, wl.bin_w, wl.bin_h, f_lo, f_hi)
     ip.update(lr=lr, hr=hr, out=out)
     return ip
+
+
+# ----------------------------------------------------------------------------------- temporal reuse
+# SURVEY §8(f)3, §3.2.2 P:584-609. Phi (CCL + exact sum) is C (ref_phi_inv_area); the series, CDF
+# pick and budget allocation are plain Python floats (IEEE fp64, one operation at a time in the
+# order written), the order the CUDA kernel follows (readings D18 in DESIGN.md).
+
+def phi_inv_area(res_frame: np.ndarray, thr: int) -> tuple[float, int]:
+    """The 1/Area operator of one frame: (Phi, number of components)."""
+    r = np.ascontiguousarray(res_frame, np.int16)
+    H, W = r.shape
+    n = ctypes.c_int64(0)
+    f = lib().ref_phi_inv_area
+    f.restype = ctypes.c_double
+    return float(f(W, H, _p(r), int(thr), ctypes.byref(n))), int(n.value)
+
+
+def phi_series(residual: np.ndarray, thr: int) -> np.ndarray:
+    """Phi of every frame: [S][F] fp64 from the [S][F][H][W] int16 Y residuals."""
+    S, F = residual.shape[:2]
+    return np.array([[phi_inv_area(residual[s, f], thr)[0] for f in range(F)] for s in range(S)], np.float64)
+
+
+def delta_series(phi: list[float]) -> tuple[list[float], float, list[float], list[float]]:
+    """(|dPhi_i| for i = 0..F-2, T = their sum, S = Norm(|dPhi|) (L1), CDF M[k] = sum_{i<k} S_i
+    for k = 1..F-1 (M[0] = 0)): dPhi_i = Phi_{i+1} - Phi_i belongs to frame i+1."""
+    F = len(phi)
+    a = [abs(phi[i + 1] - phi[i]) for i in range(F - 1)]
+    T = 0.0
+    for x in a:
+        T = T + x
+    Sn = [x / T if T > 0.0 else 0.0 for x in a]
+    M = [0.0] * F
+    m = 0.0
+    for k in range(1, F):
+        m = m + Sn[k - 1]
+        M[k] = m
+    return a, T, Sn, M
+
+
+def allocate_budget(totals: list[float], budget: int, F: int) -> list[int]:
+    """Frames per stream: each stream keeps its anchor frame; the rest of the budget is shared
+    by the ratio sum_i |dPhi_ij| / sum_j sum_i |dPhi_ij| with the largest-remainder rule (ties: lower
+    stream), each capped at F. The budget is clamped to [S, S*F]."""
+    S = len(totals)
+    B = min(max(budget, S), S * F)
+    rest = B - S
+    Tsum = 0.0
+    for t in totals:
+        Tsum = Tsum + t
+    q = [(float(rest) * t) / Tsum if Tsum > 0.0 else float(rest) / float(S) for t in totals]
+    fl = [math.floor(x) for x in q]
+    rem = [q[j] - fl[j] for j in range(S)]
+    n = [1 + fl[j] for j in range(S)]
+    left = rest - sum(fl)
+    for j in sorted(range(S), key=lambda j: (-rem[j], j))[:max(left, 0)]:
+        n[j] += 1
+    return [min(x, F) for x in n]
+
+
+def cdf_pick(M: list[float], n: int, F: int) -> list[int]:
+    """Frame 0 (the anchor) and, for N = n - 1 even intervals of the CDF's y axis, the
+    smallest frame k >= 1 with M[k] >= (t + 0.5) / N; duplicates collapse."""
+    sel = {0}
+    N = n - 1
+    for t in range(N):
+        y = (t + 0.5) / N
+        for k in range(1, F):
+            if M[k] >= y:
+                sel.add(k)
+                break
+    return sorted(sel)
+
+
+def temporal_select(residual: np.ndarray, thr: int, budget: int) -> dict:
+    """The whole §3.2.2 step for one chunk: phi [S][F], selected [S][F] u8, reuse [S][F] (the nearest
+    selected frame at or before f), frames_per_stream [S]."""
+    S, F = residual.shape[:2]
+    phi = phi_series(residual, thr)
+    series = [delta_series(list(phi[s])) for s in range(S)]
+    n = allocate_budget([t for _, t, _, _ in series], budget, F)
+    selected = np.zeros((S, F), np.uint8)
+    reuse = np.zeros((S, F), np.int32)
+    for s in range(S):
+        for f in cdf_pick(series[s][3], n[s], F):
+            selected[s, f] = 1
+        last = 0
+        for f in range(F):
+            last = f if selected[s, f] else last
+            reuse[s, f] = last
+    return dict(phi=phi, selected=selected, reuse=reuse, frames_per_stream=np.array(n, np.int32))

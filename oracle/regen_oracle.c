@@ -701,3 +701,49 @@ int ref_scatter_mt(int S, int F, int W, int H, int mb, int scale, const uint8_t*
   free(jobs);
   return 0;
 }
+
+/* ------------------------------------------------------------------------------------------ */
+/* f3. Temporal MB-importance reuse, §3.2.2: the 1/Area operator Phi of one frame's   */
+/* Y-channel residual (Appx D.2 P:1625-1628: "1/Area captures the change of small    */
+/* objects"). Readings (D18): foreground = |residual| > thr; components are           */
+/* 4-connected (BFS flood fill in raster order); Phi = sum over components of 1/area, each term  */
+/* the correctly rounded fp64 1.0/area and the sum the exact sum of those terms rounded once to */
+/* fp64 (an order-independent definition: terms are multiples of 2^-80 for areas < 2^28, so an  */
+/* __int128 accumulator of term * 2^80 is exact). Returns Phi; *ncomp = number of components.   */
+/* ------------------------------------------------------------------------------------------ */
+double ref_phi_inv_area(int W, int H, const int16_t* res, int thr, int64_t* ncomp) {
+  const int64_t n = (int64_t)W * H;
+  uint8_t* seen = (uint8_t*)calloc((size_t)(n > 0 ? n : 1), 1);
+  int64_t* queue = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+  __int128 acc = 0;
+  int64_t nc = 0;
+  for (int64_t start = 0; start < n; ++start) {
+    const int v0 = res[start] < 0 ? -res[start] : res[start];
+    if (v0 <= thr || seen[start]) continue;
+    int64_t head = 0, tail = 0, area = 0;
+    seen[start] = 1;
+    queue[tail++] = start;
+    while (head < tail) {
+      const int64_t c = queue[head++];
+      const int cx = (int)(c % W), cy = (int)(c / W);
+      ++area;
+      const int nx[4] = {cx, cx - 1, cx + 1, cx}, ny[4] = {cy - 1, cy, cy, cy + 1};
+      for (int d = 0; d < 4; ++d) {
+        if (nx[d] < 0 || ny[d] < 0 || nx[d] >= W || ny[d] >= H) continue;
+        const int64_t nb = (int64_t)ny[d] * W + nx[d];
+        const int v = res[nb] < 0 ? -res[nb] : res[nb];
+        if (v > thr && !seen[nb]) {
+          seen[nb] = 1;
+          queue[tail++] = nb;
+        }
+      }
+    }
+    ++nc;
+    const double t = 1.0 / (double)area;            /* correctly rounded term */
+    acc += (__int128)ldexp(t, 80);                   /* exact: t is a multiple of 2^-80 */
+  }
+  free(seen);
+  free(queue);
+  if (ncomp) *ncomp = nc;
+  return ldexp((double)acc, -80);                    /* int128 -> double: round to nearest even */
+}

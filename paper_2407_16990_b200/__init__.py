@@ -23,7 +23,7 @@ ORDER_DENSITY, ORDER_AREA, ORDER_HEIGHT = 0, 1, 2
 POLICY_GUILLOTINE, POLICY_MAXRECT, POLICY_SKYLINE, POLICY_SHELF = 0, 1, 2, 3
 DENSITY_SPAN, DENSITY_MEMBERS = 0, 1
 DTYPE_BF16, DTYPE_FP32 = 0, 1
-CALL_SELECT, CALL_PACK, CALL_ENHANCE, CALL_SCATTER, CALL_ENHANCE_SCATTER = 0, 1, 2, 3, 4
+CALL_SELECT, CALL_PACK, CALL_ENHANCE, CALL_SCATTER, CALL_ENHANCE_SCATTER, CALL_TEMPORAL = 0, 1, 2, 3, 4, 5
 ST_REGION_OVERFLOW, ST_BOX_OVERFLOW, ST_FREELIST_OVERFLOW, ST_TOPK_INCOMPLETE = 1, 2, 4, 8
 TOPK_STATE_BYTES, TOPK_DIGITS = 24, 1 << 16
 
@@ -32,7 +32,7 @@ EXPORTED = ["regen_select_mbs", "regen_pack_regions", "regen_sr_create", "regen_
             "regen_status_string", "regen_last_error", "regen_abi_version", "regen_enhance_kernel_count",
             "regen_enhance_scatter", "regen_trace_enable", "regen_trace_read", "regen_trace_filter",
             "regen_enhance_owned", "regen_scatter_bilinear", "regen_topk_init", "regen_topk_histogram",
-            "regen_topk_pick", "regen_select_mbs_global"]
+            "regen_topk_pick", "regen_select_mbs_global", "regen_temporal_select", "regen_reuse_importance"]
 
 
 class Geom(ctypes.Structure):
@@ -90,6 +90,8 @@ def _load():
     lib.regen_scatter_bilinear.argtypes = [P(Geom), i32, vp, vp, vp, i32, vp]
     lib.regen_workspace_size.argtypes = [i32, P(Geom), vp, vp, P(sz)]
     lib.regen_topk_init.argtypes = [i64, vp, vp]
+    lib.regen_temporal_select.argtypes = [P(Geom), vp, i32, i64, vp, vp, vp, vp, vp, sz, vp]
+    lib.regen_reuse_importance.argtypes = [P(Geom), vp, vp, vp, vp]
     lib.regen_topk_histogram.argtypes = [P(Geom), i64, vp, vp, vp, vp]
     lib.regen_topk_pick.argtypes = [vp, vp, vp]
     lib.regen_select_mbs_global.argtypes = [P(Geom), P(SelectParams), i64, vp, vp, vp, vp, vp, i64, vp, vp, vp, sz, vp]
@@ -102,12 +104,9 @@ def _load():
     lib.regen_status_string.restype = ctypes.c_char_p
     lib.regen_last_error.restype = ctypes.c_char_p
     lib.regen_abi_version.restype = i32
-    for name in ["regen_select_mbs", "regen_pack_regions", "regen_sr_create", "regen_sr_destroy",
-                 "regen_stitch_bins", "regen_enhance_packed", "regen_scatter_blend", "regen_workspace_size",
-                 "regen_enhance_kernel_count", "regen_enhance_scatter", "regen_trace_enable", "regen_trace_read", "regen_trace_filter",
-                 "regen_enhance_owned", "regen_scatter_bilinear", "regen_topk_init", "regen_topk_histogram",
-            "regen_topk_pick", "regen_select_mbs_global"]:
-        getattr(lib, name).restype = ctypes.c_int
+    for name in EXPORTED:
+        if name not in ("regen_capacity_mbs", "regen_status_string", "regen_last_error", "regen_abi_version"):
+            getattr(lib, name).restype = ctypes.c_int
     return lib
 
 
@@ -203,6 +202,39 @@ def select_mbs_global(geom, params, stream0, importance, state, sel_bitmap, labe
                                        _ptr(sel_bitmap), _ptr(labels), _ptr(regions), max_regions, _ptr(num_regions),
                                        _ptr(status), _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)),
            "regen_select_mbs_global")
+
+
+def temporal_select(geom, residual_y, threshold, budget, phi, selected, reuse, frames_per_stream, ws, stream=None):
+    _check(lib.regen_temporal_select(ctypes.byref(geom), _ptr(residual_y), threshold, budget, _ptr(phi), _ptr(selected),
+                                     _ptr(reuse), _ptr(frames_per_stream), _ptr(ws), ws.numel() * ws.element_size(),
+                                     _stream(stream)), "regen_temporal_select")
+
+
+def reuse_importance(geom, pred, reuse, out, stream=None):
+    _check(lib.regen_reuse_importance(ctypes.byref(geom), _ptr(pred), _ptr(reuse), _ptr(out), _stream(stream)),
+           "regen_reuse_importance")
+
+
+class TemporalReuse:
+    """Buffers of regen_temporal_select for one chunk of S streams x F frames."""
+
+    def __init__(self, S, F, W, H, threshold=8, device="cuda"):
+        import torch
+        self.geom = Geom(S, F, W, H, 16)
+        self.threshold = threshold
+        self.phi = torch.zeros((S, F), dtype=torch.float64, device=device)
+        self.selected = torch.zeros((S, F), dtype=torch.uint8, device=device)
+        self.reuse = torch.zeros((S, F), dtype=torch.int32, device=device)
+        self.frames = torch.zeros(S, dtype=torch.int32, device=device)
+        self.ws = torch.empty(workspace_size(CALL_TEMPORAL, self.geom), dtype=torch.uint8, device=device)
+
+    def run(self, residual_y, budget, stream=None):
+        temporal_select(self.geom, residual_y, self.threshold, budget, self.phi, self.selected, self.reuse, self.frames,
+                        self.ws, stream)
+
+    def reuse_maps(self, pred, out, stream=None):
+        reuse_importance(self.geom, pred, self.reuse, out, stream)
+        return out
 
 
 def stitch_bins(geom, params, dtype, frames, boxes, max_boxes, num_boxes, num_bins, lr_bins, ws, stream=None):

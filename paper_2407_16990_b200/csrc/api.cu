@@ -25,6 +25,7 @@ regen_status validate_geom(const regen_geom* g) {
 size_t select_workspace_bytes(const regen_geom& g);
 size_t pack_workspace_bytes(const regen_geom& g, int64_t max_regions);
 size_t enhance_scatter_ws_bytes(const SRNet* net, const regen_pack_params& p);
+size_t temporal_workspace_bytes(const regen_geom& g);
 
 }  // namespace regen
 
@@ -51,6 +52,9 @@ extern "C" regen_status regen_workspace_size(int32_t which, const regen_geom* ge
     }
     case REGEN_CALL_SCATTER:
       *bytes = 0;
+      return REGEN_OK;
+    case REGEN_CALL_TEMPORAL:
+      *bytes = temporal_workspace_bytes(*geom);
       return REGEN_OK;
     case REGEN_CALL_ENHANCE_SCATTER: {
       REGEN_REQUIRE(params && sr, "ENHANCE_SCATTER needs pack params and the SR handle");

@@ -9,6 +9,7 @@ random inputs with the shapes, value distributions and structure of the paper's 
   variants: 10 integer levels (massive ties), noise-heavy, all-equal, checkerboard,
   full-frame.
 * frames: RGB8 HWC uniform random (SR latency is pixel-value agnostic).
+* Y residuals (temporal reuse, §3.2.2): int16, sparse moving objects + noise + occasional scene cuts.
 * SR weights: torch.nn.Conv2d default init U(+-1/sqrt(fan_in)) for weights and biases (reading D11).
 """
 from __future__ import annotations
@@ -68,6 +69,38 @@ def frames_rgb8(S: int, F: int, H: int, W: int, seed: int = 0, s0: int = 0) -> n
     for s in range(S):
         rng = _rng(seed, 2, s0 + s)
         out[s] = rng.integers(0, 256, size=(F, H, W, 3), dtype=np.uint8)
+    return out
+
+
+def residuals_y(S: int, F: int, H: int, W: int, seed: int = 0, s0: int = 0, scene_cut: float = 0.1) -> np.ndarray:
+    """int16 [S][F][H][W] Y-channel residuals of streams s0 .. s0+S-1 (the decoder's residual tap,
+    P:598 footnote): mostly zero (the codec predicted the block well), a few small moving objects
+    whose pixels carry signed residuals U(+-10..60) with holes (so they split into several small
+    components), sparse noise on 0.05% of the pixels, and with probability `scene_cut` per frame a
+    large textured block (a big change that the 1/Area operator weighs little)."""
+    out = np.zeros((S, F, H, W), np.int16)
+    for s in range(S):
+        rng = _rng(seed, 4, s0 + s)
+        n_obj = int(rng.integers(3, 13))
+        pos = rng.uniform([0, 0], [W, H], size=(n_obj, 2))
+        vel = rng.uniform(-4, 4, size=(n_obj, 2))
+        size = rng.integers(3, 25, size=(n_obj, 2))
+        for f in range(F):
+            r = out[s, f]
+            for o in range(n_obj):
+                x0, y0 = int(pos[o, 0]) % W, int(pos[o, 1]) % H
+                w, h = int(size[o, 0]), int(size[o, 1])
+                blk = r[y0:y0 + h, x0:x0 + w]
+                mag = rng.integers(10, 61, size=blk.shape) * rng.choice([-1, 1], size=blk.shape)
+                keep = rng.random(blk.shape) < 0.8
+                blk[keep] = mag[keep]
+                pos[o] += vel[o]
+            noise = rng.random((H, W)) < 0.0005
+            r[noise] = rng.integers(-30, 31, size=int(noise.sum()))
+            if rng.random() < scene_cut:
+                bw, bh = int(rng.integers(W // 4, W // 2)), int(rng.integers(H // 4, H // 2))
+                bx, by = int(rng.integers(0, W - bw)), int(rng.integers(0, H - bh))
+                r[by:by + bh, bx:bx + bw] = rng.integers(-40, 41, size=(bh, bw))
     return out
 
 
@@ -161,7 +194,7 @@ CONFIGS = {
     # C5: 16 streams of 720p in 8 selection groups of 2 streams (a 2-stream group at the 50% end of
     # the ratio sweep already needs ~3k bins of C=64 activations); ratio set per run (5..50%)
     "c5": Workload("c5_16x720p_x2_edsr16x64_bf16", 2, 30, 1280, 720, 5.0, 128, 128, 4,
-                   SRConfig(2, 64, 16, 1.0, bf16=True), 4096, groups=8),
+                   SRConfig(2, 64, 16, 1.0, bf16=True), 5632, groups=8),
 }
 C5_RATIOS = (5.0, 10.0, 15.0, 20.0, 25.0, 35.0, 50.0)
 

@@ -133,7 +133,7 @@ def test_status_freelist_overflow_keeps_a_valid_plan(monkeypatch):
     rg = _rg()
     wl = dataclasses.replace(_wl_small(), partition_mb=1)      # Block mode: many boxes, many free areas
     imp_h = synth.importance_maps(wl.S, wl.F, wl.GH, wl.GW, 5, "noisy")
-    monkeypatch.setenv("REGEN_PACK_POOL_LIMIT", "40")        # 32 register slots + 8 overflow slots
+    monkeypatch.setenv("REGEN_PACK_POOL_LIMIT", "1")         # one live free area per bin
     p = _make(wl, synth.sr_weights(wl.sr, 0))()
     imp = torch.from_numpy(imp_h).cuda()
     p.select(imp)
