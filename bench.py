@@ -266,6 +266,8 @@ def main() -> None:
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--dry-run", action="store_true", help="launcher/sharding only (CPU, gloo): print the plan")
+    ap.add_argument("--input", default="rgb", choices=["rgb", "nv12"],
+                    help="frame format: RGB8, or NV12 decoder output converted on the GPU inside the step")
     args = ap.parse_args()
     wl = synth.CONFIGS[args.config]
     if args.ratio is not None:
@@ -307,7 +309,8 @@ def main() -> None:
     seed = 0
     G = len(groups)
     imp_h = [synth.importance_maps(wl.S, wl.F, wl.GH, wl.GW, seed, s0=g0) for g0, _ in groups]
-    fr_h = [synth.frames_rgb8(wl.S, wl.F, wl.H, wl.W, seed, s0=g0) for g0, _ in groups]
+    nv12 = args.input == "nv12"
+    fr_h = [(synth.frames_nv12 if nv12 else synth.frames_rgb8)(wl.S, wl.F, wl.H, wl.W, seed, s0=g0) for g0, _ in groups]
     w = synth.sr_weights(wl.sr, 0)
 
     def make_pipe():
@@ -326,7 +329,21 @@ def main() -> None:
         # two pipelines (double-buffered state): the index path (select + pack) of batch k+1 on one CUDA
         # stream while the SR (enhance + scatter) of batch k runs on another (schedule.py: the same
         # runner the full-size parity tests drive); a rank with several groups cycles through them
-        runner = PipelinedRunner(make_pipe, dev, bilinear=os.environ.get("REGEN_BILINEAR", "side"))
+        # a rank with several selection groups keeps up to 4 pipelines and runs the index paths of up
+        # to 3 groups at once (each packer on its own SM); memory permitting (REGEN_PIPES / REGEN_FRONTS
+        # override, A/B aids)
+        n_pipes = 2
+        if G > 1:
+            free0 = torch.cuda.mem_get_info(dev)[0]
+            probe = make_pipe()
+            per_pipe = max(1, free0 - torch.cuda.mem_get_info(dev)[0])
+            del probe
+            torch.cuda.empty_cache()
+            n_pipes = int(max(2, min(4, G, (0.7 * torch.cuda.mem_get_info(dev)[0]) // per_pipe)))
+        n_pipes = int(os.environ.get("REGEN_PIPES", n_pipes))
+        n_front = int(os.environ.get("REGEN_FRONTS", max(1, n_pipes - 1)))
+        runner = PipelinedRunner(make_pipe, dev, bilinear=os.environ.get("REGEN_BILINEAR", "side"), nv12=nv12,
+                                 n_pipes=n_pipes, n_front=n_front)
         pipes = runner.pipes
         p = pipes[0]
         imp = [torch.from_numpy(a).to(dev) for a in imp_h]
@@ -336,11 +353,12 @@ def main() -> None:
 
         def step_instrumented(gi):
             ev[0].record(stream)
+            frames = p.convert_nv12(fr[gi]) if nv12 else fr[gi]
             p.select(imp[gi])
             ev[1].record(stream)
             p.pack_step(imp[gi])
             ev[2].record(stream)
-            p.enhance_scatter(fr[gi])
+            p.enhance_scatter(frames)
             ev[3].record(stream)
 
         # serial instrumented batches (L2 flushed before each): per-stage device time and the work of
@@ -434,7 +452,7 @@ def main() -> None:
         runner.e2e(imp_pin, fr_pin, out_pin, 1, stream)                   # warm
         e2e_t = runner.e2e(imp_pin, fr_pin, out_pin, args.e2e_steps, stream)
         last = args.e2e_steps * G - 1
-        assert torch.equal(out_pin[last % 2], pipes[last % 2].out.cpu())
+        assert torch.equal(out_pin[last % 2], pipes[last % runner.P].out.cpu())
     if world > 1:
         t = torch.tensor([0.0 if e2e_t != e2e_t else e2e_t], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -535,16 +553,18 @@ def main() -> None:
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if strong else "weak", "vs_baseline": None,
             "dtype": "bf16" if wl.sr.bf16 else "f32", "data": "synthetic",
-            "config": {"workload": wl.name, "streams_total": (wl.groups if strong else world) * wl.S,
+            "config": {"workload": wl.name + ("_nv12" if nv12 else ""), "input": "NV12 (BT.601 on the GPU in the step)"
+                       if nv12 else "RGB8", "streams_total": (wl.groups if strong else world) * wl.S,
                        "selection_group_streams": wl.S, "groups_rank0": G, "frames_per_step": int(job_frames),
                        "frame": f"{wl.W}x{wl.H}->x{wl.sr.scale}", "topk_pct": wl.pct,
                        "bins_per_step": int(job_bins), "bin": f"{wl.bin_w}x{wl.bin_h}", "boxes_per_step": int(job_boxes),
                        "sr": f"EDSR {wl.sr.n_resblocks}x{wl.sr.channels} x{wl.sr.scale}",
                        "l2": "timed steps run back to back; each step's working set (packed activations and HR "
                              "frames, >1 GB) is >10x the 126 MB L2, so no step finds the previous one's data",
-                       "schedule": "index path (select+pack) of batch k+1 overlapped with SR (enhance+scatter) of batch k "
-                                   "on two CUDA streams (bilinear pass on a third, lowest-priority stream), double-buffered "
-                                   "pipeline state; a rank cycles through its selection groups"
+                       "schedule": (f"{runner.P if G else 0} pipelines, index paths (select+pack) of up to "
+                                    f"{len(runner.s_fronts) if G else 0} batches on their own streams ahead of the SR "
+                                    "(enhance+scatter) stream, bilinear pass on a lowest-priority stream; a rank cycles "
+                                    "through its selection groups")
                                    + ("; the K steps replayed as one captured CUDA graph" if graph is not None else ""),
                        "parallelism": (f"strong dp{world}: {wl.groups} selection groups sharded by rank" if strong
                                        else f"weak dp{world}: one selection group per rank") +

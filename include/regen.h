@@ -318,6 +318,16 @@ REGEN_API regen_status regen_temporal_select(const regen_geom* geom, const int16
 REGEN_API regen_status regen_reuse_importance(const regen_geom* geom, const float* d_pred, const int32_t* d_reuse,
                                     float* d_out, void* stream);
 
+/* ---------------------------------------------------------------------------------------------
+ * NV12 input (the hardware decoder's output format; decode stage P:424 §3.1).
+ *   d_nv12  [S][F] frames of frame_w*frame_h*3/2 bytes: Y plane [frame_h][frame_w] then the
+ *           interleaved U,V plane [frame_h/2][frame_w/2][2]
+ *   d_rgb8  [S][F][frame_h][frame_w][3] out, the d_frames of every other call
+ * BT.601 limited range, 8-bit integer form, nearest chroma (D19, bit-exact vs the oracle).
+ * REGEN_E_INVALID unless frame_w % 4 == 0, frame_h % 2 == 0 and both buffers are 4-byte aligned.
+ * ------------------------------------------------------------------------------------------- */
+REGEN_API regen_status regen_nv12_to_rgb8(const regen_geom* geom, const uint8_t* d_nv12, uint8_t* d_rgb8, void* stream);
+
 /* Workspace bytes for a call (which = REGEN_CALL_*; params = the call's params struct;
  * sr = SR handle for ENHANCE, else NULL). */
 REGEN_API regen_status regen_workspace_size(int32_t which, const regen_geom* geom, const void* params, const void* sr,

@@ -283,6 +283,16 @@ def run_workload(wl, importance: np.ndarray, frames: np.ndarray, weights: np.nda
     return ip
 
 
+def nv12_to_rgb8(nv12: np.ndarray, W: int, H: int) -> np.ndarray:
+    """f4 (reading D19): uint8 NV12 frames [..., H*W*3/2] -> RGB8 [..., H, W, 3]."""
+    a = np.ascontiguousarray(nv12, np.uint8)
+    lead = a.shape[:-1]
+    frames = int(np.prod(lead)) if lead else 1
+    out = np.zeros(lead + (H, W, 3), np.uint8)
+    lib().ref_nv12_to_rgb8(ctypes.c_int64(frames), W, H, _p(a), _p(out))
+    return out
+
+
 # ----------------------------------------------------------------------------------- temporal reuse
 # SURVEY §8(f)3, §3.2.2 P:584-609. Phi (CCL + exact sum) is C (ref_phi_inv_area); the series, CDF
 # pick and budget allocation are plain Python floats (IEEE fp64, one operation at a time in the

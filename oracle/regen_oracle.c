@@ -747,3 +747,32 @@ double ref_phi_inv_area(int W, int H, const int16_t* res, int thr, int64_t* ncom
   if (ncomp) *ncomp = nc;
   return ldexp((double)acc, -80);                    /* int128 -> double: round to nearest even */
 }
+
+/* ------------------------------------------------------------------------------------------ */
+/* f4. NV12 decoder output ("decoded into frames") to the RGB8 frames the path reads.     */
+/* Reading D19: ITU-R BT.601 limited range in the common 8-bit integer form                     */
+/*   C = Y-16, D = U-128, E = V-128; R = clip((298C + 409E + 128) >> 8),                        */
+/*   G = clip((298C - 100D - 208E + 128) >> 8), B = clip((298C + 516D + 128) >> 8),              */
+/* chroma of pixel (x, y) = the U/V sample (x/2, y/2) (nearest). NV12 frame = Y plane [H][W]    */
+/* then interleaved U,V plane [H/2][W/2][2]; out [frames][H][W][3].                             */
+/* ------------------------------------------------------------------------------------------ */
+static int clip255(int v) { return v < 0 ? 0 : (v > 255 ? 255 : v); }
+
+int ref_nv12_to_rgb8(int64_t frames, int W, int H, const uint8_t* nv12, uint8_t* rgb) {
+  for (int64_t f = 0; f < frames; ++f) {
+    const uint8_t* Y = nv12 + f * (int64_t)W * H * 3 / 2;
+    const uint8_t* UV = Y + (int64_t)W * H;
+    uint8_t* out = rgb + f * (int64_t)W * H * 3;
+    for (int y = 0; y < H; ++y)
+      for (int x = 0; x < W; ++x) {
+        const int C = Y[(int64_t)y * W + x] - 16;
+        const int D = UV[(int64_t)(y / 2) * W + 2 * (x / 2)] - 128;
+        const int E = UV[(int64_t)(y / 2) * W + 2 * (x / 2) + 1] - 128;
+        uint8_t* px = out + ((int64_t)y * W + x) * 3;
+        px[0] = (uint8_t)clip255((298 * C + 409 * E + 128) >> 8);
+        px[1] = (uint8_t)clip255((298 * C - 100 * D - 208 * E + 128) >> 8);
+        px[2] = (uint8_t)clip255((298 * C + 516 * D + 128) >> 8);
+      }
+  }
+  return 0;
+}

@@ -32,7 +32,8 @@ EXPORTED = ["regen_select_mbs", "regen_pack_regions", "regen_sr_create", "regen_
             "regen_status_string", "regen_last_error", "regen_abi_version", "regen_enhance_kernel_count",
             "regen_enhance_scatter", "regen_trace_enable", "regen_trace_read", "regen_trace_filter",
             "regen_enhance_owned", "regen_scatter_bilinear", "regen_topk_init", "regen_topk_histogram",
-            "regen_topk_pick", "regen_select_mbs_global", "regen_temporal_select", "regen_reuse_importance"]
+            "regen_topk_pick", "regen_select_mbs_global", "regen_temporal_select", "regen_reuse_importance",
+            "regen_nv12_to_rgb8"]
 
 
 class Geom(ctypes.Structure):
@@ -90,6 +91,7 @@ def _load():
     lib.regen_scatter_bilinear.argtypes = [P(Geom), i32, vp, vp, vp, i32, vp]
     lib.regen_workspace_size.argtypes = [i32, P(Geom), vp, vp, P(sz)]
     lib.regen_topk_init.argtypes = [i64, vp, vp]
+    lib.regen_nv12_to_rgb8.argtypes = [P(Geom), vp, vp, vp]
     lib.regen_temporal_select.argtypes = [P(Geom), vp, i32, i64, vp, vp, vp, vp, vp, sz, vp]
     lib.regen_reuse_importance.argtypes = [P(Geom), vp, vp, vp, vp]
     lib.regen_topk_histogram.argtypes = [P(Geom), i64, vp, vp, vp, vp]
@@ -202,6 +204,10 @@ def select_mbs_global(geom, params, stream0, importance, state, sel_bitmap, labe
                                        _ptr(sel_bitmap), _ptr(labels), _ptr(regions), max_regions, _ptr(num_regions),
                                        _ptr(status), _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)),
            "regen_select_mbs_global")
+
+
+def nv12_to_rgb8(geom, nv12, rgb8, stream=None):
+    _check(lib.regen_nv12_to_rgb8(ctypes.byref(geom), _ptr(nv12), _ptr(rgb8), _stream(stream)), "regen_nv12_to_rgb8")
 
 
 def temporal_select(geom, residual_y, threshold, budget, phi, selected, reuse, frames_per_stream, ws, stream=None):
@@ -403,6 +409,15 @@ class Pipeline:
         out = self.out if out is None else out
         scatter_bilinear(self.geom, self.scale, frames, self.owner, out, self.out_dtype, stream)
         return out
+
+    def convert_nv12(self, nv12, stream=None):
+        """NV12 decoder frames [S][F][H*W*3/2] u8 -> the RGB8 frames tensor the other calls read."""
+        t = self.torch
+        if getattr(self, "_rgb", None) is None:
+            g = self.geom
+            self._rgb = t.empty((g.S, g.F, g.frame_h, g.frame_w, 3), dtype=t.uint8, device=self.out.device)
+        nv12_to_rgb8(self.geom, nv12, self._rgb, stream)
+        return self._rgb
 
     def run(self, importance, frames, out=None, stream=None, fused=True):
         """select -> pack -> enhance -> scatter; fused=True uses regen_enhance_scatter for the last two."""

@@ -240,6 +240,7 @@ struct PackArgs {
   regen_box* boxes;
   uint64_t* rect;           // [PACK_MAX_BINS][PACK_SLOTS] free areas: x | y<<16 | w<<32 | h<<48 (workspace)
   uint32_t* seqv;           // [PACK_MAX_BINS][PACK_SLOTS] creation sequence of each free area
+  uint64_t* pool;           // [2][PACK_POOL] pool path: keys then rects of the slots beyond the registers
   const int32_t* order;
   const int64_t* num_boxes;
   int64_t max_boxes;
@@ -247,9 +248,283 @@ struct PackArgs {
   int32_t* status;
   int bin_w, bin_h, max_bins, gutter;
   int prof;         // REGEN_PACK_PROF=1: print per-phase cycle counts
-  int slot_limit;   // live free areas per bin (PACK_SLOTS; REGEN_PACK_POOL_LIMIT=n lowers it: a test aid
-                    // that makes REGEN_ST_FREELIST_OVERFLOW reachable on small inputs)
+  int slot_limit;   // bins path: live free areas per bin (PACK_SLOTS)
+  int pool_limit;   // pool path: live free areas (PACK_POOL + 32). REGEN_PACK_POOL_LIMIT=n lowers both: a
+                    // test aid that makes REGEN_ST_FREELIST_OVERFLOW reachable on small inputs
 };
+
+// Two data structures for the same sequential Alg. 1 loop (identical placements, both bit-exact
+// against the oracle): up to PACK_BINS_FROM boxes a single pool of live areas held in registers (one
+// per lane) + SMEM/global overflow (pack_pool: a short dependent chain per box while the pool stays
+// small); beyond, per-bin area lists with dominance summaries (pack_bins: per-box cost independent
+// of the total number of live areas, which reaches thousands on the 720p 50% and 8-stream groups).
+constexpr int PACK_BINS_FROM = 5000;
+constexpr int PACK_SMEM = 48 * 1024;   // dynamic SMEM of either path: fits beside a resident SR CTA
+
+constexpr int PACK_POOL = 8192;   // live free areas beyond the register slots (global workspace, L1/L2)
+constexpr int PACK_DIMS = 4096;   // box footprints + indices staged in SMEM in packing order (32 KB)
+constexpr int PACK_SOV = 1024;    // overflow slots 32 .. 32+PACK_SOV-1 in SMEM (16 KB; 48 KB total so the CTA fits beside a resident SR CTA), the rest global
+
+
+// One warp. The live free areas of the opened bins form a compact pool: key = bin << 32 | creation
+// sequence (unique; its minimum is the first area in (bin, seq) order, D12), rect = x | y<<16 | w<<32
+// | h<<48. Slot s < 32 lives in a REGISTER of lane s (the pool holds ~15 areas on the paper's maps
+// after pruning), slots >= 32 in a global overflow array (L1-resident). Per box: lanes test their
+// areas (fit unrotated or rotated), a warp min-reduction picks the first fit, every lane
+// replays the placement and the guillotine remainders (D6) on identical state: the consumed area's
+// slot takes the first kept remainder (or the pool's last entry), the second is appended. Unopened
+// bins are implicit (opened lazily in order). The packer is one dependent chain per box, so it is
+// written for the fewest instructions on that chain: the next footprint is prefetched, a register
+// slot update is one predicated move, the clock probes run only under REGEN_PACK_PROF=1.
+__device__ __forceinline__ bool fits(uint64_t r, int pw, int ph) {
+  const int fw = (int)((r >> 32) & 0xFFFF), fh = (int)(r >> 48);
+  return (fw >= pw && fh >= ph) || (fw >= ph && fh >= pw);
+}
+
+// Large pools (thousands of live areas on noisy maps / Block mode / 8-stream groups): when the overflow
+// part of the pool exceeds PACK_BIG slots, warp 0 hands the fit test of that box to all PACK_WARPS warps
+// (named barrier 1: publish the box, each warp scans a strided share of the overflow slots and posts its
+// first fit, warp 0 merges the candidates); small pools keep the single-warp path and the helper warps
+// sleep on the barrier.
+constexpr int PACK_WARPS = 8;
+constexpr int PACK_BIG = 192;
+
+// non-.aligned named barrier, entered by whole warps after a __syncwarp (lane-0 branches precede it)
+__device__ __forceinline__ void pack_bar() {
+  __syncwarp();
+  asm volatile("barrier.sync 1, %0;" ::"r"(32 * PACK_WARPS) : "memory");
+}
+
+// warp-wide first fit: min key over the lanes' candidates, with the holder's rect and slot
+__device__ __forceinline__ void warp_first_fit(uint64_t best, uint64_t brect, int bslot, uint64_t& wkey,
+                                               uint64_t& wrect, int& wslot) {
+  const uint32_t bhi = (uint32_t)(best >> 32);
+  const uint32_t mhi = __reduce_min_sync(0xffffffffu, bhi);
+  const uint32_t mlo = __reduce_min_sync(0xffffffffu, bhi == mhi ? (uint32_t)best : 0xFFFFFFFFu);
+  wkey = ((uint64_t)mhi << 32) | mlo;
+  const uint32_t hold = __ballot_sync(0xffffffffu, best == wkey);
+  const int hl = hold ? __ffs(hold) - 1 : 0;
+  wrect = __shfl_sync(0xffffffffu, brect, hl);
+  wslot = __shfl_sync(0xffffffffu, bslot, hl);
+}
+
+__device__ void pack_pool(const PackArgs& a, uint8_t* psm) {
+  __shared__ int task_hw, task_pw, task_ph;   // the box whose fit test the helper warps join (hw < 0: done)
+  __shared__ uint64_t cand_key[PACK_WARPS], cand_rect[PACK_WARPS];
+  __shared__ int cand_slot[PACK_WARPS];
+  uint32_t* dims = (uint32_t*)psm;                      // (w+g) | (h+g)<<16 of the oi-th box in order
+  int32_t* ords = (int32_t*)(dims + PACK_DIMS);         // box index of the oi-th box in order
+  uint64_t* skey = (uint64_t*)(ords + PACK_DIMS);       // overflow slots 32 .. 32+PACK_SOV-1 (SMEM)
+  uint64_t* srect = skey + PACK_SOV;
+  uint64_t* gkey = a.pool;                              // overflow slots beyond (global, L1-resident)
+  uint64_t* grect = a.pool + PACK_POOL;
+  // overflow slot i (= pool slot 32 + i)
+  auto ov_key = [&](int i) -> uint64_t& { return i < PACK_SOV ? skey[i] : gkey[i - PACK_SOV]; };
+  auto ov_rect = [&](int i) -> uint64_t& { return i < PACK_SOV ? srect[i] : grect[i - PACK_SOV]; };
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t n = min(*a.num_boxes, a.max_boxes);
+  if (warp > 0) {
+    // =========== helper warps: join the fit test of large-pool boxes ===========
+    for (;;) {
+      pack_bar();   // B1: a task (or the end) is published
+      const int hw = task_hw, pw = task_pw, ph = task_ph;
+      if (hw < 0) return;
+      uint64_t best = ~0ull, brect = 0;
+      int bslot = -1;
+      for (int s0 = 32 + 32 * warp + lane; s0 < hw; s0 += 128 * PACK_WARPS) {
+        uint64_t kk[4], rq[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int sl = s0 + 32 * PACK_WARPS * u;
+          kk[u] = sl < hw ? ov_key(sl - 32) : ~0ull;
+          rq[u] = sl < hw ? ov_rect(sl - 32) : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (fits(rq[u], pw, ph) && kk[u] < best) { best = kk[u]; brect = rq[u]; bslot = s0 + 32 * PACK_WARPS * u; }
+      }
+      uint64_t wk, wr;
+      int ws;
+      warp_first_fit(best, brect, bslot, wk, wr, ws);
+      if (lane == 0) { cand_key[warp] = wk; cand_rect[warp] = wr; cand_slot[warp] = ws; }
+      pack_bar();   // B2: candidates posted
+    }
+  }
+  // placement-invariant pruning bounds: a free area no box fits in (either orientation) is never stored
+  int mA = 1 << 30, mB = 1 << 30;
+  for (int64_t i = lane; i < n; i += 32) {
+    const int bi = a.order[i];
+    const regen_box& bx = a.boxes[bi];
+    const int pw = bx.w + a.gutter, ph = bx.h + a.gutter;
+    mA = min(mA, min(pw, ph));
+    mB = min(mB, max(pw, ph));
+    if (i < PACK_DIMS) {
+      dims[i] = (uint32_t)pw | ((uint32_t)ph << 16);
+      ords[i] = bi;
+    }
+  }
+  mA = __reduce_min_sync(0xffffffffu, mA);
+  mB = __reduce_min_sync(0xffffffffu, mB);
+  __syncwarp();
+  uint64_t rk = ~0ull, rr = 0ull;   // this lane's register slot: empty never fits, never wins
+  const int FW = a.bin_w - 1, FH = a.bin_h + a.gutter;   // a fresh bin's free area (x=1, y=0)
+  int hw = 0;        // live areas: slots [0, hw)
+  int opened = 0;    // bins opened (lazily, in index order)
+  uint32_t seq = 0;
+  int used = 0;
+  bool overflow = false;
+  long long c_scan = 0, c_dec = 0, c_upd = 0, hw_sum = 0;
+  int npw = 0, nph = 0, nb = 0;
+  auto fetch = [&](int64_t oi) {
+    if (oi >= n) return;
+    if (oi < PACK_DIMS) {
+      const uint32_t d = dims[oi];
+      npw = (int)(d & 0xFFFF);
+      nph = (int)(d >> 16);
+      nb = ords[oi];
+    } else {
+      nb = a.order[oi];
+      npw = a.boxes[nb].w + a.gutter;
+      nph = a.boxes[nb].h + a.gutter;
+    }
+  };
+  fetch(0);
+  for (int64_t oi = 0; oi < n; ++oi) {
+    long long t0 = 0;
+    if (a.prof) t0 = clock64();
+    const int pw = npw, ph = nph, b = nb;
+    fetch(oi + 1);   // prefetch: off the dependent chain
+    uint64_t best = fits(rr, pw, ph) ? rk : ~0ull;
+    uint64_t brect = rr;
+    int bslot = lane;
+    const bool big = hw - 32 > PACK_BIG;   // warp-uniform
+    if (big) {
+      if (lane == 0) { task_hw = hw; task_pw = pw; task_ph = ph; }
+      pack_bar();   // B1
+    }
+    // overflow slots: this warp's share (all of them on the single-warp path), 4 loads per lane in flight
+    const int ostride = big ? 32 * PACK_WARPS : 32;
+    for (int s0 = 32 + lane; s0 < hw; s0 += 4 * ostride) {
+      uint64_t kk[4], rq[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int sl = s0 + ostride * u;
+        kk[u] = sl < hw ? ov_key(sl - 32) : ~0ull;
+        rq[u] = sl < hw ? ov_rect(sl - 32) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (fits(rq[u], pw, ph) && kk[u] < best) { best = kk[u]; brect = rq[u]; bslot = s0 + ostride * u; }
+    }
+    long long t1 = 0;
+    if (a.prof) { t1 = clock64(); hw_sum += hw; }
+    // 64-bit warp min as two 32-bit REDUX (bin in the high word, sequence in the low word)
+    uint64_t wkey, wrect;
+    int wslot;
+    warp_first_fit(best, brect, bslot, wkey, wrect, wslot);
+    if (big) {
+      pack_bar();   // B2: the helpers' candidates are posted
+      uint64_t ck = ~0ull, cr = 0;
+      int cs = -1;
+      if (lane == 0) { ck = wkey; cr = wrect; cs = wslot; }
+      else if (lane < PACK_WARPS) { ck = cand_key[lane]; cr = cand_rect[lane]; cs = cand_slot[lane]; }
+      warp_first_fit(ck, cr, cs, wkey, wrect, wslot);
+    }
+    __syncwarp();   // every lane's overflow-slot reads of this box's scan precede lane 0's writes below
+    int fx, fy, fw, fh, bin, slot = -1;
+    bool place = true;
+    if (wkey != ~0ull) {
+      slot = wslot;
+      fx = (int)(wrect & 0xFFFF); fy = (int)((wrect >> 16) & 0xFFFF);
+      fw = (int)((wrect >> 32) & 0xFFFF); fh = (int)(wrect >> 48);
+      bin = (int)(wkey >> 32);
+    } else if (opened < a.max_bins && ((FW >= pw && FH >= ph) || (FW >= ph && FH >= pw))) {
+      bin = opened++;
+      fx = 1; fy = 0; fw = FW; fh = FH;
+    } else {
+      place = false;
+      fx = fy = fw = fh = bin = 0;
+    }
+    long long t2 = 0;
+    if (a.prof) {
+      t2 = clock64();
+      c_scan += t1 - t0;
+      c_dec += t2 - t1;
+    }
+    if (place) {
+      const bool rot = !(fw >= pw && fh >= ph);
+      const int uw = rot ? ph : pw, uh = rot ? pw : ph;
+      used = max(used, bin + 1);
+      if (lane == 0) {   // bin, bx / by, rotated: two 8-B stores
+        int2* pl = reinterpret_cast<int2*>(&a.boxes[b].bin);
+        pl[0] = make_int2(bin, fx);
+        pl[1] = make_int2(fy, rot ? 1 : 0);
+      }
+      // InnerFree (D6): guillotine remainders; vertical = {right full height, bottom}, horizontal =
+      // {bottom full width, right}; the option whose larger remainder is larger wins, ties vertical
+      const int dw = fw - uw, dh = fh - uh;
+      const int64_t v_a = (int64_t)dw * fh, v_b = (int64_t)uw * dh;
+      const int64_t h_a = (int64_t)fw * dh, h_b = (int64_t)dw * uh;
+      const bool vert = max(v_a, v_b) >= max(h_a, h_b);
+      const int rx0 = vert ? fx + uw : fx, ry0 = vert ? fy : fy + uh;
+      const int rw0 = vert ? dw : fw, rh0 = vert ? fh : dh;
+      const int rx1 = vert ? fx : fx + uw, ry1 = vert ? fy + uh : fy;
+      const int rw1 = vert ? uw : dw, rh1 = vert ? dh : uh;
+      int free_slot = slot;   // the consumed area's slot, to be refilled
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int rx = t ? rx1 : rx0, ry = t ? ry1 : ry0, rw = t ? rw1 : rw0, rh = t ? rh1 : rh0;
+        if (rw <= 0 || rh <= 0) continue;
+        const uint32_t sq = seq++;   // sequence numbers follow the oracle's creation order
+        if (min(rw, rh) < mA || max(rw, rh) < mB) continue;   // unusable: never stored
+        int dst;
+        if (free_slot >= 0) { dst = free_slot; free_slot = -1; }
+        else if (hw < a.pool_limit) dst = hw++;
+        else { overflow = true; continue; }
+        const uint64_t nk = ((uint64_t)bin << 32) | sq;
+        const uint64_t nr = (uint64_t)(uint32_t)(rx | (ry << 16)) | ((uint64_t)(uint32_t)(rw | (rh << 16)) << 32);
+        if (dst < 32) {
+          if (lane == dst) { rk = nk; rr = nr; }
+        } else if (lane == 0) {
+          ov_key(dst - 32) = nk;
+          ov_rect(dst - 32) = nr;
+        }
+      }
+      if (free_slot >= 0) {   // nothing refilled the consumed slot: move the last live area into it
+        --hw;
+        if (free_slot != hw) {
+          uint64_t lk, lq;
+          if (hw < 32) {
+            lk = __shfl_sync(0xffffffffu, rk, hw);
+            lq = __shfl_sync(0xffffffffu, rr, hw);
+          } else {
+            lk = ov_key(hw - 32);
+            lq = ov_rect(hw - 32);
+          }
+          if (free_slot < 32) {
+            if (lane == free_slot) { rk = lk; rr = lq; }
+          } else if (lane == 0) {
+            ov_key(free_slot - 32) = lk;
+            ov_rect(free_slot - 32) = lq;
+          }
+        }
+        if (hw < 32 && lane == hw) { rk = ~0ull; rr = 0ull; }   // the vacated register slot is empty
+      }
+    }
+    __syncwarp();   // lane 0's overflow-slot writes are visible to every lane before the next scan
+    if (a.prof) c_upd += clock64() - t2;
+  }
+  if (lane == 0) task_hw = -1;
+  pack_bar();   // release the helper warps
+  if (a.prof && lane == 0)
+    printf("[pack-prof] boxes %lld scan %lld dec %lld upd %lld cycles, mean live areas %.1f, bins %d\n", (long long)n,
+           c_scan, c_dec, c_upd, n ? (double)hw_sum / n : 0.0, used);
+  if (lane == 0) {
+    *a.num_bins = used;
+    if (overflow) atomicOr(a.status, REGEN_ST_FREELIST_OVERFLOW);
+  }
+}
+
 
 // One warp; lane l owns slot l of every bin's free-area list (it alone reads and writes that slot, so
 // the lists need no cross-lane memory ordering). An area fits a box in some orientation iff its
@@ -275,10 +550,10 @@ __device__ __forceinline__ uint32_t warp_max2(uint32_t v) {   // per-half maxima
   return (a << 16) | b;
 }
 
-__global__ void __launch_bounds__(32, 1) pack_kernel(PackArgs a) {
-  __shared__ uint32_t bsum[PACK_MAX_BINS];            // per opened bin
-  __shared__ uint32_t gsum[PACK_MAX_BINS / 32];       // per 32 bins
-  __shared__ uint8_t bcnt[PACK_MAX_BINS];             // live areas per bin
+__device__ void pack_bins(const PackArgs& a, uint8_t* psm) {
+  uint32_t* bsum = (uint32_t*)psm;                    // [PACK_MAX_BINS] per opened bin
+  uint32_t* gsum = bsum + PACK_MAX_BINS;              // [PACK_MAX_BINS / 32] per 32 bins
+  uint8_t* bcnt = (uint8_t*)(gsum + PACK_MAX_BINS / 32);   // [PACK_MAX_BINS] live areas per bin
   const int lane = threadIdx.x;
   const int64_t n = min(*a.num_boxes, a.max_boxes);
   // placement-invariant pruning bounds: a free area no box fits in (either orientation) is never stored
@@ -425,6 +700,15 @@ __global__ void __launch_bounds__(32, 1) pack_kernel(PackArgs a) {
   }
 }
 
+__global__ void __launch_bounds__(32 * PACK_WARPS, 1) pack_kernel(PackArgs a) {
+  extern __shared__ __align__(16) uint8_t psm[];
+  if (min(*a.num_boxes, a.max_boxes) > PACK_BINS_FROM) {
+    if (threadIdx.x < 32) pack_bins(a, psm);
+  } else {
+    pack_pool(a, psm);
+  }
+}
+
 __global__ void owner_fix_kernel(int32_t* owner, int64_t n_mbs, const regen_box* boxes, const int64_t* num_boxes,
                                  int64_t max_boxes) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -441,7 +725,7 @@ static size_t pack_ws(const regen_geom& g, int64_t max_regions, void* base, int3
   int32_t* rc = c.take<int32_t>((size_t)max_regions + 1);
   int64_t* ro = c.take<int64_t>((size_t)max_regions + 1);
   int64_t* nr = c.take<int64_t>(4);
-  uint64_t* rt = c.take<uint64_t>((size_t)PACK_MAX_BINS * PACK_SLOTS);
+  uint64_t* rt = c.take<uint64_t>((size_t)PACK_MAX_BINS * PACK_SLOTS + 2 * (size_t)PACK_POOL);
   uint32_t* sq = c.take<uint32_t>((size_t)PACK_MAX_BINS * PACK_SLOTS);
   if (rcount) *rcount = rc;
   if (roff) *roff = ro;
@@ -550,6 +834,7 @@ extern "C" regen_status regen_pack_regions(const regen_geom* geom, const regen_p
   k.boxes = d_boxes;
   k.rect = rect;
   k.seqv = seqv;
+  k.pool = rect + (size_t)PACK_MAX_BINS * PACK_SLOTS;
   k.order = d_order;
   k.num_boxes = d_num_boxes;
   k.max_boxes = max_boxes;
@@ -564,11 +849,16 @@ extern "C" regen_status regen_pack_regions(const regen_geom* geom, const regen_p
     k.prof = (e && e[0] == '1') ? 1 : 0;
     const char* lim = getenv("REGEN_PACK_POOL_LIMIT");
     k.slot_limit = PACK_SLOTS;
-    if (lim && atoi(lim) > 0) k.slot_limit = std::min(atoi(lim), PACK_SLOTS);
+    k.pool_limit = PACK_POOL + 32;
+    if (lim && atoi(lim) > 0) {
+      k.slot_limit = std::min(atoi(lim), PACK_SLOTS);
+      k.pool_limit = std::min(atoi(lim), PACK_POOL + 32);
+    }
   }
+  REGEN_CUDA(cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PACK_SMEM));
   {
     REGEN_TRACE("pack", s);
-    pack_kernel<<<1, 32, 0, s>>>(k);   // 45 KB of static SMEM: fits beside a resident SR CTA
+    pack_kernel<<<1, 32 * PACK_WARPS, PACK_SMEM, s>>>(k);
   }
   REGEN_LAUNCH_CHECK();
   if (k.prof) {

@@ -104,6 +104,17 @@ def residuals_y(S: int, F: int, H: int, W: int, seed: int = 0, s0: int = 0, scen
     return out
 
 
+def frames_nv12(S: int, F: int, H: int, W: int, seed: int = 0, s0: int = 0) -> np.ndarray:
+    """uint8 [S][F][H*W*3/2] NV12 frames (decoder output): limited-range Y in [16, 235], U/V in [16, 240],
+    uniform random (SR cost is content-agnostic)."""
+    out = np.empty((S, F, H * W * 3 // 2), np.uint8)
+    for s in range(S):
+        rng = _rng(seed, 5, s0 + s)
+        out[s, :, : H * W] = rng.integers(16, 236, size=(F, H * W), dtype=np.uint8)
+        out[s, :, H * W:] = rng.integers(16, 241, size=(F, H * W // 2), dtype=np.uint8)
+    return out
+
+
 @dataclasses.dataclass(frozen=True)
 class SRConfig:
     scale: int

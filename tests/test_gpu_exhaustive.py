@@ -129,11 +129,12 @@ def test_status_box_overflow_truncates_boxes_deterministically():
     np.testing.assert_array_equal(g["owner"], oracle.mb_owner(own, pl))
 
 
-def test_status_freelist_overflow_keeps_a_valid_plan(monkeypatch):
+@pytest.mark.parametrize("F", [3, 30])   # 3 frames: the pool path; 30 frames (5520 boxes): the per-bin path
+def test_status_freelist_overflow_keeps_a_valid_plan(monkeypatch, F):
     rg = _rg()
-    wl = dataclasses.replace(_wl_small(), partition_mb=1)      # Block mode: many boxes, many free areas
+    wl = dataclasses.replace(synth.small(synth.CONFIGS["c2"], F=F), partition_mb=1)   # Block mode: many boxes
     imp_h = synth.importance_maps(wl.S, wl.F, wl.GH, wl.GW, 5, "noisy")
-    monkeypatch.setenv("REGEN_PACK_POOL_LIMIT", "1")         # one live free area per bin
+    monkeypatch.setenv("REGEN_PACK_POOL_LIMIT", "1")         # one live free area (per bin on the bins path)
     p = _make(wl, synth.sr_weights(wl.sr, 0))()
     imp = torch.from_numpy(imp_h).cuda()
     p.select(imp)

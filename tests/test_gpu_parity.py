@@ -118,6 +118,20 @@ def test_index_path_partition_sizes(P):
     _assert_index_equal(g, o)
 
 
+@pytest.mark.parametrize("cfg,F,P,pct,kind", [("c2", 30, 1, 20.0, "blobs"),     # 5520 boxes (Block mode)
+                                              ("c5", 14, 4, 50.0, "blobs"),     # 720p 50%: ~5.8k boxes, ~2.3k bins
+                                              ("c4g", 30, 2, 15.0, "noisy")])
+def test_index_path_large_pools_bit_exact(cfg, F, P, pct, kind):
+    """Beyond PACK_BINS_FROM boxes the packer switches to per-bin area lists with dominance summaries
+    (pack.cu pack_bins); placements stay bit-exact against the oracle's linear first-fit scan."""
+    wl = dataclasses.replace(synth.small(synth.CONFIGS[cfg], F=F), partition_mb=P, pct=pct)
+    imp = synth.importance_maps(wl.S, wl.F, wl.GH, wl.GW, 17, kind)
+    _, g = _run_index(wl, imp, synth.sr_weights(wl.sr, 0))
+    o = _oracle_index(wl, imp)
+    assert len(o["boxes"]) > 5000
+    _assert_index_equal(g, o)
+
+
 def test_index_path_small_max_bins_leaves_unplaced():
     wl = dataclasses.replace(synth.small(synth.CONFIGS["c2"], F=3), max_bins=5)
     imp = synth.importance_maps(wl.S, wl.F, wl.GH, wl.GW, 2)
