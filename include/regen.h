@@ -328,7 +328,8 @@ REGEN_API regen_status regen_reuse_importance(const regen_geom* geom, const floa
  * ------------------------------------------------------------------------------------------- */
 REGEN_API regen_status regen_nv12_to_rgb8(const regen_geom* geom, const uint8_t* d_nv12, uint8_t* d_rgb8, void* stream);
 
-/* Workspace bytes for a call (which = REGEN_CALL_*; params = the call's params struct;
+/* Workspace bytes for a call (which = REGEN_CALL_*; params = the call's params struct — for PACK,
+ * NULL sizes the default guillotine packer, the pack params add a placement policy's per-bin state;
  * sr = SR handle for ENHANCE, else NULL). */
 REGEN_API regen_status regen_workspace_size(int32_t which, const regen_geom* geom, const void* params, const void* sr,
                                   size_t* bytes);

@@ -117,16 +117,31 @@ def sort(bx: np.ndarray, density: np.ndarray, policy: int = ORDER_DENSITY) -> np
     return order[: len(bx)].copy()
 
 
-def pack(bx: np.ndarray, order: np.ndarray, bin_w: int, bin_h: int, max_bins: int, gutter: int = 1):
-    """O5b (Alg.1 l.7-21, Alg.2): placement int32 [n][4] (bin,bx,by,rot), num_bins."""
+POLICY_GUILLOTINE, POLICY_MAXRECT, POLICY_SKYLINE, POLICY_SHELF = 0, 1, 2, 3
+_PACK_FN = {POLICY_GUILLOTINE: "ref_pack", POLICY_MAXRECT: "ref_pack_maxrect", POLICY_SKYLINE: "ref_pack_skyline",
+            POLICY_SHELF: "ref_pack_shelf"}
+
+
+def pack(bx: np.ndarray, order: np.ndarray, bin_w: int, bin_h: int, max_bins: int, gutter: int = 1,
+         policy: int = POLICY_GUILLOTINE):
+    """O5b (Alg.1 l.7-21, Alg.2): placement int32 [n][4] (bin,bx,by,rot), num_bins. policy: the
+    guillotine reading (D6), or MAXRECT (D14), SKYLINE (D15), SHELF (D16)."""
     bx = np.ascontiguousarray(bx, np.int32)
     order = np.ascontiguousarray(order, np.int32)
     pl = np.zeros((max(len(bx), 1), 4), np.int32)
     nb = ctypes.c_int32(0)
-    rc = lib().ref_pack(ctypes.c_int64(len(bx)), _p(bx), _p(order), bin_w, bin_h, max_bins, gutter, _p(pl),
-                        ctypes.byref(nb))
+    rc = getattr(lib(), _PACK_FN[policy])(ctypes.c_int64(len(bx)), _p(bx), _p(order), bin_w, bin_h, max_bins,
+                                          gutter, _p(pl), ctypes.byref(nb))
     assert rc == 0
     return pl[: len(bx)].copy(), int(nb.value)
+
+
+def max_empty_rect(occ: np.ndarray) -> tuple[int, int, int, int]:
+    """Alg. 2 (reading D14) on a [Hg][W] occupancy grid (nonzero = used): (x, y, w, h)."""
+    o = np.ascontiguousarray(occ != 0, np.uint8)
+    out = np.zeros(4, np.int32)
+    lib().ref_max_empty_rect(_p(o), o.shape[1], o.shape[0], _p(out))
+    return tuple(int(v) for v in out)
 
 
 def inner_free(fw: int, fh: int, uw: int, uh: int) -> list[tuple[int, int, int, int]]:
@@ -257,13 +272,14 @@ def scatter(frames: np.ndarray, bx: np.ndarray, placement: np.ndarray, owner: np
 def index_path(importance: np.ndarray, W: int, H: int, k: int, *, mode: int = MODE_TOPK, tau: float = 0.0,
                scope: int = SCOPE_GLOBAL, conn: int = 8, expand: int = 3, partition_mb: int = 4,
                bin_w: int = 128, bin_h: int = 128, max_bins: int = 4096, gutter: int = 1,
-               order_policy: int = ORDER_DENSITY, cap: int = -1, density_mode: int = DENSITY_SPAN) -> dict:
+               order_policy: int = ORDER_DENSITY, cap: int = -1, density_mode: int = DENSITY_SPAN,
+               policy: int = POLICY_GUILLOTINE) -> dict:
     """Selection -> regions -> boxes -> sort -> pack, in Alg. 1's order."""
     sel = select(importance, W, H, mode, k, tau, scope, cap=cap)
     labels, regs = regions(sel, W, H, conn)
     bx, dens, box_of = boxes(importance, labels, regs, W, H, expand, partition_mb, density_mode=density_mode)
     order = sort(bx, dens, order_policy)
-    pl, nbins = pack(bx, order, bin_w, bin_h, max_bins, gutter)
+    pl, nbins = pack(bx, order, bin_w, bin_h, max_bins, gutter, policy)
     return dict(sel=sel, labels=labels, regions=regs, boxes=bx, density=dens, box_of_mb=box_of,
                 order=order, placement=pl, num_bins=nbins, owner=mb_owner(box_of, pl))
 

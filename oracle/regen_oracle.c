@@ -776,3 +776,196 @@ int ref_nv12_to_rgb8(int64_t frames, int W, int H, const uint8_t* nv12, uint8_t*
   }
   return 0;
 }
+
+/* ------------------------------------------------------------------------------------------ */
+/* f1. Placement policies beside the guillotine reading. Common frame: a bin is  */
+/* W columns x (H + g) rows, column 0 reserved (D8); a box needs a (w+g) x (h+g) footprint,      */
+/* (h+g) x (w+g) when rotated; boxes are taken in the given order; bins are opened lazily in     */
+/* index order; RotatePacking prefers the unrotated footprint; placement record as   */
+/* ref_pack; a box that fits nowhere is unplaced.                                                */
+/* ------------------------------------------------------------------------------------------ */
+
+/* Alg. 2 InnerFree read literally (D14): the maximal empty rectangle of a bin's free cells.     */
+/* left[y][x] = free cells ending at (x, y) going left; for each column x (Alg. 2's outer loop   */
+/* over j), the largest rectangle under the histogram left[.][x] by the monotone stack (pop      */
+/* while left[top] >= left[y]: down[top] = y; up[y] = top); the first maximal area in (x, y)     */
+/* order wins. occ: [Hg][W] bytes, 1 = used. out: x, y, w, h (all 0 if the bin is full).         */
+void ref_max_empty_rect(const uint8_t* occ, int W, int Hg, int32_t* out) {
+  int* left = (int*)malloc(sizeof(int) * (size_t)W * Hg);
+  int* up = (int*)malloc(sizeof(int) * (size_t)Hg);
+  int* down = (int*)malloc(sizeof(int) * (size_t)Hg);
+  int* stk = (int*)malloc(sizeof(int) * (size_t)Hg);
+  for (int y = 0; y < Hg; ++y)
+    for (int x = 0; x < W; ++x)
+      left[y * W + x] = occ[(int64_t)y * W + x] ? 0 : (x > 0 ? left[y * W + x - 1] : 0) + 1;
+  int64_t best = 0;
+  out[0] = out[1] = out[2] = out[3] = 0;
+  for (int x = 0; x < W; ++x) {
+    int top = 0;
+    for (int y = 0; y < Hg; ++y) {
+      up[y] = -1;
+      down[y] = Hg;
+    }
+    for (int y = 0; y < Hg; ++y) {
+      while (top > 0 && left[stk[top - 1] * W + x] >= left[y * W + x]) down[stk[--top]] = y;
+      up[y] = top > 0 ? stk[top - 1] : -1;
+      stk[top++] = y;
+    }
+    for (int y = 0; y < Hg; ++y) {
+      const int l = left[y * W + x];
+      const int64_t area = (int64_t)(down[y] - up[y] - 1) * l;
+      if (area > best) {
+        best = area;
+        out[0] = x - l + 1; out[1] = up[y] + 1; out[2] = l; out[3] = down[y] - up[y] - 1;
+      }
+    }
+  }
+  free(left); free(up); free(down); free(stk);
+}
+
+static void pack_init_placement(int64_t n, int32_t* placement) {
+  for (int64_t i = 0; i < n; ++i)
+    placement[4 * i] = -1, placement[4 * i + 1] = 0, placement[4 * i + 2] = 0, placement[4 * i + 3] = 0;
+}
+
+int ref_pack_maxrect(int64_t num_boxes, const int32_t* boxes, const int32_t* order, int bin_w, int bin_h,
+                     int max_bins, int gutter, int32_t* placement, int32_t* num_bins) {
+  const int W = bin_w, Hg = bin_h + gutter;
+  uint8_t* occ = (uint8_t*)calloc((size_t)(max_bins > 0 ? max_bins : 1) * W * Hg, 1);
+  int32_t* mer = (int32_t*)malloc(sizeof(int32_t) * 4 * (size_t)(max_bins > 0 ? max_bins : 1));
+  int opened = 0, used = 0;
+  pack_init_placement(num_boxes, placement);
+  for (int64_t oi = 0; oi < num_boxes; ++oi) {
+    const int32_t b = order[oi];
+    const int pw = boxes[12 * b + 8] + gutter, ph = boxes[12 * b + 9] + gutter;
+    int bin = -1;
+    for (int k = 0; k <= opened && k < max_bins; ++k) {   /* freeareas: one MER per bin, bin order */
+      if (k == opened) {                                  /* open the next bin lazily */
+        uint8_t* o = occ + (size_t)k * W * Hg;
+        for (int y = 0; y < Hg; ++y) o[(int64_t)y * W] = 1;   /* reserved column 0 */
+        ref_max_empty_rect(o, W, Hg, mer + 4 * k);
+      }
+      const int fw = mer[4 * k + 2], fh = mer[4 * k + 3];
+      if ((fw >= pw && fh >= ph) || (fw >= ph && fh >= pw)) { bin = k; break; }
+      if (k == opened) break;                             /* not even a fresh bin admits it */
+    }
+    if (bin < 0) continue;
+    if (bin == opened) ++opened;
+    const int32_t* r = mer + 4 * bin;
+    const int rot = !(r[2] >= pw && r[3] >= ph);
+    const int uw = rot ? ph : pw, uh = rot ? pw : ph;
+    placement[4 * b] = bin; placement[4 * b + 1] = r[0]; placement[4 * b + 2] = r[1]; placement[4 * b + 3] = rot;
+    if (bin + 1 > used) used = bin + 1;
+    uint8_t* o = occ + (size_t)bin * W * Hg;
+    for (int y = r[1]; y < r[1] + uh; ++y)
+      for (int x = r[0]; x < r[0] + uw; ++x) o[(int64_t)y * W + x] = 1;
+    ref_max_empty_rect(o, W, Hg, mer + 4 * bin);            /* Update: the bin's new free area */
+  }
+  free(occ);
+  free(mer);
+  *num_bins = used;
+  return 0;
+}
+
+/* D15 skyline bottom-left: a bin's skyline is the height of the used part of every column      */
+/* (column 0 reserved: full). A footprint uw x uh can rest at x (1 <= x, x + uw <= W) at          */
+/* y = max height over [x, x+uw), if y + uh <= H + g; the lowest y wins, then the leftmost x. In  */
+/* the first bin (index order) that admits the box: the best unrotated position if there is one, */
+/* else the best rotated one; the columns under the footprint rise to y + uh.                    */
+static int sky_best(const int32_t* hgt, int W, int Hg, int uw, int uh, int* bx, int* by) {
+  int found = 0;
+  for (int x = 1; x + uw <= W; ++x) {
+    int y = 0;
+    for (int c = x; c < x + uw; ++c) y = hgt[c] > y ? hgt[c] : y;
+    if (y + uh > Hg) continue;
+    if (!found || y < *by || (y == *by && x < *bx)) { *bx = x; *by = y; found = 1; }
+  }
+  return found;
+}
+
+int ref_pack_skyline(int64_t num_boxes, const int32_t* boxes, const int32_t* order, int bin_w, int bin_h,
+                     int max_bins, int gutter, int32_t* placement, int32_t* num_bins) {
+  const int W = bin_w, Hg = bin_h + gutter;
+  int32_t* hgt = (int32_t*)calloc((size_t)(max_bins > 0 ? max_bins : 1) * W, sizeof(int32_t));
+  int opened = 0, used = 0;
+  pack_init_placement(num_boxes, placement);
+  for (int64_t oi = 0; oi < num_boxes; ++oi) {
+    const int32_t b = order[oi];
+    const int pw = boxes[12 * b + 8] + gutter, ph = boxes[12 * b + 9] + gutter;
+    for (int k = 0; k <= opened && k < max_bins; ++k) {
+      int32_t* h = hgt + (size_t)k * W;
+      if (k == opened) h[0] = Hg;                          /* fresh bin: column 0 reserved */
+      int x = 0, y = 0, rot = 0;
+      if (sky_best(h, W, Hg, pw, ph, &x, &y)) rot = 0;
+      else if (sky_best(h, W, Hg, ph, pw, &x, &y)) rot = 1;
+      else {
+        if (k == opened) break;
+        continue;
+      }
+      if (k == opened) ++opened;
+      const int uw = rot ? ph : pw, uh = rot ? pw : ph;
+      for (int c = x; c < x + uw; ++c) h[c] = y + uh;
+      placement[4 * b] = k; placement[4 * b + 1] = x; placement[4 * b + 2] = y; placement[4 * b + 3] = rot;
+      if (k + 1 > used) used = k + 1;
+      break;
+    }
+  }
+  free(hgt);
+  *num_bins = used;
+  return 0;
+}
+
+/* D16 first-fit shelves: a bin holds shelves (y0, height, end x) in creation order and the y of   */
+/* its next shelf. A box goes on the first shelf (bin order, then shelf order) where it fits      */
+/* unrotated (height <= shelf height, end + width <= W), else rotated; otherwise, in the same    */
+/* bin, on a new shelf at the bin's next y if the bin has the height (unrotated preferred; the    */
+/* new shelf's height is the box's); otherwise the next bin. Shelves start at x = 1 (column 0).  */
+#define SHELF_CAP 256
+int ref_pack_shelf(int64_t num_boxes, const int32_t* boxes, const int32_t* order, int bin_w, int bin_h,
+                   int max_bins, int gutter, int32_t* placement, int32_t* num_bins) {
+  const int W = bin_w, Hg = bin_h + gutter;
+  const size_t nb = (size_t)(max_bins > 0 ? max_bins : 1);
+  int32_t* sy = (int32_t*)malloc(sizeof(int32_t) * nb * SHELF_CAP);
+  int32_t* sh = (int32_t*)malloc(sizeof(int32_t) * nb * SHELF_CAP);
+  int32_t* sx = (int32_t*)malloc(sizeof(int32_t) * nb * SHELF_CAP);
+  int32_t* ns = (int32_t*)calloc(nb, sizeof(int32_t));
+  int32_t* top = (int32_t*)calloc(nb, sizeof(int32_t));
+  int opened = 0, used = 0, rc = 0;
+  pack_init_placement(num_boxes, placement);
+  for (int64_t oi = 0; oi < num_boxes; ++oi) {
+    const int32_t b = order[oi];
+    const int pw = boxes[12 * b + 8] + gutter, ph = boxes[12 * b + 9] + gutter;
+    for (int k = 0; k <= opened && k < max_bins; ++k) {
+      int px = -1, py = 0, rot = 0;
+      for (int s = 0; s < ns[k] && px < 0; ++s) {
+        const size_t i = (size_t)k * SHELF_CAP + s;
+        if (ph <= sh[i] && sx[i] + pw <= W) { px = sx[i]; py = sy[i]; rot = 0; sx[i] += pw; }
+        else if (pw <= sh[i] && sx[i] + ph <= W) { px = sx[i]; py = sy[i]; rot = 1; sx[i] += ph; }
+      }
+      if (px < 0 && ns[k] < SHELF_CAP) {
+        int hh = 0, ww = 0;
+        if (top[k] + ph <= Hg && 1 + pw <= W) { hh = ph; ww = pw; rot = 0; }
+        else if (top[k] + pw <= Hg && 1 + ph <= W) { hh = pw; ww = ph; rot = 1; }
+        if (hh > 0) {
+          const size_t i = (size_t)k * SHELF_CAP + ns[k]++;
+          sy[i] = top[k]; sh[i] = hh; sx[i] = 1 + ww;
+          px = 1; py = top[k];
+          top[k] += hh;
+        }
+      } else if (px < 0) {
+        rc = 2;   /* shelf table full */
+      }
+      if (px < 0) {
+        if (k == opened) break;
+        continue;
+      }
+      if (k == opened) ++opened;
+      placement[4 * b] = k; placement[4 * b + 1] = px; placement[4 * b + 2] = py; placement[4 * b + 3] = rot;
+      if (k + 1 > used) used = k + 1;
+      break;
+    }
+  }
+  free(sy); free(sh); free(sx); free(ns); free(top);
+  *num_bins = used;
+  return rc;
+}

@@ -336,7 +336,7 @@ class Pipeline:
         self.order = torch.empty(self.max_boxes, dtype=i32, device=dev)
         self.owner = torch.empty(self.n_mbs, dtype=i32, device=dev)
         # the workspace of the calls run() makes; the separate enhance call (HR bins) grows it on first use
-        ws = max(workspace_size(CALL_SELECT, self.geom), workspace_size(CALL_PACK, self.geom),
+        ws = max(workspace_size(CALL_SELECT, self.geom), workspace_size(CALL_PACK, self.geom, self.pack),
                  workspace_size(CALL_ENHANCE_SCATTER, self.geom, self.pack, self.sr.handle))
         self.ws = torch.empty(ws, dtype=u8, device=dev)
         self.hr_dtype = DTYPE_BF16 if bf16 else DTYPE_FP32

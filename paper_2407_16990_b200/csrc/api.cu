@@ -23,7 +23,7 @@ regen_status validate_geom(const regen_geom* g) {
 }
 
 size_t select_workspace_bytes(const regen_geom& g);
-size_t pack_workspace_bytes(const regen_geom& g, int64_t max_regions);
+size_t pack_workspace_bytes(const regen_geom& g, int64_t max_regions, const regen_pack_params* p);
 size_t enhance_scatter_ws_bytes(const SRNet* net, const regen_pack_params& p);
 size_t temporal_workspace_bytes(const regen_geom& g);
 
@@ -41,7 +41,7 @@ extern "C" regen_status regen_workspace_size(int32_t which, const regen_geom* ge
       *bytes = select_workspace_bytes(*geom);
       return REGEN_OK;
     case REGEN_CALL_PACK:
-      *bytes = pack_workspace_bytes(*geom, n_mbs(*geom));
+      *bytes = pack_workspace_bytes(*geom, n_mbs(*geom), (const regen_pack_params*)params);
       return REGEN_OK;
     case REGEN_CALL_ENHANCE: {
       REGEN_REQUIRE(params && sr, "ENHANCE needs pack params and the SR handle");

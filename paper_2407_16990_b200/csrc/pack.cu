@@ -19,6 +19,10 @@
 namespace regen {
 
 size_t select_workspace_bytes(const regen_geom& g);
+size_t policy_workspace_bytes(const regen_pack_params& p);
+regen_status launch_pack_policy(const regen_pack_params& p, regen_box* d_boxes, const int32_t* d_order,
+                                const int64_t* d_num_boxes, int64_t max_boxes, int32_t* d_num_bins,
+                                int32_t* d_status, void* ws, cudaStream_t s);
 
 // ------------------------------------------------------------------------------------ boxes
 
@@ -736,8 +740,10 @@ static size_t pack_ws(const regen_geom& g, int64_t max_regions, void* base, int3
   return c.off + 256;
 }
 
-size_t pack_workspace_bytes(const regen_geom& g, int64_t max_regions) {
-  return pack_ws(g, max_regions, nullptr, nullptr, nullptr, nullptr);
+// the guillotine packer's state, plus a placement policy's per-bin state when params name one
+size_t pack_workspace_bytes(const regen_geom& g, int64_t max_regions, const regen_pack_params* p) {
+  const size_t base = (pack_ws(g, max_regions, nullptr, nullptr, nullptr, nullptr) + 255) / 256 * 256;
+  return p && p->policy != REGEN_POLICY_GUILLOTINE ? base + policy_workspace_bytes(*p) : base;
 }
 
 }  // namespace regen
@@ -761,14 +767,15 @@ extern "C" regen_status regen_pack_regions(const regen_geom* geom, const regen_p
   REGEN_REQUIRE(p->order == REGEN_ORDER_DENSITY || p->order == REGEN_ORDER_AREA || p->order == REGEN_ORDER_HEIGHT,
                 "bad order");
   REGEN_REQUIRE(p->density == REGEN_DENSITY_SPAN || p->density == REGEN_DENSITY_MEMBERS, "bad density mode");
-  REGEN_REQUIRE(p->policy == REGEN_POLICY_GUILLOTINE, "policy %d not built", p->policy);
+  REGEN_REQUIRE(p->policy >= REGEN_POLICY_GUILLOTINE && p->policy <= REGEN_POLICY_SHELF, "bad policy %d", p->policy);
   REGEN_REQUIRE(d_importance && d_labels && d_num_regions && d_num_boxes && d_num_bins && d_mb_owner && d_status,
                 "null device pointer");
   REGEN_REQUIRE(max_boxes >= 1 && max_boxes < (1ll << 31) && d_boxes && d_order, "bad boxes buffer");
   const regen_geom g = *geom;
   // the region capacity is implied by the labels: at most one region per MB
   const int64_t max_regions = n_mbs(g);
-  REGEN_REQUIRE(ws_bytes >= pack_workspace_bytes(g, max_regions) && d_ws, "workspace too small");
+  REGEN_REQUIRE(ws_bytes >= pack_workspace_bytes(g, max_regions, p) && d_ws, "workspace too small (%zu < %zu)",
+                ws_bytes, pack_workspace_bytes(g, max_regions, p));
   cudaStream_t s = (cudaStream_t)stream;
   int32_t* rcount;
   int64_t *roff, *nreg;
@@ -855,8 +862,12 @@ extern "C" regen_status regen_pack_regions(const regen_geom* geom, const regen_p
       k.pool_limit = std::min(atoi(lim), PACK_POOL + 32);
     }
   }
-  REGEN_CUDA(cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PACK_SMEM));
-  {
+  if (p->policy != REGEN_POLICY_GUILLOTINE) {   // SURVEY §8(f)1 comparison policies (pack_policies.cu)
+    void* pws = (uint8_t*)d_ws + (pack_ws(g, max_regions, nullptr, nullptr, nullptr, nullptr) + 255) / 256 * 256;
+    regen_status ps = launch_pack_policy(*p, d_boxes, d_order, d_num_boxes, max_boxes, d_num_bins, d_status, pws, s);
+    if (ps != REGEN_OK) return ps;
+  } else {
+    REGEN_CUDA(cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PACK_SMEM));
     REGEN_TRACE("pack", s);
     pack_kernel<<<1, 32 * PACK_WARPS, PACK_SMEM, s>>>(k);
   }

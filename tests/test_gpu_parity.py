@@ -107,6 +107,28 @@ def test_index_path_bit_exact(name, kind, kw):
     _assert_index_equal(g, o)
 
 
+POLICY_CASES = [(pol, name, kind, extra) for pol in (1, 2, 3)
+                for name, kind, extra in [("c2f4", "blobs", {}), ("c2f4", "noisy", {}), ("c3f2", "blobs", {}),
+                                          ("c1", "blobs", {}), ("c2f4", "noisy", {"max_bins": 6})]] + \
+               [(3, "c2f4", "blobs", {"order": 2}), (2, "c2f4", "levels", {"order": 1})]
+
+
+@pytest.mark.parametrize("policy,name,kind,extra", POLICY_CASES)
+def test_index_path_policies_bit_exact(policy, name, kind, extra):
+    """MAXRECT (literal Alg. 2, D14), SKYLINE (D15) and SHELF (D16) placements on the GPU
+    (pack_policies.cu) equal the oracle's, including unplaced boxes when the bins run out."""
+    wl = _wl(name)
+    if "max_bins" in extra:
+        wl = dataclasses.replace(wl, max_bins=extra["max_bins"])
+    imp = synth.importance_maps(wl.S, wl.F, wl.GH, wl.GW, 19, kind)
+    order = extra.get("order", 0)
+    _, g = _run_index(wl, imp, synth.sr_weights(wl.sr, 0), policy=policy, order=order)
+    o = _oracle_index(wl, imp, policy=policy, order_policy=order)
+    if "max_bins" in extra:
+        assert (o["placement"][:, 0] < 0).any()
+    _assert_index_equal(g, o)
+
+
 @pytest.mark.parametrize("P", [1, 2, 7])
 def test_index_path_partition_sizes(P):
     """Block mode (partition_mb = 1: every selected MB its own box, SURVEY §8(f)1 'Block') and the
