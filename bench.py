@@ -329,17 +329,16 @@ def main() -> None:
         # two pipelines (double-buffered state): the index path (select + pack) of batch k+1 on one CUDA
         # stream while the SR (enhance + scatter) of batch k runs on another (schedule.py: the same
         # runner the full-size parity tests drive); a rank with several groups cycles through them
-        # a rank with several selection groups keeps up to 4 pipelines and runs the index paths of up
-        # to 3 groups at once (each packer on its own SM); memory permitting (REGEN_PIPES / REGEN_FRONTS
-        # override, A/B aids)
-        n_pipes = 2
-        if G > 1:
-            free0 = torch.cuda.mem_get_info(dev)[0]
-            probe = make_pipe()
-            per_pipe = max(1, free0 - torch.cuda.mem_get_info(dev)[0])
-            del probe
-            torch.cuda.empty_cache()
-            n_pipes = int(max(2, min(4, G, (0.7 * torch.cuda.mem_get_info(dev)[0]) // per_pipe)))
+        # up to 4 pipelines, the index paths of up to 3 batches (consecutive groups, or consecutive chunks of
+        # one group) in flight at once, each packer on its own SM, so that a sequential packer that is
+        # slower than a batch's SR (8-stream groups) does not bound the step; memory permitting
+        # (REGEN_PIPES / REGEN_FRONTS override, A/B aids)
+        free0 = torch.cuda.mem_get_info(dev)[0]
+        probe = make_pipe()
+        per_pipe = max(1, free0 - torch.cuda.mem_get_info(dev)[0])
+        del probe
+        torch.cuda.empty_cache()
+        n_pipes = int(max(2, min(4, (0.7 * torch.cuda.mem_get_info(dev)[0]) // per_pipe)))
         n_pipes = int(os.environ.get("REGEN_PIPES", n_pipes))
         n_front = int(os.environ.get("REGEN_FRONTS", max(1, n_pipes - 1)))
         runner = PipelinedRunner(make_pipe, dev, bilinear=os.environ.get("REGEN_BILINEAR", "side"), nv12=nv12,

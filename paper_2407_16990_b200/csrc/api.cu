@@ -24,7 +24,7 @@ regen_status validate_geom(const regen_geom* g) {
 
 size_t select_workspace_bytes(const regen_geom& g);
 size_t pack_workspace_bytes(const regen_geom& g, int64_t max_regions, const regen_pack_params* p);
-size_t enhance_scatter_ws_bytes(const SRNet* net, const regen_pack_params& p);
+size_t enhance_scatter_ws_bytes(const SRNet* net, const regen_pack_params& p, int64_t box_cap);
 size_t temporal_workspace_bytes(const regen_geom& g);
 
 }  // namespace regen
@@ -47,7 +47,7 @@ extern "C" regen_status regen_workspace_size(int32_t which, const regen_geom* ge
       REGEN_REQUIRE(params && sr, "ENHANCE needs pack params and the SR handle");
       const regen_pack_params* p = (const regen_pack_params*)params;
       REGEN_REQUIRE(p->max_bins >= 1 && p->bin_w >= 4 && p->bin_h >= 1, "bad bin geometry");
-      *bytes = enhance_bufs((const SRNet*)sr, *p, nullptr).bytes;
+      *bytes = enhance_bufs((const SRNet*)sr, *p, nullptr, false, n_mbs(*geom)).bytes;
       return REGEN_OK;
     }
     case REGEN_CALL_SCATTER:
@@ -60,7 +60,7 @@ extern "C" regen_status regen_workspace_size(int32_t which, const regen_geom* ge
       REGEN_REQUIRE(params && sr, "ENHANCE_SCATTER needs pack params and the SR handle");
       const regen_pack_params* p = (const regen_pack_params*)params;
       REGEN_REQUIRE(p->max_bins >= 1 && p->bin_w >= 4 && p->bin_h >= 1, "bad bin geometry");
-      *bytes = enhance_scatter_ws_bytes((const SRNet*)sr, *p);
+      *bytes = enhance_scatter_ws_bytes((const SRNet*)sr, *p, n_mbs(*geom));
       return REGEN_OK;
     }
     default:

@@ -304,6 +304,122 @@ __global__ void gather_kernel(const uint8_t* frames, const regen_box* boxes, con
   }
 }
 
+// One-pass stitch (bins of width % 32 == 0, <= 1024): per-bin box lists (count, scan, fill), then a
+// CTA per band of STITCH_BAND rows of a bin paints the band's box ids into SMEM from its bin's list and
+// writes every pixel of the band once: map, the owned-pixel frame destination, the packed input
+// (gather, D7 rotation, u8/255 -> bf16/fp32, D9) and the occupancy bits. Replaces clear + paint +
+// gather (which wrote map and dst twice and read map back).
+constexpr int STITCH_BAND = 8;
+
+__global__ void bin_count_kernel(const regen_box* boxes, const int64_t* num_boxes, int64_t max_boxes, int32_t* cnt) {
+  const int64_t nb = min(*num_boxes, max_boxes);
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    const int bin = boxes[b].bin;
+    if (bin >= 0) atomicAdd(cnt + bin, 1);
+  }
+}
+
+__global__ void __launch_bounds__(1024) bin_scan_kernel(const int32_t* num_bins, int max_bins, int32_t* cnt,
+                                                        int32_t* off) {
+  __shared__ int scratch[33];
+  const int n = min(*num_bins, max_bins);
+  int carry = 0;
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const int c = i < n ? cnt[i] : 0;
+    int tot;
+    const int ex = block_exclusive_scan(c, scratch, &tot);
+    if (i < n) { off[i] = carry + ex; cnt[i] = carry + ex; }   // cnt becomes the fill cursor
+    carry += tot;
+  }
+  if (threadIdx.x == 0) off[n] = carry;
+}
+
+__global__ void bin_fill_kernel(const regen_box* boxes, const int64_t* num_boxes, int64_t max_boxes, int32_t* cur,
+                                int32_t* list) {
+  const int64_t nb = min(*num_boxes, max_boxes);
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    const int bin = boxes[b].bin;
+    if (bin >= 0) list[atomicAdd(cur + bin, 1)] = (int32_t)b;
+  }
+}
+
+template <typename T, int LAYOUT>
+__global__ void __launch_bounds__(256) stitch_band_kernel(const uint8_t* frames, const regen_box* boxes,
+                                                          const int32_t* off, const int32_t* list,
+                                                          const int32_t* num_bins, int max_bins, int bin_w, int bin_h,
+                                                          int F, int W, int H, int32_t* map, T* out, uint32_t* mbits,
+                                                          OwnArgs oa) {
+  extern __shared__ int32_t band_ids[];   // [STITCH_BAND][bin_w]
+  const int nbands = (bin_h + STITCH_BAND - 1) / STITCH_BAND;
+  const int items = min(*num_bins, max_bins) * nbands;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const int npx = STITCH_BAND * bin_w;
+  const int words = bin_w / 32;
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    const int bin = item / nbands, y0 = (item - bin * nbands) * STITCH_BAND;
+    const int rows = min(STITCH_BAND, bin_h - y0);
+    for (int i = threadIdx.x; i < npx; i += blockDim.x) band_ids[i] = -1;
+    __syncthreads();
+    // paint: a warp per box of this bin, its footprint rows inside the band
+    for (int j = off[bin] + warp; j < off[bin + 1]; j += nwarps) {
+      const int id = list[j];
+      const regen_box& bx = boxes[id];
+      const int fw = bx.rotated ? bx.h : bx.w, fh = bx.rotated ? bx.w : bx.h;
+      const int ra = max(bx.by, y0), rb = min(bx.by + fh, y0 + rows);
+      for (int r = ra; r < rb; ++r)
+        for (int p = lane; p < fw; p += 32) band_ids[(r - y0) * bin_w + bx.bx + p] = id;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < rows * bin_w; i += blockDim.x) {
+      const int yy = i / bin_w, x = i - yy * bin_w, y = y0 + yy;
+      const int32_t id = band_ids[i];
+      const size_t px = ((size_t)bin * bin_h + y) * bin_w + x;
+      if (mbits != nullptr) {   // bin_w % 32 == 0: a warp covers 32 consecutive pixels of one row
+        const uint32_t bits = __ballot_sync(0xffffffffu, id >= 0);
+        if (lane == 0) mbits[((size_t)bin * bin_h + y) * words + x / 32] = bits;
+      }
+      map[px] = id;
+      float v[3] = {0.f, 0.f, 0.f};
+      int64_t d = -1;
+      if (id >= 0) {
+        const regen_box& bx = boxes[id];
+        const int p = x - bx.bx, q = y - bx.by;
+        const int sx = bx.rotated ? bx.x0 + q : bx.x0 + p;
+        const int sy = bx.rotated ? bx.y0 + bx.h - 1 - p : bx.y0 + q;
+        const uint8_t* src = frames + ((((int64_t)bx.stream * F + bx.frame) * H + sy) * W + sx) * 3;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[c] = __fdiv_rn((float)src[c], 255.0f);
+        if (oa.owner) {
+          const int32_t* ow = oa.owner + ((size_t)bx.stream * oa.F + bx.frame) * oa.GH * oa.GW;
+          if (ow[(sy / oa.mb) * oa.GW + sx / oa.mb] == id) {
+            const int64_t OW = (int64_t)oa.W * oa.s, OH = (int64_t)oa.H * oa.s;
+            d = ((((int64_t)bx.stream * oa.F + bx.frame) * OH + (int64_t)oa.s * sy) * OW + (int64_t)oa.s * sx) |
+                ((int64_t)bx.rotated << 62);
+          }
+        }
+      }
+      if (oa.owner) oa.dst[px] = d;
+      if (LAYOUT == 0) {
+        T* o = out + px * 8;
+        if (sizeof(T) == 2) {
+          const __nv_bfloat162 h01 = __floats2bfloat162_rn(v[0], v[1]), h2 = __floats2bfloat162_rn(v[2], 0.f);
+          *reinterpret_cast<uint4*>(o) = make_uint4(*reinterpret_cast<const uint32_t*>(&h01),
+                                                    *reinterpret_cast<const uint32_t*>(&h2), 0u, 0u);
+        } else {
+          reinterpret_cast<float4*>(o)[0] = make_float4(v[0], v[1], v[2], 0.f);
+          reinterpret_cast<float4*>(o)[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      } else {
+        T* o = out + px * 4;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) o[c] = to_t<T>(c < 3 ? v[c] : 0.0f);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------------------------------ SIMT conv
 
 struct SimtArgs {
@@ -428,7 +544,7 @@ regen_status conv_simt_launch(const SRNet* net, const ConvDesc& cv, const void* 
 
 // frames_out: the buffers of the frame-output calls (regen_enhance_scatter / _owned); with the fused
 // fold + combine the HR-resolution partial-sum buffer `u` is never touched and is not carved
-EnhanceBufs enhance_bufs(const SRNet* net, const regen_pack_params& p, void* base, bool frames_out) {
+EnhanceBufs enhance_bufs(const SRNet* net, const regen_pack_params& p, void* base, bool frames_out, int64_t box_cap) {
   Carver c(base);
   const size_t es = net->cfg.dtype == REGEN_DTYPE_BF16 ? 2 : 4;
   const int C8 = net->cfg.channels / 8, s = net->cfg.scale;
@@ -437,6 +553,7 @@ EnhanceBufs enhance_bufs(const SRNet* net, const regen_pack_params& p, void* bas
   e.map = c.take<int32_t>(px);
   e.mbits = c.take<uint32_t>((size_t)p.max_bins * p.bin_h * ((p.bin_w + 31) / 32));
   e.dst = c.take<int64_t>(px);
+  e.lists = box_cap > 0 ? c.take<int32_t>(2 * ((size_t)p.max_bins + 1) + (size_t)box_cap) : nullptr;
   e.counters = c.take<int32_t>(N_COUNTERS);
   e.x0 = c.take<uint8_t>(px * 8 * es);
   e.a0 = c.take<uint8_t>(px * C8 * 8 * es);
@@ -490,7 +607,7 @@ regen_status stitch_into(const regen_geom& g, const regen_pack_params& p, int dt
                          const uint8_t* d_frames, const regen_box* d_boxes, const int64_t* d_num_boxes,
                          int64_t max_boxes, const int32_t* d_num_bins, int32_t* map, void* out, cudaStream_t s,
                          uint32_t* mbits = nullptr, const int32_t* owner = nullptr, int64_t* dst = nullptr,
-                         int scale = 0) {
+                         int scale = 0, int32_t* lists = nullptr) {
   OwnArgs oa;
   oa.owner = owner;
   oa.dst = dst;
@@ -501,6 +618,35 @@ regen_status stitch_into(const regen_geom& g, const regen_pack_params& p, int dt
   oa.GH = grid_h(g);
   oa.GW = grid_w(g);
   oa.mb = g.mb;
+  if (lists != nullptr && p.bin_w % 32 == 0 && p.bin_w <= 1024) {
+    int32_t* cnt = lists;                       // [max_bins + 1] counts, then fill cursors
+    int32_t* off = lists + p.max_bins + 1;      // [max_bins + 1]
+    int32_t* list = off + p.max_bins + 1;       // [max_boxes]
+    const unsigned gb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((max_boxes + 255) / 256, 148 * 4));
+    REGEN_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)p.max_bins + 1), s));
+    {
+      REGEN_TRACE("stitch_lists", s);
+      bin_count_kernel<<<gb, 256, 0, s>>>(d_boxes, d_num_boxes, max_boxes, cnt);
+      bin_scan_kernel<<<1, 1024, 0, s>>>(d_num_bins, p.max_bins, cnt, off);
+      bin_fill_kernel<<<gb, 256, 0, s>>>(d_boxes, d_num_boxes, max_boxes, cnt, list);
+    }
+    REGEN_LAUNCH_CHECK();
+    const size_t smem = sizeof(int32_t) * STITCH_BAND * p.bin_w;
+    const unsigned grid = (unsigned)std::min<int64_t>((int64_t)p.max_bins * ((p.bin_h + STITCH_BAND - 1) / STITCH_BAND),
+                                                      148 * 8);
+    REGEN_TRACE("stitch", s);
+#define STITCH_GO(T, L)                                                                                          \
+  stitch_band_kernel<T, L><<<grid, 256, smem, s>>>(d_frames, d_boxes, off, list, d_num_bins, p.max_bins, p.bin_w, \
+                                                   p.bin_h, g.F, g.frame_w, g.frame_h, map, (T*)out, mbits, oa)
+    if (dtype == REGEN_DTYPE_BF16) {
+      if (layout == 0) STITCH_GO(__nv_bfloat16, 0); else STITCH_GO(__nv_bfloat16, 1);
+    } else {
+      if (layout == 0) STITCH_GO(float, 0); else STITCH_GO(float, 1);
+    }
+#undef STITCH_GO
+    REGEN_LAUNCH_CHECK();
+    return REGEN_OK;
+  }
   {
     REGEN_TRACE("clear", s);
     clear_kernel<<<STITCH_CTAS, 256, 0, s>>>(d_num_bins, p.max_bins, (size_t)p.bin_w * p.bin_h, map,
@@ -581,7 +727,7 @@ static regen_status enhance_run(const SRNet* net, const regen_geom* geom, const 
   REGEN_CUDA(cudaMemsetAsync(e.counters, 0, N_COUNTERS * sizeof(int32_t), s));
   regen_status st = stitch_into(*geom, *p, net->cfg.dtype, 0, d_frames, d_boxes, d_num_boxes, max_boxes, d_num_bins,
                                 e.map, e.x0, s, e.mbits, fa ? fa->owner : nullptr, e.dst,
-                                net->cfg.scale);
+                                net->cfg.scale, e.lists);
   if (st != REGEN_OK) return st;
   const auto& cv = net->convs;
   if (net->cfg.n_resblocks == 0) {
@@ -647,8 +793,8 @@ static size_t hr_bins_bytes(const SRNet* net, const regen_pack_params& p) {
 }
 
 // workspace of regen_enhance_scatter: the enhance buffers, plus the HR bins when the fold is off
-size_t enhance_scatter_ws_bytes(const SRNet* net, const regen_pack_params& p) {
-  const size_t e = (enhance_bufs(net, p, nullptr, true).bytes + 255) / 256 * 256;
+size_t enhance_scatter_ws_bytes(const SRNet* net, const regen_pack_params& p, int64_t box_cap) {
+  const size_t e = (enhance_bufs(net, p, nullptr, true, box_cap).bytes + 255) / 256 * 256;
   return fold_enabled(net, p.bin_w) ? e : e + hr_bins_bytes(net, p) + 256;
 }
 
@@ -668,9 +814,9 @@ extern "C" regen_status regen_enhance_packed(void* sr, const regen_geom* geom, c
   const SRNet* net = (const SRNet*)sr;
   st = validate_pack(p, net);
   if (st != REGEN_OK) return st;
-  EnhanceBufs e = enhance_bufs(net, *p, nullptr);
+  EnhanceBufs e = enhance_bufs(net, *p, nullptr, false, n_mbs(*geom));
   REGEN_REQUIRE(d_ws && ws_bytes >= e.bytes, "workspace too small (%zu < %zu)", ws_bytes, e.bytes);
-  e = enhance_bufs(net, *p, d_ws);
+  e = enhance_bufs(net, *p, d_ws, false, n_mbs(*geom));
   return enhance_run(net, geom, p, d_frames, d_boxes, max_boxes, d_num_boxes, d_num_bins, d_hr_bins, e,
                      (cudaStream_t)stream, nullptr);
 }
@@ -695,9 +841,9 @@ static regen_status enhance_scatter_parts(void* sr, const regen_geom* geom, cons
   st = validate_pack(p, net);
   if (st != REGEN_OK) return st;
   REGEN_REQUIRE(net->cfg.scale >= 2, "scale must be >= 2");
-  const size_t need = enhance_scatter_ws_bytes(net, *p);
+  const size_t need = enhance_scatter_ws_bytes(net, *p, n_mbs(*geom));
   REGEN_REQUIRE(d_ws && ws_bytes >= need, "workspace too small (%zu < %zu)", ws_bytes, need);
-  EnhanceBufs e = enhance_bufs(net, *p, d_ws, true);
+  EnhanceBufs e = enhance_bufs(net, *p, d_ws, true, n_mbs(*geom));
   if (fold_enabled(net, p->bin_w)) {
     FoldFrameArgs fa;
     fa.geom = *geom;

@@ -64,6 +64,8 @@ struct EnhanceBufs {
   int64_t* dst;      // [max_bins][bin_h][bin_w] for a pixel whose source MB is owned by its box: the
                      // HR frame pixel index of its top-left HR pixel | rotated << 62; -1 otherwise
                      // (written by paint only when the owner grid is given: regen_enhance_scatter)
+  int32_t* lists;    // one-pass stitch: [max_bins+1] counts/cursors, [max_bins+1] offsets, [box_cap] box ids
+                     // grouped by bin (null when the workspace was sized without a box capacity)
   int32_t* counters; // [N_COUNTERS] dynamic scheduler counters, zeroed per call: conv i at i,
                      // fused residual block k at RB_COUNTER0 + k
   void* x0;          // [max_bins][bin_h][1][bin_w][8]
@@ -75,7 +77,8 @@ struct EnhanceBufs {
   size_t bytes;
 };
 
-EnhanceBufs enhance_bufs(const SRNet* net, const regen_pack_params& p, void* base, bool frames_out = false);
+EnhanceBufs enhance_bufs(const SRNet* net, const regen_pack_params& p, void* base, bool frames_out = false,
+                         int64_t box_cap = 0);
 
 // conv launchers
 regen_status conv_simt_launch(const SRNet* net, const ConvDesc& cv, const void* in, void* out, const void* skip,
