@@ -6,6 +6,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/regen.h"
 
 namespace regen {
@@ -84,6 +86,14 @@ struct TraceScope {
   }
 };
 #define REGEN_TRACE(name, stream) ::regen::TraceScope trace_scope_(name, stream)
+
+// NVTX range around every ABI call (header-only NVTX v3: a no-op unless a tool such as Nsight
+// Systems injects itself), so timelines show which call launched which kernels.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define REGEN_NVTX(name) ::regen::NvtxRange nvtx_range_(name)
 
 // ---------------------------------------------------------------- device helpers
 __device__ __forceinline__ uint32_t score_ord(float s) {

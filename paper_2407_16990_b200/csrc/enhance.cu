@@ -110,6 +110,7 @@ extern "C" regen_status regen_sr_destroy(void* handle);
 
 extern "C" regen_status regen_sr_create(const regen_sr_config* cfg, const float* h_weights, size_t n_weights,
                                         void** out_handle) {
+  REGEN_NVTX("regen_sr_create");
   REGEN_REQUIRE(cfg && h_weights && out_handle, "null argument");
   REGEN_REQUIRE(cfg->scale == 2 || cfg->scale == 3 || cfg->scale == 4, "scale must be 2, 3 or 4");
   REGEN_REQUIRE(cfg->channels >= 8 && cfg->channels <= 64 && cfg->channels % 8 == 0,
@@ -178,6 +179,7 @@ extern "C" regen_status regen_sr_create(const regen_sr_config* cfg, const float*
 }
 
 extern "C" regen_status regen_sr_destroy(void* handle) {
+  REGEN_NVTX("regen_sr_destroy");
   if (!handle) return REGEN_OK;
   SRNet* net = (SRNet*)handle;
   cudaFree(net->d_w32);
@@ -687,6 +689,7 @@ extern "C" regen_status regen_stitch_bins(const regen_geom* geom, const regen_pa
                                           const uint8_t* d_frames, const regen_box* d_boxes, int64_t max_boxes,
                                           const int64_t* d_num_boxes, const int32_t* d_num_bins, void* d_lr_bins,
                                           void* d_ws, size_t ws_bytes, void* stream) {
+  REGEN_NVTX("regen_stitch_bins");
   regen_status st = validate_geom(geom);
   if (st != REGEN_OK) return st;
   st = validate_pack(p);
@@ -804,6 +807,7 @@ extern "C" regen_status regen_enhance_packed(void* sr, const regen_geom* geom, c
                                              const uint8_t* d_frames, const regen_box* d_boxes, int64_t max_boxes,
                                              const int64_t* d_num_boxes, const int32_t* d_num_bins, void* d_hr_bins,
                                              int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream) {
+  REGEN_NVTX("regen_enhance_packed");
   REGEN_REQUIRE(sr != nullptr, "null SR handle");
   regen_status st = validate_geom(geom);
   if (st != REGEN_OK) return st;
@@ -870,6 +874,7 @@ extern "C" regen_status regen_enhance_scatter(void* sr, const regen_geom* geom, 
                                               const int64_t* d_num_boxes, const int32_t* d_num_bins,
                                               const int32_t* d_mb_owner, void* d_out, int32_t out_dtype,
                                               int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream) {
+  REGEN_NVTX("regen_enhance_scatter");
   return enhance_scatter_parts(sr, geom, p, d_frames, d_boxes, max_boxes, d_num_boxes, d_num_bins, d_mb_owner, d_out,
                                out_dtype, d_status, d_ws, ws_bytes, (cudaStream_t)stream, 3);
 }
@@ -879,6 +884,7 @@ extern "C" regen_status regen_enhance_owned(void* sr, const regen_geom* geom, co
                                             const int64_t* d_num_boxes, const int32_t* d_num_bins,
                                             const int32_t* d_mb_owner, void* d_out, int32_t out_dtype,
                                             int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream) {
+  REGEN_NVTX("regen_enhance_owned");
   return enhance_scatter_parts(sr, geom, p, d_frames, d_boxes, max_boxes, d_num_boxes, d_num_bins, d_mb_owner, d_out,
                                out_dtype, d_status, d_ws, ws_bytes, (cudaStream_t)stream, 1);
 }

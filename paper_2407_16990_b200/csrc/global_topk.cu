@@ -124,6 +124,7 @@ static unsigned grid_for(int64_t n) { return (unsigned)std::max<int64_t>(1, std:
 using namespace regen;
 
 extern "C" regen_status regen_topk_init(int64_t k, regen_topk_state* d_state, void* stream) {
+  REGEN_NVTX("regen_topk_init");
   REGEN_REQUIRE(k >= 0 && d_state, "k >= 0 and a state buffer required");
   cudaStream_t s = (cudaStream_t)stream;
   {
@@ -136,6 +137,7 @@ extern "C" regen_status regen_topk_init(int64_t k, regen_topk_state* d_state, vo
 
 extern "C" regen_status regen_topk_histogram(const regen_geom* geom, int64_t stream0, const float* d_importance,
                                              const regen_topk_state* d_state, uint32_t* d_hist, void* stream) {
+  REGEN_NVTX("regen_topk_histogram");
   regen_status st = validate_geom(geom);
   if (st != REGEN_OK) return st;
   REGEN_REQUIRE(d_importance && d_state && d_hist, "null device pointer");
@@ -154,6 +156,7 @@ extern "C" regen_status regen_topk_histogram(const regen_geom* geom, int64_t str
 }
 
 extern "C" regen_status regen_topk_pick(const uint32_t* d_hist, regen_topk_state* d_state, void* stream) {
+  REGEN_NVTX("regen_topk_pick");
   REGEN_REQUIRE(d_hist && d_state, "null device pointer");
   cudaStream_t s = (cudaStream_t)stream;
   {
@@ -170,6 +173,7 @@ extern "C" regen_status regen_select_mbs_global(const regen_geom* geom, const re
                                                 int32_t* d_labels, regen_region* d_regions, int64_t max_regions,
                                                 int64_t* d_num_regions, int32_t* d_status, void* d_ws,
                                                 size_t ws_bytes, void* stream) {
+  REGEN_NVTX("regen_select_mbs_global");
   regen_status st = validate_geom(geom);
   if (st != REGEN_OK) return st;
   REGEN_REQUIRE(p != nullptr, "params is null");

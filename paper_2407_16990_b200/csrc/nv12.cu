@@ -63,6 +63,7 @@ using namespace regen;
 
 extern "C" regen_status regen_nv12_to_rgb8(const regen_geom* geom, const uint8_t* d_nv12, uint8_t* d_rgb8,
                                            void* stream) {
+  REGEN_NVTX("regen_nv12_to_rgb8");
   regen_status st = validate_geom(geom);
   if (st != REGEN_OK) return st;
   REGEN_REQUIRE(d_nv12 && d_rgb8, "null device pointer");

@@ -756,6 +756,7 @@ extern "C" regen_status regen_pack_regions(const regen_geom* geom, const regen_p
                                            regen_box* d_boxes, int64_t max_boxes, int64_t* d_num_boxes,
                                            int32_t* d_order, int32_t* d_num_bins, int32_t* d_mb_owner,
                                            int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream) {
+  REGEN_NVTX("regen_pack_regions");
   regen_status st = validate_geom(geom);
   if (st != REGEN_OK) return st;
   REGEN_REQUIRE(p != nullptr, "params is null");

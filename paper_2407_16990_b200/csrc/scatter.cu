@@ -487,6 +487,7 @@ extern "C" regen_status regen_scatter_blend(const regen_geom* geom, const regen_
                                             const uint8_t* d_frames, const regen_box* d_boxes,
                                             const int32_t* d_mb_owner, const void* d_hr_bins, int32_t hr_dtype,
                                             void* d_out, int32_t out_dtype, void* stream) {
+  REGEN_NVTX("regen_scatter_blend");
   regen_status st = validate_geom(geom);
   if (st != REGEN_OK) return st;
   REGEN_REQUIRE(p != nullptr, "pack params null");
@@ -501,6 +502,7 @@ extern "C" regen_status regen_scatter_blend(const regen_geom* geom, const regen_
 extern "C" regen_status regen_scatter_bilinear(const regen_geom* geom, int32_t scale, const uint8_t* d_frames,
                                                const int32_t* d_mb_owner, void* d_out, int32_t out_dtype,
                                                void* stream) {
+  REGEN_NVTX("regen_scatter_bilinear");
   regen_status st = validate_geom(geom);
   if (st != REGEN_OK) return st;
   REGEN_REQUIRE(scale >= 2 && scale <= 4, "scale must be 2, 3 or 4");

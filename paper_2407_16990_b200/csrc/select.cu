@@ -382,6 +382,7 @@ extern "C" regen_status regen_select_mbs(const regen_geom* geom, const regen_sel
                                          const float* d_importance, uint32_t* d_sel_bitmap, int32_t* d_labels,
                                          regen_region* d_regions, int64_t max_regions, int64_t* d_num_regions,
                                          int32_t* d_status, void* d_ws, size_t ws_bytes, void* stream) {
+  REGEN_NVTX("regen_select_mbs");
   regen_status st = validate_geom(geom);
   if (st != REGEN_OK) return st;
   REGEN_REQUIRE(p != nullptr, "params is null");

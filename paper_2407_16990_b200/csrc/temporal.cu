@@ -251,6 +251,7 @@ extern "C" regen_status regen_temporal_select(const regen_geom* geom, const int1
                                               int64_t budget, double* d_phi, uint8_t* d_selected, int32_t* d_reuse,
                                               int32_t* d_frames_per_stream, void* d_ws, size_t ws_bytes,
                                               void* stream) {
+  REGEN_NVTX("regen_temporal_select");
   regen_status st = validate_geom(geom);
   if (st != REGEN_OK) return st;
   REGEN_REQUIRE(d_residual_y && d_phi && d_selected && d_reuse && d_frames_per_stream, "null device pointer");
@@ -312,6 +313,7 @@ extern "C" regen_status regen_temporal_select(const regen_geom* geom, const int1
 
 extern "C" regen_status regen_reuse_importance(const regen_geom* geom, const float* d_pred, const int32_t* d_reuse,
                                                float* d_out, void* stream) {
+  REGEN_NVTX("regen_reuse_importance");
   regen_status st = validate_geom(geom);
   if (st != REGEN_OK) return st;
   REGEN_REQUIRE(d_pred && d_reuse && d_out && d_pred != d_out, "null or aliased device pointer");

@@ -14,7 +14,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'resblock' -c 2 -o $O/${TAG}_prof_rb -f \
     $B > $O/${TAG}_ncu_full_rb.log 2>&1; echo "full rb rc=$?"
 timeout 1500 ncu --set full --clock-control none --import-source on \
-    -k regex:'conv_tc|bilinear|gather|clear|paint|pack_kernel|select_kernel|ccl_kernel|box_write|sort_bitonic' -c 14 \
+    -k regex:"conv_tc|bilinear|stitch|pack_kernel|select_kernel|ccl_kernel|box_write|sort_bitonic" -c 14 \
     -o $O/${TAG}_prof -f $B > $O/${TAG}_ncu_full.log 2>&1; echo "full rc=$?"
 for r in ${TAG}_prof_rb ${TAG}_prof; do
   ncu -i $O/$r.ncu-rep --page raw --csv > $O/$r.raw.csv 2>/dev/null

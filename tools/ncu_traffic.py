@@ -31,8 +31,12 @@ def trace_name(kernel: str) -> str | None:
         return "scatter_bilinear" if re.search(r"(true|\(bool\)1|, 1)>", kernel) else "scatter"
     if "combine_kernel" in kernel:
         return "fold_combine_frames" if re.search(r"(true|\(bool\)1|, 1)>", kernel) else "fold_combine"
+    if "stitch_band_kernel" in kernel:
+        return "stitch"
+    if "sort_bitonic_kernel" in kernel:
+        return "sort_rank"
     for k in ("gather", "paint", "select", "ccl", "region_write", "box_count", "box_write", "sort_rank", "pack",
-              "owner_fix", "conv_simt"):
+              "owner_fix", "conv_simt", "pack_policy", "topk_hist", "topk_select", "nv12_rgb"):
         if re.search(rf"\b{k}_kernel", kernel):
             return k
     return None
@@ -40,23 +44,24 @@ def trace_name(kernel: str) -> str | None:
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("report")
+    ap.add_argument("report", nargs="+")
     ap.add_argument("--out", default="profiles/ncu_traffic.json")
     a = ap.parse_args()
-    raw = subprocess.run(["ncu", "-i", a.report, "--page", "raw", "--csv"], check=True, capture_output=True,
-                         text=True).stdout
-    rows = list(csv.reader(io.StringIO(raw)))
-    h, units = rows[0], rows[1]
-    ki, ri, wi, ti = (h.index(x) for x in ("Kernel Name", "dram__bytes_read.sum", "dram__bytes_write.sum",
-                                            "gpu__time_duration.sum"))
     acc: dict[str, list] = {}
-    for r in rows[2:]:
-        name = trace_name(r[ki])
-        if name is None:
-            continue
-        b = float(r[ri].replace(",", "")) * UNIT[units[ri]] + float(r[wi].replace(",", "")) * UNIT[units[wi]]
-        acc.setdefault(name, []).append((b, float(r[ti].replace(",", ""))))
-    out = {"source": a.report.split("/")[-1],
+    for rep in a.report:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], check=True, capture_output=True,
+                             text=True).stdout
+        rows = list(csv.reader(io.StringIO(raw)))
+        h, units = rows[0], rows[1]
+        ki, ri, wi, ti = (h.index(x) for x in ("Kernel Name", "dram__bytes_read.sum", "dram__bytes_write.sum",
+                                                "gpu__time_duration.sum"))
+        for r in rows[2:]:
+            name = trace_name(r[ki])
+            if name is None:
+                continue
+            b = float(r[ri].replace(",", "")) * UNIT[units[ri]] + float(r[wi].replace(",", "")) * UNIT[units[wi]]
+            acc.setdefault(name, []).append((b, float(r[ti].replace(",", ""))))
+    out = {"source": " + ".join(x.split("/")[-1] for x in a.report),
            "note": "dram__bytes_read.sum + dram__bytes_write.sum per launch (bytes), mean over the captured launches; "
                    "ncu --set full --clock-control none, cold cache",
            "kernels": {k: sum(x[0] for x in v) / len(v) for k, v in sorted(acc.items())},

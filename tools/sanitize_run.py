@@ -31,3 +31,33 @@ for kind in ("blobs", "noisy"):
     r = p.host_results()
     assert r["status"] == 0
     print(kind, "boxes", r["num_boxes"], "bins", r["num_bins"])
+
+# round-2 kernels: the per-bin packer path (> 5000 boxes), the placement policies, the one-pass stitch,
+# cross-rank top-N, temporal reuse and NV12 conversion
+wl30 = dataclasses.replace(synth.CONFIGS["c2"], partition_mb=1)
+imp = torch.from_numpy(synth.importance_maps(wl30.S, wl30.F, wl30.GH, wl30.GW, 5)).cuda()
+sr_small = synth.SRConfig(3, 16, 1, 1.0, True)
+w_small = synth.sr_weights(sr_small, 0)
+p = rg.Pipeline(S=wl30.S, F=wl30.F, W=wl30.W, H=wl30.H, k=wl30.k, bin_w=128, bin_h=128, max_bins=wl30.max_bins,
+                partition_mb=1, scale=3, channels=16, n_resblocks=1, weights=w_small)
+p.select(imp)
+p.pack_step(imp)
+print("bins path: boxes", p.host_results()["num_boxes"])
+wl4 = synth.small(synth.CONFIGS["c2"], F=4)
+imp4 = torch.from_numpy(synth.importance_maps(wl4.S, wl4.F, wl4.GH, wl4.GW, 6, "noisy")).cuda()
+for pol, order in ((rg.POLICY_MAXRECT, 0), (rg.POLICY_SKYLINE, 0), (rg.POLICY_SHELF, 2)):
+    q = rg.Pipeline(S=wl4.S, F=wl4.F, W=wl4.W, H=wl4.H, k=wl4.k, bin_w=128, bin_h=128, max_bins=64, partition_mb=4,
+                    scale=3, channels=16, n_resblocks=1, weights=w_small, policy=pol, order=order)
+    q.select(imp4)
+    q.pack_step(imp4)
+    print("policy", pol, "bins", q.host_results()["num_bins"])
+from paper_2407_16990_b200.global_topk import global_select  # noqa: E402
+global_select([(q, 0, imp4)], wl4.k, "cuda")
+torch.cuda.synchronize()
+t = rg.TemporalReuse(2, 30, 640, 360)
+t.run(torch.from_numpy(synth.residuals_y(2, 30, 360, 640, 1)).cuda(), 12)
+nv = torch.from_numpy(synth.frames_nv12(1, 2, 360, 640, 1)).cuda()
+rgb = torch.empty((1, 2, 360, 640, 3), dtype=torch.uint8, device="cuda")
+rg.nv12_to_rgb8(rg.Geom(1, 2, 640, 360, 16), nv, rgb)
+torch.cuda.synchronize()
+print("round-2 kernels ok")
