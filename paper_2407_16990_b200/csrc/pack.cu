@@ -686,6 +686,7 @@ __device__ void pack_bins(const PackArgs& a, uint8_t* psm) {
         a.seqv[(size_t)bin * PACK_SLOTS + lane] = mys;
       }
       const uint32_t bs = warp_max2(lane < cnt ? area_sum(myr) : 0u);
+      __syncwarp();   // every lane's read of bcnt[bin] above precedes lane 0's write
       if (lane == 0) { bsum[bin] = bs; bcnt[bin] = (uint8_t)cnt; }
       __syncwarp();
       const int gb = (bin >> 5) << 5;
