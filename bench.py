@@ -511,8 +511,9 @@ def main() -> None:
         lr_bytes = wl.S * wl.F * wl.W * wl.H * 3
         hbm_alg = {"scatter_bilinear": ((s2 * (wl.S * wl.F * wl.W * wl.H * G - sel_px) * 3 * es_out) / max(G, 1)
                                         + lr_bytes, "HR bytes of the non-owned pixels written + LR frames read"),
-                   "gather": ((box_px * 3 + n_bins * wl.bin_w * wl.bin_h * 16) / max(G, 1),
-                              "box pixels read (u8 RGB) + packed bins written (8 bf16 channels)")}
+                   "stitch": ((box_px * 3 + n_bins * wl.bin_w * wl.bin_h * 16) / max(G, 1),
+                              "box pixels read (u8 RGB) + packed bins written (8 bf16 channels); the bin map, "
+                              "owned-pixel destinations and occupancy bits it also writes are implementation traffic")}
         hbm = {}
         for name, (nbytes, what) in hbm_alg.items():
             if name in kern_all:

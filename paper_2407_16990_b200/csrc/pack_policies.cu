@@ -23,6 +23,17 @@ namespace regen {
 constexpr int PP_THREADS = 256;
 constexpr int PP_MAX_BINS = 8192;
 constexpr int SHELF_CAP = 256;   // shelves per bin (as the oracle)
+constexpr int SKY_NW = 8;        // SKYLINE summary widths 4, 8, ..., 512
+__host__ __device__ constexpr int sky_w(int i) { return 4 << i; }
+
+// SKYLINE filter: a footprint uw x uh can rest in bin k only if, for the widest summary width w <= uw,
+// the lowest resting height of a w-wide footprint (<= that of the uw-wide one) leaves uh rows
+__device__ __forceinline__ bool sky_may_fit(const int16_t* lw, int uw, int uh, int Hg) {
+  if (uw < sky_w(0)) return true;   // narrower than every summary width: no filter
+  int i = 0;
+  while (i + 1 < SKY_NW && sky_w(i + 1) <= uw) ++i;
+  return lw[i] + uh <= Hg;
+}
 
 struct PolicyArgs {
   regen_box* boxes;
@@ -36,6 +47,7 @@ struct PolicyArgs {
   uint32_t* occ;      // MAXRECT: [max_bins][Hg][W32] occupancy bits
   int4* mer;          // MAXRECT: [max_bins] the bin's free area (x, y, w, h)
   int16_t* hgt;       // SKYLINE: [max_bins][W] column heights
+  int16_t* lw;        // SKYLINE: [max_bins][SKY_NW] lowest resting height of a footprint SKY_W(i) wide
   int16_t* sy;        // SHELF: [max_bins][SHELF_CAP] shelf y0, height, end x
   int16_t* sh;
   int16_t* sx;
@@ -121,8 +133,14 @@ __global__ void __launch_bounds__(PP_THREADS, 1) pack_policy_kernel(PolicyArgs a
     while (placed_bin < 0) {
       // first candidate bin >= from (summary filter), the fresh bin `opened` always a candidate
       unsigned long long c = ~0ull;
-      for (int k = from + threadIdx.x; k < opened; k += PP_THREADS)
-        if (sum_a[k] >= qa) { c = (unsigned long long)k; break; }
+      for (int k = from + threadIdx.x; k < opened; k += PP_THREADS) {
+        bool ok = sum_a[k] >= qa;
+        if (ok && a.policy == REGEN_POLICY_SKYLINE) {
+          const int16_t* lw = a.lw + (size_t)k * SKY_NW;
+          ok = sky_may_fit(lw, pw, ph, Hg) || sky_may_fit(lw, ph, pw, Hg);
+        }
+        if (ok) { c = (unsigned long long)k; break; }
+      }
       unsigned long long cand = block_min64(c, red);
       int k = cand == ~0ull ? opened : (int)cand;
       if (k >= a.max_bins) break;
@@ -256,6 +274,20 @@ __global__ void __launch_bounds__(PP_THREADS, 1) pack_policy_kernel(PolicyArgs a
       for (int cc = 1 + threadIdx.x; cc < W; cc += PP_THREADS) lo = min(lo, (unsigned long long)h[cc]);
       const unsigned long long m = block_min64(lo, red);
       if (threadIdx.x == 0) sum_a[k] = (int16_t)(m == ~0ull ? 0 : Hg - (int)m);
+      // per-width lowest resting heights (warp i: width sky_w(i); lanes over the positions)
+      const int wi = threadIdx.x >> 5;
+      if (wi < SKY_NW) {
+        const int w = sky_w(wi);
+        int best = Hg + 1;
+        for (int x = 1 + (threadIdx.x & 31); x + w <= W; x += 32) {
+          int y = 0;
+          for (int cc = x; cc < x + w; ++cc) y = max(y, (int)h[cc]);
+          best = min(best, y);
+        }
+        best = __reduce_min_sync(0xffffffffu, best);
+        if ((threadIdx.x & 31) == 0) a.lw[(size_t)k * SKY_NW + wi] = (int16_t)best;
+      }
+      __syncthreads();
     } else {
       __syncthreads();
       // summary: the most width left on a shelf, or the height left above the top shelf
@@ -285,6 +317,7 @@ size_t policy_workspace_bytes(const regen_pack_params& p) {
       break;
     case REGEN_POLICY_SKYLINE:
       c.take<int16_t>(B * p.bin_w);
+      c.take<int16_t>(B * SKY_NW);
       break;
     case REGEN_POLICY_SHELF:
       c.take<int16_t>(3 * B * SHELF_CAP);
@@ -322,6 +355,7 @@ regen_status launch_pack_policy(const regen_pack_params& p, regen_box* d_boxes, 
     a.stack = c.take<short2>((size_t)PP_THREADS * Hg);
   } else if (p.policy == REGEN_POLICY_SKYLINE) {
     a.hgt = c.take<int16_t>(B * p.bin_w);
+    a.lw = c.take<int16_t>(B * SKY_NW);
   } else {
     a.sy = c.take<int16_t>(B * SHELF_CAP);
     a.sh = c.take<int16_t>(B * SHELF_CAP);

@@ -31,12 +31,12 @@ def _make(wl, w, **kw):
                                bf16=wl.sr.bf16, res_scale=wl.sr.res_scale, **kw)
 
 
-def _every_pixel(wl, seed):
+def _every_pixel(wl, seed, **pipe_kw):
     from paper_2407_16990_b200.schedule import PipelinedRunner
     imp_h = synth.importance_maps(wl.S, wl.F, wl.GH, wl.GW, seed)
     fr_h = synth.frames_rgb8(wl.S, wl.F, wl.H, wl.W, seed)
     w = synth.sr_weights(wl.sr, seed)
-    r = PipelinedRunner(_make(wl, w), "cuda")
+    r = PipelinedRunner(_make(wl, w, **pipe_kw), "cuda", n_pipes=3, n_front=2)
     imp, fr = torch.from_numpy(imp_h).cuda(), torch.from_numpy(fr_h).cuda()
     r.run_eager(imp, fr, 2)
     torch.cuda.synchronize()
@@ -49,7 +49,7 @@ def _every_pixel(wl, seed):
     assert torch.equal(r.pipes[0].out, r.pipes[1].out)
     res = r.pipes[0].host_results()
     o = oracle.index_path(imp_h, wl.W, wl.H, wl.k, partition_mb=wl.partition_mb, bin_w=wl.bin_w, bin_h=wl.bin_h,
-                          max_bins=wl.max_bins)
+                          max_bins=wl.max_bins, policy=pipe_kw.get("policy", 0), order_policy=pipe_kw.get("order", 0))
     assert res["status"] == 0 and res["num_bins"] == o["num_bins"]
     np.testing.assert_array_equal(res["owner"], o["owner"])
     np.testing.assert_array_equal(np.stack([res["boxes"][c] for c in ("bin", "bx", "by", "rotated")], 1),
@@ -80,6 +80,28 @@ def test_c3_two_frames_every_box_every_hr_pixel():
     """C3 (8 streams, one selection group) at 2 frames per stream: every box and HR pixel."""
     worst, nbox = _every_pixel(synth.small(synth.CONFIGS["c3"], F=2), 22)
     assert nbox > 200
+
+
+def test_c4_group_two_frames_every_box_every_hr_pixel():
+    """C4's selection group (8 streams, top-15%) at 2 frames per stream: every box and HR pixel."""
+    worst, nbox = _every_pixel(synth.small(synth.CONFIGS["c4"], F=2), 23)
+    assert nbox > 150
+
+
+def test_c5_group_two_frames_every_box_every_hr_pixel():
+    """C5's selection group (2 streams of 720p -> 1440p x2, EDSR 16 x 64: the unfused C = 64 convs and
+    the p = 2 fold) at 2 frames per stream and a 10% ratio: every box and HR pixel."""
+    import dataclasses as dc
+    worst, nbox = _every_pixel(dc.replace(synth.small(synth.CONFIGS["c5"], F=2), pct=10.0), 24)
+    assert nbox > 50
+
+
+@pytest.mark.parametrize("policy,order", [(1, 0), (2, 0), (3, 2)])
+def test_policy_packings_through_the_whole_path(policy, order):
+    """The SR and paste-back do not depend on the packer: bins filled by the MAXRECT / SKYLINE / SHELF
+    policies give every HR pixel within tolerance too (C2 geometry, 3 frames)."""
+    worst, nbox = _every_pixel(synth.small(synth.CONFIGS["c2"], F=3), 25, policy=policy, order=order)
+    assert nbox > 40
 
 
 # ----------------------------------------------------------------------------- status bits
