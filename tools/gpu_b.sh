@@ -22,7 +22,7 @@ import json
 try:
     d=json.loads(open("$O/${TAG}_bench$i.json").read().strip().splitlines()[-1])
     r=d.get("roofline",{}); rs=d.get("roofline_step",{})
-    print("value", round(d["value"]), "ms", round(d["ms_per_step"],3), "kfrac", r.get("frac"), "stepfrac", rs.get("frac"), "e2e", round(d["e2e"]["value"]), "cpu", d.get("cpu_baseline",{}).get("value"))
+    print("value", round(d["value"]), "ms", round(d["ms_per_step"],3), "kfrac", r.get("frac"), "stepfrac", rs.get("frac"), "e2e", d["e2e"]["value"], "cpu", d.get("cpu_baseline",{}).get("value"))
     for k,v in list(d["kernels"].items())[:14]: print(f'  {k:24s} {v["launches_per_step"]:6.1f} {v["ms_mean"]*1000:9.1f} {v["share"]:.3f}')
 except Exception as e: print("parse fail", e)
 PY
