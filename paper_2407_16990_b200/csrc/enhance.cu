@@ -353,6 +353,8 @@ __global__ void __launch_bounds__(256) stitch_band_kernel(const uint8_t* frames,
                                                           int F, int W, int H, int32_t* map, T* out, uint32_t* mbits,
                                                           OwnArgs oa) {
   extern __shared__ int32_t band_ids[];   // [STITCH_BAND][bin_w]
+  __shared__ float u8f[256];              // fp32(u8 / 255), correctly rounded (D9): one table load per value
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) u8f[i] = __fdiv_rn((float)i, 255.0f);
   const int nbands = (bin_h + STITCH_BAND - 1) / STITCH_BAND;
   const int items = min(*num_bins, max_bins) * nbands;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
@@ -373,8 +375,12 @@ __global__ void __launch_bounds__(256) stitch_band_kernel(const uint8_t* frames,
         for (int p = lane; p < fw; p += 32) band_ids[(r - y0) * bin_w + bx.bx + p] = id;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < rows * bin_w; i += blockDim.x) {
-      const int yy = i / bin_w, x = i - yy * bin_w, y = y0 + yy;
+    // bin_w dividing the block: a thread keeps its column and steps rows (no division per pixel)
+    const int ystep = (blockDim.x % bin_w == 0) ? (int)blockDim.x / bin_w : 0;
+    const int xs = threadIdx.x % bin_w, ys = threadIdx.x / bin_w;
+    for (int i = threadIdx.x, yy = ys, x = xs; i < rows * bin_w; i += blockDim.x) {
+      if (ystep == 0) { yy = i / bin_w; x = i - yy * bin_w; }
+      const int y = y0 + yy;
       const int32_t id = band_ids[i];
       const size_t px = ((size_t)bin * bin_h + y) * bin_w + x;
       if (mbits != nullptr) {   // bin_w % 32 == 0: a warp covers 32 consecutive pixels of one row
@@ -391,7 +397,7 @@ __global__ void __launch_bounds__(256) stitch_band_kernel(const uint8_t* frames,
         const int sy = bx.rotated ? bx.y0 + bx.h - 1 - p : bx.y0 + q;
         const uint8_t* src = frames + ((((int64_t)bx.stream * F + bx.frame) * H + sy) * W + sx) * 3;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) v[c] = __fdiv_rn((float)src[c], 255.0f);
+        for (int c = 0; c < 3; ++c) v[c] = u8f[src[c]];
         if (oa.owner) {
           const int32_t* ow = oa.owner + ((size_t)bx.stream * oa.F + bx.frame) * oa.GH * oa.GW;
           if (ow[(sy / oa.mb) * oa.GW + sx / oa.mb] == id) {
@@ -417,6 +423,7 @@ __global__ void __launch_bounds__(256) stitch_band_kernel(const uint8_t* frames,
 #pragma unroll
         for (int c = 0; c < 4; ++c) o[c] = to_t<T>(c < 3 ? v[c] : 0.0f);
       }
+      yy += ystep;
     }
     __syncthreads();
   }
@@ -620,7 +627,8 @@ regen_status stitch_into(const regen_geom& g, const regen_pack_params& p, int dt
   oa.GH = grid_h(g);
   oa.GW = grid_w(g);
   oa.mb = g.mb;
-  if (lists != nullptr && p.bin_w % 32 == 0 && p.bin_w <= 1024) {
+  static const bool old_stitch = getenv("REGEN_OLD_STITCH") != nullptr;   // A/B aid: clear + paint + gather
+  if (lists != nullptr && p.bin_w % 32 == 0 && p.bin_w <= 1024 && !old_stitch) {
     int32_t* cnt = lists;                       // [max_bins + 1] counts, then fill cursors
     int32_t* off = lists + p.max_bins + 1;      // [max_bins + 1]
     int32_t* list = off + p.max_bins + 1;       // [max_boxes]
