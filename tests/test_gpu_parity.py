@@ -335,3 +335,28 @@ def test_upsampler_tail_fold_matches_oracle_and_literal_path(s, C, monkeypatch):
     monkeypatch.setenv("REGEN_NO_FOLD", "1")
     worst_lit = _check_pixels(wl, seed=11, kind="noisy", box_sample=sample)
     assert worst_fold <= TOL[True] and worst_lit <= TOL[True]
+
+
+def test_no_selection_gives_the_pure_bilinear_frames():
+    """k = 0: no region, no box, no bin; every HR pixel is the D10 bilinear value (the enhance call runs
+    over zero bins)."""
+    wl = synth.small(synth.CONFIGS["c2"], F=2)
+    imp = synth.importance_maps(wl.S, wl.F, wl.GH, wl.GW, 3)
+    fr = synth.frames_rgb8(wl.S, wl.F, wl.H, wl.W, 3)
+    p = _pipeline(wl, synth.sr_weights(wl.sr, 0), k=0)
+    out = p.run(torch.from_numpy(imp).cuda(), torch.from_numpy(fr).cuda())
+    g = p.host_results()
+    assert g["num_boxes"] == 0 and g["num_bins"] == 0
+    ref = oracle.scatter(fr, np.zeros((0, 12), np.int32), np.zeros((0, 4), np.int32), np.full(g["owner"].shape, -1,
+                         np.int32), np.zeros(1), wl.sr.scale, wl.bin_w, wl.bin_h)
+    got = out.float().cpu().numpy().reshape(ref.shape)
+    assert np.abs(got - ref).max() <= 2e-2 * 0.5
+
+
+@pytest.mark.parametrize("W,H", [(200, 120), (328, 184)])
+def test_odd_frame_sizes_whole_path(W, H):
+    """Frame widths that are not a multiple of 8 (the bilinear pass takes its row kernel) and partial
+    MBs on both axes, through the whole bf16 path: index path bit-exact, every HR pixel in tolerance."""
+    wl = dataclasses.replace(synth.small(synth.CONFIGS["c2"], F=2), W=W, H=H, pct=25.0,
+                             sr=synth.SRConfig(3, 16, 1, 1.0, True))
+    _check_pixels(wl, seed=6, kind="noisy")
