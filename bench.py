@@ -341,8 +341,9 @@ def main() -> None:
         n_pipes = int(max(2, min(4, (0.7 * torch.cuda.mem_get_info(dev)[0]) // per_pipe)))
         n_pipes = int(os.environ.get("REGEN_PIPES", n_pipes))
         n_front = int(os.environ.get("REGEN_FRONTS", max(1, n_pipes - 1)))
+        split = os.environ.get("REGEN_SPLIT_FOLD", "0") == "1"
         runner = PipelinedRunner(make_pipe, dev, bilinear=os.environ.get("REGEN_BILINEAR", "side"), nv12=nv12,
-                                 n_pipes=n_pipes, n_front=n_front)
+                                 n_pipes=n_pipes, n_front=n_front, split_fold=split)
         pipes = runner.pipes
         p = pipes[0]
         imp = [torch.from_numpy(a).to(dev) for a in imp_h]

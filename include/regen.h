@@ -328,6 +328,26 @@ REGEN_API regen_status regen_reuse_importance(const regen_geom* geom, const floa
  * ------------------------------------------------------------------------------------------- */
 REGEN_API regen_status regen_nv12_to_rgb8(const regen_geom* geom, const uint8_t* d_nv12, uint8_t* d_rgb8, void* stream);
 
+/* ---------------------------------------------------------------------------------------------
+ * regen_enhance_owned split into two stream-ordered halves, for schedules that run the partial-sum
+ * combine of batch k on another stream beside batch k+1's convolutions (BF16 tensor-core path with the
+ * UP∘TAIL fold; REGEN_E_UNSUPPORTED otherwise):
+ *   regen_enhance_partials: a6 + a7 up to the fold conv; its partial sums stay in d_ws.
+ *   regen_fold_combine_frames: the combine of those partials into the owned MBs' HR pixels of d_out.
+ * Both take the same d_ws (sized by regen_workspace_size(REGEN_CALL_ENHANCE, ...)); the pair is
+ * bit-identical to regen_enhance_owned. The combine must complete before the next partials call on
+ * the same workspace.
+ * ------------------------------------------------------------------------------------------- */
+REGEN_API regen_status regen_enhance_partials(void* sr, const regen_geom* geom, const regen_pack_params* params,
+                                    const uint8_t* d_frames, const regen_box* d_boxes, int64_t max_boxes,
+                                    const int64_t* d_num_boxes, const int32_t* d_num_bins,
+                                    const int32_t* d_mb_owner, int32_t* d_status, void* d_ws, size_t ws_bytes,
+                                    void* stream);
+REGEN_API regen_status regen_fold_combine_frames(void* sr, const regen_geom* geom, const regen_pack_params* params,
+                                       const regen_box* d_boxes, const int32_t* d_num_bins,
+                                       const int32_t* d_mb_owner, void* d_out, int32_t out_dtype, void* d_ws,
+                                       size_t ws_bytes, void* stream);
+
 /* Workspace bytes for a call (which = REGEN_CALL_*; params = the call's params struct — for PACK,
  * NULL sizes the default guillotine packer, the pack params add a placement policy's per-bin state;
  * sr = SR handle for ENHANCE, else NULL). */

@@ -33,7 +33,7 @@ EXPORTED = ["regen_select_mbs", "regen_pack_regions", "regen_sr_create", "regen_
             "regen_enhance_scatter", "regen_trace_enable", "regen_trace_read", "regen_trace_filter",
             "regen_enhance_owned", "regen_scatter_bilinear", "regen_topk_init", "regen_topk_histogram",
             "regen_topk_pick", "regen_select_mbs_global", "regen_temporal_select", "regen_reuse_importance",
-            "regen_nv12_to_rgb8"]
+            "regen_nv12_to_rgb8", "regen_enhance_partials", "regen_fold_combine_frames"]
 
 
 class Geom(ctypes.Structure):
@@ -92,6 +92,8 @@ def _load():
     lib.regen_workspace_size.argtypes = [i32, P(Geom), vp, vp, P(sz)]
     lib.regen_topk_init.argtypes = [i64, vp, vp]
     lib.regen_nv12_to_rgb8.argtypes = [P(Geom), vp, vp, vp]
+    lib.regen_enhance_partials.argtypes = [vp, P(Geom), P(PackParams), vp, vp, i64, vp, vp, vp, vp, vp, sz, vp]
+    lib.regen_fold_combine_frames.argtypes = [vp, P(Geom), P(PackParams), vp, vp, vp, vp, i32, vp, sz, vp]
     lib.regen_temporal_select.argtypes = [P(Geom), vp, i32, i64, vp, vp, vp, vp, vp, sz, vp]
     lib.regen_reuse_importance.argtypes = [P(Geom), vp, vp, vp, vp]
     lib.regen_topk_histogram.argtypes = [P(Geom), i64, vp, vp, vp, vp]
@@ -402,6 +404,30 @@ class Pipeline:
         out = self.out if out is None else out
         enhance_owned(self.sr, self.geom, self.pack, frames, self.boxes, self.max_boxes, self.counts[1:2],
                       self.num_bins, self.owner, out, self.out_dtype, self.status, self.ws, stream)
+        return out
+
+    def _split_ws(self):
+        need = workspace_size(CALL_ENHANCE, self.geom, self.pack, self.sr.handle)
+        if self.ws.numel() < need:
+            self.ws = self.torch.empty(need, dtype=self.torch.uint8, device=self.out.device)
+        return self.ws
+
+    def enhance_partials(self, frames, stream=None):
+        """regen_enhance_partials: the SR up to the UP∘TAIL fold's partial sums (kept in the workspace)."""
+        ws = self._split_ws()
+        _check(lib.regen_enhance_partials(self.sr.handle, ctypes.byref(self.geom), ctypes.byref(self.pack),
+                                          _ptr(frames), _ptr(self.boxes), self.max_boxes, _ptr(self.counts[1:2]),
+                                          _ptr(self.num_bins), _ptr(self.owner), _ptr(self.status), _ptr(ws),
+                                          ws.numel(), _stream(stream)), "regen_enhance_partials")
+
+    def fold_combine(self, out=None, stream=None):
+        """regen_fold_combine_frames: the owned MBs' HR pixels from the partial sums of enhance_partials."""
+        out = self.out if out is None else out
+        ws = self._split_ws()
+        _check(lib.regen_fold_combine_frames(self.sr.handle, ctypes.byref(self.geom), ctypes.byref(self.pack),
+                                             _ptr(self.boxes), _ptr(self.num_bins), _ptr(self.owner), _ptr(out),
+                                             self.out_dtype, _ptr(ws), ws.numel(), _stream(stream)),
+               "regen_fold_combine_frames")
         return out
 
     def scatter_bilinear(self, frames, out=None, stream=None):

@@ -731,10 +731,12 @@ namespace regen {
 
 // stitch + SR of the packed batch; the HR result goes to hr_bins, or (fa != null, fold path only)
 // straight into the HR frames for owned MBs
+// partials_only (fold path, fa != null): stop after the fold conv, its partial sums left in e.u for a
+// later regen_fold_combine_frames
 static regen_status enhance_run(const SRNet* net, const regen_geom* geom, const regen_pack_params* p,
                                 const uint8_t* d_frames, const regen_box* d_boxes, int64_t max_boxes,
                                 const int64_t* d_num_boxes, const int32_t* d_num_bins, void* d_hr_bins,
-                                const EnhanceBufs& e, cudaStream_t s, FoldFrameArgs* fa) {
+                                const EnhanceBufs& e, cudaStream_t s, FoldFrameArgs* fa, bool partials_only = false) {
   REGEN_CUDA(cudaMemsetAsync(e.counters, 0, N_COUNTERS * sizeof(int32_t), s));
   regen_status st = stitch_into(*geom, *p, net->cfg.dtype, 0, d_frames, d_boxes, d_num_boxes, max_boxes, d_num_bins,
                                 e.map, e.x0, s, e.mbits, fa ? fa->owner : nullptr, e.dst,
@@ -781,13 +783,13 @@ static regen_status enhance_run(const SRNet* net, const regen_geom* geom, const 
     if (fa) {
       fa->map = e.map;
       fa->dst = e.dst;
-      if (fold_fused_supported(net, p->bin_w))   // combine fused into the fold conv: no partials in HBM
+      if (!partials_only && fold_fused_supported(net, p->bin_w))   // combine fused into the fold conv: no partials in HBM
         return fold_fused_launch(net, up_in, e.mbits, p->max_bins, d_num_bins, p->bin_w, p->bin_h,
                                  e.counters + net->fold_conv, s, (ord++) & 1, *fa);
     }
     // last upsampler + tail as the folded conv (partials in e.u) and the partial-sum combine
     st = run_conv(net, cv[net->fold_conv], up_in, e.u, nullptr, e, *p, d_num_bins, s, ord++);
-    if (st == REGEN_OK)
+    if (st == REGEN_OK && !partials_only)
       st = fold_combine_launch(net, e.u, d_hr_bins, e.mbits, p->max_bins, d_num_bins, p->bin_w, p->bin_h, s, fa);
     return st;
   }
@@ -895,4 +897,64 @@ extern "C" regen_status regen_enhance_owned(void* sr, const regen_geom* geom, co
   REGEN_NVTX("regen_enhance_owned");
   return enhance_scatter_parts(sr, geom, p, d_frames, d_boxes, max_boxes, d_num_boxes, d_num_bins, d_mb_owner, d_out,
                                out_dtype, d_status, d_ws, ws_bytes, (cudaStream_t)stream, 1);
+}
+
+// The SR of regen_enhance_owned split in two stream-ordered halves (fold path only): the convolutions
+// up to the UP∘TAIL fold's partial sums (kept in the workspace), and the partial-sum combine that writes
+// the owned MBs' HR pixels into the frames. Together bit-identical to regen_enhance_owned; the combine
+// can then run on another stream beside the next batch's convolutions.
+extern "C" regen_status regen_enhance_partials(void* sr, const regen_geom* geom, const regen_pack_params* p,
+                                               const uint8_t* d_frames, const regen_box* d_boxes, int64_t max_boxes,
+                                               const int64_t* d_num_boxes, const int32_t* d_num_bins,
+                                               const int32_t* d_mb_owner, int32_t* d_status, void* d_ws,
+                                               size_t ws_bytes, void* stream) {
+  REGEN_NVTX("regen_enhance_partials");
+  REGEN_REQUIRE(sr != nullptr, "null SR handle");
+  regen_status st = validate_geom(geom);
+  if (st != REGEN_OK) return st;
+  const SRNet* net = (const SRNet*)sr;
+  st = validate_pack(p, net);
+  if (st != REGEN_OK) return st;
+  REGEN_REQUIRE(d_frames && d_boxes && d_num_boxes && d_num_bins && d_mb_owner && d_status, "null device pointer");
+  REGEN_REQUIRE(max_boxes >= 1 && max_boxes < (1ll << 31), "bad max_boxes");
+  REGEN_UNSUPPORTED_IF(!fold_enabled(net, p->bin_w), "enhance_partials needs the UP-TAIL fold (BF16 tensor-core path)");
+  EnhanceBufs e = enhance_bufs(net, *p, nullptr, false, n_mbs(*geom));
+  REGEN_REQUIRE(d_ws && ws_bytes >= e.bytes, "workspace too small (%zu < %zu)", ws_bytes, e.bytes);
+  e = enhance_bufs(net, *p, d_ws, false, n_mbs(*geom));
+  FoldFrameArgs fa;
+  memset(&fa, 0, sizeof(fa));
+  fa.geom = *geom;
+  fa.boxes = d_boxes;
+  fa.owner = d_mb_owner;
+  return enhance_run(net, geom, p, d_frames, d_boxes, max_boxes, d_num_boxes, d_num_bins, nullptr, e,
+                     (cudaStream_t)stream, &fa, true);
+}
+
+extern "C" regen_status regen_fold_combine_frames(void* sr, const regen_geom* geom, const regen_pack_params* p,
+                                                  const regen_box* d_boxes, const int32_t* d_num_bins,
+                                                  const int32_t* d_mb_owner, void* d_out, int32_t out_dtype,
+                                                  void* d_ws, size_t ws_bytes, void* stream) {
+  REGEN_NVTX("regen_fold_combine_frames");
+  REGEN_REQUIRE(sr != nullptr, "null SR handle");
+  regen_status st = validate_geom(geom);
+  if (st != REGEN_OK) return st;
+  const SRNet* net = (const SRNet*)sr;
+  st = validate_pack(p, net);
+  if (st != REGEN_OK) return st;
+  REGEN_REQUIRE(d_boxes && d_num_bins && d_mb_owner && d_out, "null device pointer");
+  REGEN_REQUIRE(out_dtype == REGEN_DTYPE_BF16 || out_dtype == REGEN_DTYPE_FP32, "bad out dtype");
+  REGEN_UNSUPPORTED_IF(!fold_enabled(net, p->bin_w), "fold_combine_frames needs the UP-TAIL fold");
+  EnhanceBufs e = enhance_bufs(net, *p, nullptr, false, n_mbs(*geom));
+  REGEN_REQUIRE(d_ws && ws_bytes >= e.bytes, "workspace too small (%zu < %zu)", ws_bytes, e.bytes);
+  e = enhance_bufs(net, *p, d_ws, false, n_mbs(*geom));
+  FoldFrameArgs fa;
+  fa.geom = *geom;
+  fa.map = e.map;
+  fa.dst = e.dst;
+  fa.boxes = d_boxes;
+  fa.owner = d_mb_owner;
+  fa.out = d_out;
+  fa.out_dtype = out_dtype;
+  return fold_combine_launch(net, e.u, nullptr, e.mbits, p->max_bins, d_num_bins, p->bin_w, p->bin_h,
+                             (cudaStream_t)stream, &fa);
 }

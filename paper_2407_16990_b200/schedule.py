@@ -15,14 +15,18 @@ from . import Pipeline
 
 class PipelinedRunner:
     def __init__(self, make_pipe, device, bilinear: str = "side", nv12: bool = False, n_pipes: int = 2,
-                 n_front: int = 1):
+                 n_front: int = 1, split_fold: bool = False):
         """bilinear: where regen_scatter_bilinear of a batch runs — "side" (its own lowest-priority
         stream after the batch's index path), "front" (the index stream) or "back" (the SR stream).
         nv12: the frames are NV12 decoder output, converted (regen_nv12_to_rgb8) on the index stream
         into the pipeline's RGB8 buffer at the start of each batch. n_pipes: pipelines (batch k uses
         pipeline k % n_pipes, so up to n_pipes - 1 batches' index paths run ahead of the SR);
-        n_front: index streams (batch k's index path on stream k % n_front)."""
+        n_front: index streams (batch k's index path on stream k % n_front). split_fold: the SR stream
+        runs regen_enhance_partials and the side stream, after the batch's bilinear pass, the fold's
+        partial-sum combine (regen_fold_combine_frames), beside the next batch's convolutions."""
         assert bilinear in ("side", "front", "back")
+        assert not split_fold or bilinear == "side"
+        self.split_fold = split_fold
         assert n_pipes >= 2 and 1 <= n_front <= n_pipes
         self.bilinear = bilinear
         self.nv12 = nv12
@@ -75,17 +79,27 @@ class PipelinedRunner:
                 self.front_done[b].record(sf)
                 if self.bilinear == "front":
                     q.scatter_bilinear(fr_k, stream=sf)
-            if self.bilinear == "side":
+            if self.bilinear == "side" and not self.split_fold:
                 with torch.cuda.stream(self.s_side):
                     self.s_side.wait_event(self.front_done[b])
                     q.scatter_bilinear(fr_k, stream=self.s_side)
                     self.side_done[b].record(self.s_side)
             with torch.cuda.stream(self.s_back):
                 self.s_back.wait_event(self.front_done[b])
-                q.enhance_owned(fr_k, stream=self.s_back)
+                if self.split_fold:
+                    q.enhance_partials(fr_k, stream=self.s_back)
+                else:
+                    q.enhance_owned(fr_k, stream=self.s_back)
                 if self.bilinear == "back":
                     q.scatter_bilinear(fr_k, stream=self.s_back)
                 self.back_done[b].record(self.s_back)
+            if self.split_fold:
+                with torch.cuda.stream(self.s_side):
+                    self.s_side.wait_event(self.front_done[b])
+                    q.scatter_bilinear(fr_k, stream=self.s_side)
+                    self.s_side.wait_event(self.back_done[b])
+                    q.fold_combine(stream=self.s_side)
+                    self.side_done[b].record(self.s_side)
 
     def run_eager(self, imp, frames, n_steps: int, stream=None):
         stream = stream or torch.cuda.current_stream(self.dev)
@@ -157,18 +171,28 @@ class PipelinedRunner:
                 if self.bilinear == "front":
                     q.scatter_bilinear(fr_b, stream=sf)
                     bil_done[b].record(sf)
-            if self.bilinear == "side":
+            if self.bilinear == "side" and not self.split_fold:
                 with torch.cuda.stream(self.s_side):
                     self.s_side.wait_event(self.front_done[b])
                     q.scatter_bilinear(fr_b, stream=self.s_side)
                     bil_done[b].record(self.s_side)
             with torch.cuda.stream(self.s_back):
                 self.s_back.wait_event(self.front_done[b])
-                q.enhance_owned(fr_b, stream=self.s_back)
+                if self.split_fold:
+                    q.enhance_partials(fr_b, stream=self.s_back)
+                else:
+                    q.enhance_owned(fr_b, stream=self.s_back)
                 if self.bilinear == "back":
                     q.scatter_bilinear(fr_b, stream=self.s_back)
                     bil_done[b].record(self.s_back)
                 self.back_done[b].record(self.s_back)
+            if self.split_fold:   # the bilinear pass and the fold's combine; bil_done = the batch's frames complete
+                with torch.cuda.stream(self.s_side):
+                    self.s_side.wait_event(self.front_done[b])
+                    q.scatter_bilinear(fr_b, stream=self.s_side)
+                    self.s_side.wait_event(self.back_done[b])
+                    q.fold_combine(stream=self.s_side)
+                    bil_done[b].record(self.s_side)
             with torch.cuda.stream(s_d2h):
                 s_d2h.wait_event(self.back_done[b])
                 s_d2h.wait_event(bil_done[b])

@@ -3,6 +3,7 @@ seeded inputs. Integer outputs (selection, labels, regions, boxes incl. fp64 den
 placements, bin count, MB owners) must be bit-exact; pixels within 1e-4 (fp32 model) or 2e-2 (bf16
 model) max-abs (BASELINE.json north_star)."""
 import dataclasses
+import os
 
 import numpy as np
 import pytest
@@ -211,6 +212,13 @@ def _check_pixels(wl, seed=5, kind="blobs", box_sample=None, frame_sample=None):
             p.scatter_bilinear(fr_t, out=out_split)
             p.enhance_owned(fr_t, out=out_split)
         assert torch.equal(out_split, out), "regen_enhance_owned + regen_scatter_bilinear differ from the fused call"
+    if wl.sr.bf16 and wl.sr.n_resblocks > 0 and not os.environ.get("REGEN_NO_FOLD"):
+        # the SR half split again (regen_enhance_partials + regen_fold_combine_frames): bit-identical
+        out_split = torch.full_like(out, float("nan"))
+        p.scatter_bilinear(fr_t, out=out_split)
+        p.enhance_partials(fr_t)
+        p.fold_combine(out=out_split)
+        assert torch.equal(out_split, out), "regen_enhance_partials + regen_fold_combine_frames differ"
     g = p.host_results()
     o = _oracle_index(wl, imp)
     _assert_index_equal(g, o)
