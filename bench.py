@@ -317,7 +317,7 @@ def main() -> None:
         return rg.Pipeline(S=wl.S, F=wl.F, W=wl.W, H=wl.H, k=wl.k, bin_w=wl.bin_w, bin_h=wl.bin_h,
                            max_bins=wl.max_bins, partition_mb=wl.partition_mb, scale=wl.sr.scale,
                            channels=wl.sr.channels, n_resblocks=wl.sr.n_resblocks, weights=w, bf16=wl.sr.bf16,
-                           res_scale=wl.sr.res_scale, device=dev)
+                           res_scale=wl.sr.res_scale, device=dev, frame_format=rg.FORMAT_NV12 if nv12 else rg.FORMAT_RGB8)
 
     frames_step = G * wl.S * wl.F          # this rank's frames per step
     stream = torch.cuda.current_stream(dev)
@@ -342,7 +342,7 @@ def main() -> None:
         n_pipes = int(os.environ.get("REGEN_PIPES", n_pipes))
         n_front = int(os.environ.get("REGEN_FRONTS", max(1, n_pipes - 1)))
         split = os.environ.get("REGEN_SPLIT_FOLD", "0") == "1"
-        runner = PipelinedRunner(make_pipe, dev, bilinear=os.environ.get("REGEN_BILINEAR", "side"), nv12=nv12,
+        runner = PipelinedRunner(make_pipe, dev, bilinear=os.environ.get("REGEN_BILINEAR", "side"),
                                  n_pipes=n_pipes, n_front=n_front, split_fold=split)
         pipes = runner.pipes
         p = pipes[0]
@@ -353,7 +353,7 @@ def main() -> None:
 
         def step_instrumented(gi):
             ev[0].record(stream)
-            frames = p.convert_nv12(fr[gi]) if nv12 else fr[gi]
+            frames = fr[gi]   # RGB8, or NV12 read directly by the gather and the bilinear pass
             p.select(imp[gi])
             ev[1].record(stream)
             p.pack_step(imp[gi])
@@ -554,7 +554,7 @@ def main() -> None:
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if strong else "weak", "vs_baseline": None,
             "dtype": "bf16" if wl.sr.bf16 else "f32", "data": "synthetic",
-            "config": {"workload": wl.name + ("_nv12" if nv12 else ""), "input": "NV12 (BT.601 on the GPU in the step)"
+            "config": {"workload": wl.name + ("_nv12" if nv12 else ""), "input": "NV12 (BT.601 fused into the gather and the bilinear pass)"
                        if nv12 else "RGB8", "streams_total": (wl.groups if strong else world) * wl.S,
                        "selection_group_streams": wl.S, "groups_rank0": G, "frames_per_step": int(job_frames),
                        "frame": f"{wl.W}x{wl.H}->x{wl.sr.scale}", "topk_pct": wl.pct,

@@ -70,11 +70,17 @@ enum {
   REGEN_ST_TOPK_INCOMPLETE = 8    /* regen_select_mbs_global before the 4 digit rounds: nothing selected */
 };
 
-/* Frame geometry. MB grid GW = ceil(frame_w/mb), GH = ceil(frame_h/mb) (D1); mb = 16. */
+/* Frame geometry. MB grid GW = ceil(frame_w/mb), GH = ceil(frame_h/mb) (D1); mb = 16.
+ * format: how every call reads the LR frames d_frames: REGEN_FORMAT_RGB8 [S][F][frame_h][frame_w][3],
+ * or REGEN_FORMAT_NV12, the decoder's output: per frame a Y plane [frame_h][frame_w] then the
+ * interleaved U,V plane [frame_h/2][frame_w/2][2], converted to RGB8 by BT.601 (D19) inside the gather
+ * and the bilinear pass (frame_w % 8 == 0, frame_h % 2 == 0). */
+enum { REGEN_FORMAT_RGB8 = 0, REGEN_FORMAT_NV12 = 1 };
 typedef struct {
   int32_t S, F;               /* streams, frames per stream in this call */
   int32_t frame_w, frame_h;   /* LR frame size in pixels */
   int32_t mb;                 /* macroblock size, 16 */
+  int32_t format;             /* REGEN_FORMAT_RGB8 or REGEN_FORMAT_NV12 */
 } regen_geom;
 
 /* Cross-stream MB selection, §3.3.1 P:638-667 (D2). */

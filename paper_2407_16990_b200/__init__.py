@@ -22,6 +22,7 @@ SCOPE_GLOBAL, SCOPE_PER_STREAM, SCOPE_PER_FRAME = 0, 1, 2
 ORDER_DENSITY, ORDER_AREA, ORDER_HEIGHT = 0, 1, 2
 POLICY_GUILLOTINE, POLICY_MAXRECT, POLICY_SKYLINE, POLICY_SHELF = 0, 1, 2, 3
 DENSITY_SPAN, DENSITY_MEMBERS = 0, 1
+FORMAT_RGB8, FORMAT_NV12 = 0, 1
 DTYPE_BF16, DTYPE_FP32 = 0, 1
 CALL_SELECT, CALL_PACK, CALL_ENHANCE, CALL_SCATTER, CALL_ENHANCE_SCATTER, CALL_TEMPORAL = 0, 1, 2, 3, 4, 5
 ST_REGION_OVERFLOW, ST_BOX_OVERFLOW, ST_FREELIST_OVERFLOW, ST_TOPK_INCOMPLETE = 1, 2, 4, 8
@@ -38,7 +39,7 @@ EXPORTED = ["regen_select_mbs", "regen_pack_regions", "regen_sr_create", "regen_
 
 class Geom(ctypes.Structure):
     _fields_ = [("S", ctypes.c_int32), ("F", ctypes.c_int32), ("frame_w", ctypes.c_int32),
-                ("frame_h", ctypes.c_int32), ("mb", ctypes.c_int32)]
+                ("frame_h", ctypes.c_int32), ("mb", ctypes.c_int32), ("format", ctypes.c_int32)]
 
 
 class SelectParams(ctypes.Structure):
@@ -313,10 +314,10 @@ class Pipeline:
     def __init__(self, *, S, F, W, H, k, bin_w, bin_h, max_bins, partition_mb, scale, channels, n_resblocks,
                  weights, bf16=True, res_scale=1.0, mode=MODE_TOPK, tau=0.0, scope=SCOPE_GLOBAL, connectivity=8,
                  expand=3, gutter=1, order=ORDER_DENSITY, max_boxes=None, out_dtype=None, device="cuda", cap=-1,
-                 policy=POLICY_GUILLOTINE, density=DENSITY_SPAN):
+                 policy=POLICY_GUILLOTINE, density=DENSITY_SPAN, frame_format=FORMAT_RGB8):
         import torch
         self.torch = torch
-        self.geom = Geom(S, F, W, H, 16)
+        self.geom = Geom(S, F, W, H, 16, frame_format)   # frame_format NV12: every call reads NV12 frames
         self.sel = SelectParams(mode, scope, k, tau, connectivity, cap)
         self.pack = PackParams(bin_w, bin_h, max_bins, expand, partition_mb, gutter, order, policy, density)
         self.sr = SRNet(scale, channels, n_resblocks, weights, bf16, res_scale, bin_w)
@@ -442,7 +443,7 @@ class Pipeline:
         if getattr(self, "_rgb", None) is None:
             g = self.geom
             self._rgb = t.empty((g.S, g.F, g.frame_h, g.frame_w, 3), dtype=t.uint8, device=self.out.device)
-        nv12_to_rgb8(self.geom, nv12, self._rgb, stream)
+        nv12_to_rgb8(Geom(self.geom.S, self.geom.F, self.geom.frame_w, self.geom.frame_h, 16), nv12, self._rgb, stream)
         return self._rgb
 
     def run(self, importance, frames, out=None, stream=None, fused=True):

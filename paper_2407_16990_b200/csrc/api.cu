@@ -19,6 +19,9 @@ regen_status validate_geom(const regen_geom* g) {
   REGEN_REQUIRE(g->S >= 1 && g->F >= 1, "S and F must be >= 1");
   REGEN_REQUIRE(g->frame_w >= 1 && g->frame_h >= 1 && g->frame_w <= 16384 && g->frame_h <= 16384, "bad frame size");
   REGEN_REQUIRE(g->mb >= 1 && g->mb <= 64, "bad MB size");
+  REGEN_REQUIRE(g->format == REGEN_FORMAT_RGB8 || g->format == REGEN_FORMAT_NV12, "bad frame format %d", g->format);
+  REGEN_REQUIRE(g->format != REGEN_FORMAT_NV12 || (g->frame_w % 8 == 0 && g->frame_h % 2 == 0),
+                "NV12 frames need frame_w %% 8 == 0 and an even frame_h");
   return REGEN_OK;
 }
 

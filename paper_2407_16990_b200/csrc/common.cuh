@@ -96,6 +96,26 @@ struct NvtxRange {
 #define REGEN_NVTX(name) ::regen::NvtxRange nvtx_range_(name)
 
 // ---------------------------------------------------------------- device helpers
+// RGB8 of LR pixel (x, y) of frame `frame` (flat stream*F + frame index), from RGB8 or NV12 frames.
+// NV12: BT.601 limited range in the 8-bit integer form, nearest chroma (D19; nv12.cu, the oracle).
+__device__ __forceinline__ int bt601_clip(int v) { return min(max(v, 0), 255); }
+__device__ __forceinline__ void frame_px(const uint8_t* frames, int format, int64_t frame, int W, int H, int x, int y,
+                                         int& r, int& g, int& b) {
+  if (format == REGEN_FORMAT_NV12) {
+    const uint8_t* Y = frames + frame * ((int64_t)W * H * 3 / 2);
+    const uint8_t* UV = Y + (int64_t)W * H + (int64_t)(y >> 1) * W + 2 * (x >> 1);
+    const int c = 298 * ((int)Y[(int64_t)y * W + x] - 16), d = (int)UV[0] - 128, e = (int)UV[1] - 128;
+    r = bt601_clip((c + 409 * e + 128) >> 8);
+    g = bt601_clip((c - 100 * d - 208 * e + 128) >> 8);
+    b = bt601_clip((c + 516 * d + 128) >> 8);
+  } else {
+    const uint8_t* p = frames + ((frame * H + y) * (int64_t)W + x) * 3;
+    r = p[0];
+    g = p[1];
+    b = p[2];
+  }
+}
+
 __device__ __forceinline__ uint32_t score_ord(float s) {
   uint32_t b = __float_as_uint(s);
   if (s != s) return 0u;          // NaN lowest

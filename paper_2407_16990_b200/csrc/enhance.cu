@@ -198,6 +198,7 @@ struct OwnArgs {          // optional: mark bin pixels whose source MB is owned 
   const int32_t* owner;  // [S][F][GH][GW], null: skip
   int64_t* dst;
   int F, GH, GW, mb, W, H, s;
+  int format;            // REGEN_FORMAT_RGB8 / NV12 of the frames (read by the stitch)
 };
 
 // Grids of the stitch kernels are sized to the GPU, not to the capacities (max_boxes, max_bins):
@@ -265,7 +266,7 @@ __device__ __forceinline__ float from_t<__nv_bfloat16>(__nv_bfloat16 v) { return
 template <typename T, int LAYOUT>
 __global__ void gather_kernel(const uint8_t* frames, const regen_box* boxes, const int32_t* map,
                               const int32_t* num_bins, int bin_w, int bin_h, int F, int W, int H, T* out,
-                              uint32_t* mbits) {
+                              uint32_t* mbits, int format) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int n_rows = *num_bins * bin_h;
   for (int item = blockIdx.y; item < n_rows; item += gridDim.y) {
@@ -284,9 +285,11 @@ __global__ void gather_kernel(const uint8_t* frames, const regen_box* boxes, con
     const int p = x - bx.bx, q = y - bx.by;
     const int sx = bx.rotated ? bx.x0 + q : bx.x0 + p;
     const int sy = bx.rotated ? bx.y0 + bx.h - 1 - p : bx.y0 + q;
-    const uint8_t* src = frames + ((((int64_t)bx.stream * F + bx.frame) * H + sy) * W + sx) * 3;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) v[c] = __fdiv_rn((float)src[c], 255.0f);
+    int cr, cg, cb;
+    frame_px(frames, format, (int64_t)bx.stream * F + bx.frame, W, H, sx, sy, cr, cg, cb);
+    v[0] = __fdiv_rn((float)cr, 255.0f);
+    v[1] = __fdiv_rn((float)cg, 255.0f);
+    v[2] = __fdiv_rn((float)cb, 255.0f);
   }
   if (LAYOUT == 0) {
     T* o = out + (((int64_t)b * bin_h + y) * bin_w + x) * 8;
@@ -395,9 +398,11 @@ __global__ void __launch_bounds__(256) stitch_band_kernel(const uint8_t* frames,
         const int p = x - bx.bx, q = y - bx.by;
         const int sx = bx.rotated ? bx.x0 + q : bx.x0 + p;
         const int sy = bx.rotated ? bx.y0 + bx.h - 1 - p : bx.y0 + q;
-        const uint8_t* src = frames + ((((int64_t)bx.stream * F + bx.frame) * H + sy) * W + sx) * 3;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) v[c] = u8f[src[c]];
+        int cr, cg, cb;   // RGB8, or NV12 converted here (D19): the BT.601 conversion fused into the gather
+        frame_px(frames, oa.format, (int64_t)bx.stream * F + bx.frame, W, H, sx, sy, cr, cg, cb);
+        v[0] = u8f[cr];
+        v[1] = u8f[cg];
+        v[2] = u8f[cb];
         if (oa.owner) {
           const int32_t* ow = oa.owner + ((size_t)bx.stream * oa.F + bx.frame) * oa.GH * oa.GW;
           if (ow[(sy / oa.mb) * oa.GW + sx / oa.mb] == id) {
@@ -627,6 +632,7 @@ regen_status stitch_into(const regen_geom& g, const regen_pack_params& p, int dt
   oa.GH = grid_h(g);
   oa.GW = grid_w(g);
   oa.mb = g.mb;
+  oa.format = g.format;
   static const bool old_stitch = getenv("REGEN_OLD_STITCH") != nullptr;   // A/B aid: clear + paint + gather
   if (lists != nullptr && p.bin_w % 32 == 0 && p.bin_w <= 1024 && !old_stitch) {
     int32_t* cnt = lists;                       // [max_bins + 1] counts, then fill cursors
@@ -673,17 +679,17 @@ regen_status stitch_into(const regen_geom& g, const regen_pack_params& p, int dt
   if (dtype == REGEN_DTYPE_BF16) {
     if (layout == 0)
       gather_kernel<__nv_bfloat16, 0><<<grid, 128, 0, s>>>(d_frames, d_boxes, map, d_num_bins, p.bin_w, p.bin_h, g.F,
-                                                           g.frame_w, g.frame_h, (__nv_bfloat16*)out, mbits);
+                                                           g.frame_w, g.frame_h, (__nv_bfloat16*)out, mbits, g.format);
     else
       gather_kernel<__nv_bfloat16, 1><<<grid, 128, 0, s>>>(d_frames, d_boxes, map, d_num_bins, p.bin_w, p.bin_h, g.F,
-                                                           g.frame_w, g.frame_h, (__nv_bfloat16*)out, mbits);
+                                                           g.frame_w, g.frame_h, (__nv_bfloat16*)out, mbits, g.format);
   } else {
     if (layout == 0)
       gather_kernel<float, 0><<<grid, 128, 0, s>>>(d_frames, d_boxes, map, d_num_bins, p.bin_w, p.bin_h, g.F,
-                                                   g.frame_w, g.frame_h, (float*)out, mbits);
+                                                   g.frame_w, g.frame_h, (float*)out, mbits, g.format);
     else
       gather_kernel<float, 1><<<grid, 128, 0, s>>>(d_frames, d_boxes, map, d_num_bins, p.bin_w, p.bin_h, g.F,
-                                                   g.frame_w, g.frame_h, (float*)out, mbits);
+                                                   g.frame_w, g.frame_h, (float*)out, mbits, g.format);
   }
   REGEN_LAUNCH_CHECK();
   return REGEN_OK;

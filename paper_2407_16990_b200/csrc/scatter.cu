@@ -34,6 +34,7 @@ struct ScatterArgs {
   float inv_s;
   int mode;         // SC_ALL, SC_BILINEAR (owned MBs written elsewhere: the fold combine), SC_OWNED
   int64_t n_frames;
+  int format;       // REGEN_FORMAT_RGB8 / NV12 (converted while the LR pixels are read, D19)
 };
 
 // One CTA per (frame, LR row y) writes the S HR rows S*y .. S*y+S-1. The (at most three) LR rows
@@ -87,6 +88,16 @@ __global__ void __launch_bounds__(SC_THREADS, 8) scatter_rows_kernel(ScatterArgs
   for (int k = 0; k < (MODE == SC_OWNED ? 0 : 3); ++k) {
     const uint8_t* src = img + (size_t)min(max(y - 1 + k, 0), a.H - 1) * W3;
     uint8_t* dst = lr + k * W3p;
+    if (a.format == REGEN_FORMAT_NV12) {   // NV12 -> RGB8 row in SMEM
+      for (int j = threadIdx.x; j < W; j += SC_THREADS) {
+        int cr, cg, cb;
+        frame_px(a.frames, REGEN_FORMAT_NV12, sf, W, a.H, j, min(max(y - 1 + k, 0), a.H - 1), cr, cg, cb);
+        dst[3 * j] = (uint8_t)cr;
+        dst[3 * j + 1] = (uint8_t)cg;
+        dst[3 * j + 2] = (uint8_t)cb;
+      }
+      continue;
+    }
     if ((((uintptr_t)src) & 15) == 0) {
       for (int j = threadIdx.x; j < W3 / 16; j += SC_THREADS)
         reinterpret_cast<uint4*>(dst)[j] = __ldg(reinterpret_cast<const uint4*>(src) + j);
@@ -300,7 +311,7 @@ __global__ void __launch_bounds__(32 * BL_WARPS) bilinear_kernel(ScatterArgs a, 
       // LR columns x0-1 .. x0+8 after the vertical lerp, pre-scaled by 1/255, and the differences
       // of neighbouring columns: each HR value is then one FMA (or a copy at fraction 0)
       float vr[10][3];
-      if (x0 >= 8 && x0 + 9 <= W && ((((uintptr_t)r0) | ((uintptr_t)r1)) & 3) == 0) {
+      if (a.format == REGEN_FORMAT_RGB8 && x0 >= 8 && x0 + 9 <= W && ((((uintptr_t)r0) | ((uintptr_t)r1)) & 3) == 0) {
         const uint32_t* w0 = reinterpret_cast<const uint32_t*>(r0 + 3 * x0 - 4);
         const uint32_t* w1 = reinterpret_cast<const uint32_t*>(r1 + 3 * x0 - 4);
         uint32_t u0[8], u1[8];
@@ -336,13 +347,21 @@ __global__ void __launch_bounds__(32 * BL_WARPS) bilinear_kernel(ScatterArgs a, 
             vf[e + 1] = f2hi(r);
           }
         }
-      } else {   // first / last group of the row: clamped byte loads
+      } else {   // first / last group of the row (clamped byte loads), and NV12 frames (BT.601 on the fly)
 #pragma unroll
         for (int c = 0; c < 10; ++c) {
           const int cx = min(max(x0 - 1 + c, 0), W - 1);
+          int q0[3], q1[3];
+          if (a.format == REGEN_FORMAT_NV12) {
+            frame_px(a.frames, REGEN_FORMAT_NV12, f, W, a.H, cx, yl0, q0[0], q0[1], q0[2]);
+            frame_px(a.frames, REGEN_FORMAT_NV12, f, W, a.H, cx, yl1, q1[0], q1[1], q1[2]);
+          } else {
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) { q0[ch] = __ldg(r0 + 3 * cx + ch); q1[ch] = __ldg(r1 + 3 * cx + ch); }
+          }
 #pragma unroll
           for (int ch = 0; ch < 3; ++ch) {
-            const float p0 = (float)__ldg(r0 + 3 * cx + ch), p1 = (float)__ldg(r1 + 3 * cx + ch);
+            const float p0 = (float)q0[ch], p1 = (float)q1[ch];
             vr[c][ch] = __fmul_rn(fmaf(ly, p1 - p0, p0), 1.0f / 255.0f);
           }
         }
@@ -402,6 +421,7 @@ regen_status scatter_launch(const regen_geom& g, const regen_pack_params& p, int
                             void* d_out, int out_dtype, int mode, cudaStream_t s) {
   ScatterArgs a;
   a.frames = d_frames;
+  a.format = g.format;
   a.boxes = d_boxes;
   a.owner = d_mb_owner;
   a.hr = d_hr_bins;

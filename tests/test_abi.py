@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_struct_layouts():
     import paper_2407_16990_b200 as rg
-    assert ctypes.sizeof(rg.Geom) == 20
+    assert ctypes.sizeof(rg.Geom) == 24
     assert ctypes.sizeof(rg.SelectParams) == 32
     assert ctypes.sizeof(rg.PackParams) == 36
     assert ctypes.sizeof(rg.SRConfig) == 24
@@ -42,7 +42,7 @@ def test_struct_layouts_match_the_c_header(tmp_path):
     import subprocess
     import paper_2407_16990_b200 as rg
     src = tmp_path / "layout.c"
-    fields = {"regen_geom": (rg.Geom, "S F frame_w frame_h mb"),
+    fields = {"regen_geom": (rg.Geom, "S F frame_w frame_h mb format"),
               "regen_select_params": (rg.SelectParams, "mode scope k tau connectivity cap"),
               "regen_pack_params": (rg.PackParams, "bin_w bin_h max_bins expand partition_mb gutter order policy density"),
               "regen_sr_config": (rg.SRConfig, "scale channels n_resblocks dtype res_scale bin_w")}

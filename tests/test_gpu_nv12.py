@@ -31,3 +31,30 @@ def test_pipeline_from_nv12_equals_pipeline_from_rgb():
     a = p.run(imp, p.convert_nv12(torch.from_numpy(nv).cuda())).clone()
     b = p.run(imp, torch.from_numpy(oracle.nv12_to_rgb8(nv, wl.W, wl.H)).cuda())
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("W,H", [(640, 360), (200, 120)])
+def test_nv12_frames_read_directly_equal_the_rgb_path(W, H):
+    """geom.format = NV12: the gather and both bilinear kernels convert while reading (BT.601 fused, D19);
+    every call's HR frames equal the RGB8 path on the oracle-converted frames, bit for bit (fused call,
+    the two halves, and the separate enhance + scatter_blend with the row kernel)."""
+    import dataclasses
+    import paper_2407_16990_b200 as rg
+    wl = dataclasses.replace(synth.small(synth.CONFIGS["c2"], F=2), W=W, H=H)
+    imp = torch.from_numpy(synth.importance_maps(wl.S, wl.F, wl.GH, wl.GW, 5)).cuda()
+    nv = synth.frames_nv12(wl.S, wl.F, wl.H, wl.W, 5)
+    rgb = torch.from_numpy(oracle.nv12_to_rgb8(nv, W, H)).cuda()
+    nv = torch.from_numpy(nv).cuda()
+    w = synth.sr_weights(wl.sr, 0)
+
+    def pipe(fmt):
+        return rg.Pipeline(S=wl.S, F=wl.F, W=W, H=H, k=wl.k, bin_w=128, bin_h=128, max_bins=wl.max_bins,
+                           partition_mb=4, scale=3, channels=32, n_resblocks=2, weights=w, frame_format=fmt)
+    pr, pn = pipe(rg.FORMAT_RGB8), pipe(rg.FORMAT_NV12)
+    ref = pr.run(imp, rgb).clone()
+    assert torch.equal(pn.run(imp, nv), ref)
+    out = torch.full_like(ref, float("nan"))
+    pn.scatter_bilinear(nv, out=out)
+    pn.enhance_owned(nv, out=out)
+    assert torch.equal(out, ref)
+    assert torch.equal(pn.run(imp, nv, fused=False), pr.run(imp, rgb, fused=False))
