@@ -49,7 +49,8 @@ def test_nv12_frames_read_directly_equal_the_rgb_path(W, H):
 
     def pipe(fmt):
         return rg.Pipeline(S=wl.S, F=wl.F, W=W, H=H, k=wl.k, bin_w=128, bin_h=128, max_bins=wl.max_bins,
-                           partition_mb=4, scale=3, channels=32, n_resblocks=2, weights=w, frame_format=fmt)
+                           partition_mb=4, scale=3, channels=32, n_resblocks=wl.sr.n_resblocks, weights=w,
+                           frame_format=fmt)
     pr, pn = pipe(rg.FORMAT_RGB8), pipe(rg.FORMAT_NV12)
     ref = pr.run(imp, rgb).clone()
     assert torch.equal(pn.run(imp, nv), ref)
