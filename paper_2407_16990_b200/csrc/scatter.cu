@@ -450,8 +450,11 @@ regen_status scatter_launch(const regen_geom& g, const regen_pack_params& p, int
                       3 * (((size_t)g.frame_w * 3 + 15) / 16 * 16) + 16;
   REGEN_REQUIRE(smem <= 200 * 1024, "frame too wide for the scatter kernel (%zu B SMEM)", smem);
   const size_t es_out = out_dtype == REGEN_DTYPE_BF16 ? 2 : 4;
-  if (mode == SC_BILINEAR && g.frame_w % 8 == 0 && ((size_t)a.OW * 3 * es_out) % 16 == 0 &&
-      getenv("REGEN_OLD_BILINEAR") == nullptr) {
+  // the warp-per-HR-row bilinear kernel for RGB8 frames; NV12 frames take the row kernel, which converts
+  // each LR row once into SMEM for all S HR rows (measured: equal step time to RGB8, where the warp kernel
+  // re-converting per HR row cost 5 %)
+  if (mode == SC_BILINEAR && g.format == REGEN_FORMAT_RGB8 && g.frame_w % 8 == 0 &&
+      ((size_t)a.OW * 3 * es_out) % 16 == 0 && getenv("REGEN_OLD_BILINEAR") == nullptr) {
     const int ngroups = g.frame_w / 8, nwc = (ngroups + 31) / 32;
     const int64_t items = a.n_frames * a.OH * nwc;
     const unsigned grid2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>((items + BL_WARPS - 1) / BL_WARPS, 148 * 16));
