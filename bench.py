@@ -155,7 +155,8 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------------- CPU oracle
 
-def cpu_oracle_frames(wl: synth.Workload, seed: int, n_frames: int, threads: int, s0: int = 0) -> dict:
+def cpu_oracle_frames(wl: synth.Workload, seed: int, n_frames: int, threads: int, s0: int = 0,
+                      u8: bool = False) -> dict:
     """The oracle as it stands (C, fp64) doing the complete hot path for the first `n_frames` frames
     of one selection-group batch: the index path of the whole batch (selection is over the group,
     P:641), stitch, the SR of every placed box of those frames, and their HR frames (scatter). The
@@ -177,12 +178,15 @@ def cpu_oracle_frames(wl: synth.Workload, seed: int, n_frames: int, threads: int
     keep[mine] = True
     pl[~keep, 0] = -1          # boxes of other frames: not enhanced in this sample
     hr = oracle.enhance(wl.sr, w64, lr, ip["boxes"], pl, threads=threads)
-    oracle.scatter(fr, ip["boxes"], ip["placement"], ip["owner"], hr, wl.sr.scale, wl.bin_w, wl.bin_h, 0, n_frames,
-                   threads=threads)
+    out = oracle.scatter(fr, ip["boxes"], ip["placement"], ip["owner"], hr, wl.sr.scale, wl.bin_w, wl.bin_h, 0,
+                         n_frames, threads=threads)
+    if u8:
+        oracle.quantize_u8(fr, ip["owner"], out, wl.sr.scale, 0, n_frames)
     dt = time.perf_counter() - t0
     return {"value": n_frames / dt, "unit": "frames/s", "cores": threads, "kind": "oracle",
             "sample": f"complete hot path of frames 0..{n_frames - 1} of one {wl.S}x{wl.F}-frame {wl.name} batch "
-                      f"(index path of the whole batch, SR of their {len(mine)} boxes, their HR frames) in "
+                      f"(index path of the whole batch, SR of their {len(mine)} boxes, their "
+                      f"{'u8 ' if u8 else ''}HR frames) in "
                       f"{dt:.1f} s on {threads} host threads",
             "seconds": dt}
 
@@ -205,7 +209,8 @@ def run_reference(args, wl: synth.Workload) -> None:
     nfr = _oracle_frames_for(wl, 4.0, threads)
     vals, last = [], None
     for i in range(args.warmup + args.steps):
-        r = cpu_oracle_frames(wl, seed=i % 3, n_frames=1 if i < args.warmup else nfr, threads=threads)
+        r = cpu_oracle_frames(wl, seed=i % 3, n_frames=1 if i < args.warmup else nfr, threads=threads,
+                              u8=args.out == "u8")
         if i >= args.warmup:
             vals.append(r["value"])
             last = r
@@ -217,7 +222,8 @@ def run_reference(args, wl: synth.Workload) -> None:
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * nfr / v,
             "higher_is_better": True, "scaling": "weak" if wl.groups == 0 else "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": wl.name, "frames_per_step": nfr, "sample": cb["sample"]},
+            "config": {"workload": wl.name + ("_u8out" if args.out == "u8" else ""), "frames_per_step": nfr,
+                       "sample": cb["sample"]},
             "cpu_baseline": cb, "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0,
                                         "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -266,6 +272,8 @@ def main() -> None:
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--dry-run", action="store_true", help="launcher/sharding only (CPU, gloo): print the plan")
+    ap.add_argument("--out", default="bf16", choices=["bf16", "u8"],
+                    help="HR frame type: the model dtype (bf16), or u8 codes (reading D20: clamp, round half to even)")
     ap.add_argument("--input", default="rgb", choices=["rgb", "nv12"],
                     help="frame format: RGB8, or NV12 decoder output converted on the GPU inside the step")
     args = ap.parse_args()
@@ -317,7 +325,8 @@ def main() -> None:
         return rg.Pipeline(S=wl.S, F=wl.F, W=wl.W, H=wl.H, k=wl.k, bin_w=wl.bin_w, bin_h=wl.bin_h,
                            max_bins=wl.max_bins, partition_mb=wl.partition_mb, scale=wl.sr.scale,
                            channels=wl.sr.channels, n_resblocks=wl.sr.n_resblocks, weights=w, bf16=wl.sr.bf16,
-                           res_scale=wl.sr.res_scale, device=dev, frame_format=rg.FORMAT_NV12 if nv12 else rg.FORMAT_RGB8)
+                           res_scale=wl.sr.res_scale, device=dev, frame_format=rg.FORMAT_NV12 if nv12 else rg.FORMAT_RGB8,
+                           out_dtype=rg.DTYPE_U8 if args.out == "u8" else None)
 
     frames_step = G * wl.S * wl.F          # this rank's frames per step
     stream = torch.cuda.current_stream(dev)
@@ -507,7 +516,7 @@ def main() -> None:
                          "sr_network_tflops": box_px * fp / (stage[2] / 1000.0) / 1e12 if stage[2] else None})
         # HBM-bound kernels against the measured copy bandwidth: algorithmic bytes per launch / mean
         # launch time (concurrent replay: includes co-scheduling with the SR stream)
-        es_out = 2 if wl.sr.bf16 else 4
+        es_out = 1 if args.out == "u8" else (2 if wl.sr.bf16 else 4)
         s2 = wl.sr.scale * wl.sr.scale
         lr_bytes = wl.S * wl.F * wl.W * wl.H * 3
         hbm_alg = {"scatter_bilinear": ((s2 * (wl.S * wl.F * wl.W * wl.H * G - sel_px) * 3 * es_out) / max(G, 1)
@@ -554,8 +563,10 @@ def main() -> None:
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if strong else "weak", "vs_baseline": None,
             "dtype": "bf16" if wl.sr.bf16 else "f32", "data": "synthetic",
-            "config": {"workload": wl.name + ("_nv12" if nv12 else ""), "input": "NV12 (BT.601 fused into the gather and the bilinear pass)"
-                       if nv12 else "RGB8", "streams_total": (wl.groups if strong else world) * wl.S,
+            "config": {"workload": wl.name + ("_nv12" if nv12 else "") + ("_u8out" if args.out == "u8" else ""),
+                       "input": "NV12 (BT.601 fused into the gather and the bilinear pass)" if nv12 else "RGB8",
+                       "output": "u8 HR frames (D20: clamp, round half to even)" if args.out == "u8"
+                       else ("bf16" if wl.sr.bf16 else "fp32") + " HR frames", "streams_total": (wl.groups if strong else world) * wl.S,
                        "selection_group_streams": wl.S, "groups_rank0": G, "frames_per_step": int(job_frames),
                        "frame": f"{wl.W}x{wl.H}->x{wl.sr.scale}", "topk_pct": wl.pct,
                        "bins_per_step": int(job_bins), "bin": f"{wl.bin_w}x{wl.bin_h}", "boxes_per_step": int(job_boxes),
@@ -590,7 +601,8 @@ def main() -> None:
         if not args.no_cpu_baseline:
             import oracle
             th = oracle.host_cores()
-            cb = cpu_oracle_frames(wl, seed, _oracle_frames_for(wl, 12.0, th), th, s0=groups[0][0] if groups else 0)
+            cb = cpu_oracle_frames(wl, seed, _oracle_frames_for(wl, 12.0, th), th, s0=groups[0][0] if groups else 0,
+                                   u8=args.out == "u8")
             cb.pop("seconds", None)
             line["cpu_baseline"] = cb
         print(json.dumps(line), flush=True)

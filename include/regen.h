@@ -58,7 +58,11 @@ enum { REGEN_POLICY_GUILLOTINE = 0, REGEN_POLICY_MAXRECT = 1, REGEN_POLICY_SKYLI
 /* importance density of a box (Alg. 1 l.6): SPAN = mean over every MB of the box's MB span (P:751
  * "all MBs in it", D4, default); MEMBERS = mean over its member MBs only (P:691's set notation). */
 enum { REGEN_DENSITY_SPAN = 0, REGEN_DENSITY_MEMBERS = 1 };
-enum { REGEN_DTYPE_BF16 = 0, REGEN_DTYPE_FP32 = 1 };
+/* element types. REGEN_DTYPE_U8 is an output type of the frame-writing calls only (reading D20,
+ * SURVEY §8(c)'s "u8 output (clamp, round-half-even)"): a bilinear pixel is the exact D10 value
+ * rounded half-to-even to a code (computed in integers: 255 * bilinear(u8/255) = N / (2s)^2 exactly),
+ * an enhanced pixel is rhe(255 * clamp(v, 0, 1)) of its value v in the model dtype (exact product). */
+enum { REGEN_DTYPE_BF16 = 0, REGEN_DTYPE_FP32 = 1, REGEN_DTYPE_U8 = 2 };
 enum { REGEN_CALL_SELECT = 0, REGEN_CALL_PACK = 1, REGEN_CALL_ENHANCE = 2, REGEN_CALL_SCATTER = 3,
        REGEN_CALL_ENHANCE_SCATTER = 4, REGEN_CALL_TEMPORAL = 5 };
 
@@ -214,8 +218,8 @@ REGEN_API regen_status regen_enhance_packed(void* sr, const regen_geom* geom, co
 
 /* ---------------------------------------------------------------------------------------------
  * a8. Scatter-and-blend (eq. P:461-464): d_out [S][F][scale*frame_h][scale*frame_w][3]
- * (out_dtype bf16 or fp32) = bilinear x scale of u8/255 (D10), overwritten on the HR square of
- * every MB with d_mb_owner >= 0 by that box's HR bin pixels (un-rotated).
+ * (out_dtype bf16, fp32 or u8 (D20)) = bilinear x scale of u8/255 (D10), overwritten on the HR
+ * square of every MB with d_mb_owner >= 0 by that box's HR bin pixels (un-rotated).
  * ------------------------------------------------------------------------------------------- */
 REGEN_API regen_status regen_scatter_blend(const regen_geom* geom, const regen_pack_params* params, int32_t scale,
                                  const uint8_t* d_frames, const regen_box* d_boxes,

@@ -267,6 +267,22 @@ def scatter(frames: np.ndarray, bx: np.ndarray, placement: np.ndarray, owner: np
     return out
 
 
+def quantize_u8(frames: np.ndarray, owner: np.ndarray, hr_frames: np.ndarray, scale: int, f_lo: int = 0,
+                f_hi: int | None = None, mb: int = 16) -> np.ndarray:
+    """D20 u8 output of O8's frames [f_lo, f_hi): pasted pixels rhe(clamp(v,0,1)*255) of the fp64
+    value, bilinear pixels D10 * 255 exactly (integer weights over (2s)^2), round half to even."""
+    fr = np.ascontiguousarray(frames, np.uint8)
+    S, F, H, W = fr.shape[:4]
+    f_hi = S * F if f_hi is None else f_hi
+    hr = np.ascontiguousarray(hr_frames, np.float64)
+    assert hr.shape == (f_hi - f_lo, scale * H, scale * W, 3)
+    out = np.zeros(hr.shape, np.uint8)
+    rc = lib().ref_quantize_u8(S, F, W, H, mb, scale, _p(fr), _p(np.ascontiguousarray(owner, np.int32)), _p(hr),
+                               ctypes.c_int64(f_lo), ctypes.c_int64(f_hi), _p(out))
+    assert rc == 0
+    return out
+
+
 # ----------------------------------------------------------------------------------- pipeline
 
 def index_path(importance: np.ndarray, W: int, H: int, k: int, *, mode: int = MODE_TOPK, tau: float = 0.0,

@@ -703,6 +703,66 @@ int ref_scatter_mt(int S, int F, int W, int H, int mb, int scale, const uint8_t*
 }
 
 /* ------------------------------------------------------------------------------------------ */
+/* D20 u8 output (SURVEY §8(c) "u8 output (clamp, round-half-even)"): the HR frame of O8 as 8-bit */
+/* codes. A pasted pixel (mb_owner >= 0) of fp64 value v: rhe(clamp(v, 0, 1) * 255). A bilinear   */
+/* pixel: D10's value times 255, exactly: the source coordinate (d + 0.5)/s - 0.5 = (2d + 1 - s)   */
+/* / (2s), clamped at 0, has integer part i0 and fraction a/(2s); the value is N / (2s)^2 with     */
+/* N = (2s-b)((2s-a) p00 + a p01) + b((2s-a) p10 + a p11) over the u8 codes, rounded half to even */
+/* in integers. hr_frames: the fp64 frames of ref_scatter for [f_lo, f_hi); out likewise, u8.     */
+/* ------------------------------------------------------------------------------------------ */
+static int rhe_double(double v) {
+  double c = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+  double x = c * 255.0, fl = floor(x);
+  int q = (int)fl;
+  if (x - fl > 0.5 || (x - fl == 0.5 && (q & 1))) ++q;
+  return q;
+}
+
+static void src_num(int d, int scale, int n, int* i0, int* i1, int* a) {
+  int num = 2 * d + 1 - scale; /* source coordinate times 2s */
+  if (num < 0) num = 0;
+  *i0 = num / (2 * scale);
+  *a = num - 2 * scale * *i0;
+  if (*i0 > n - 1) { *i0 = n - 1; *a = 0; }
+  *i1 = *i0 + 1 < n ? *i0 + 1 : n - 1;
+}
+
+int ref_quantize_u8(int S, int F, int W, int H, int mb, int scale, const uint8_t* frames, const int32_t* mb_owner,
+                    const double* hr_frames, int64_t f_lo, int64_t f_hi, uint8_t* out) {
+  const int GW = grid_w(W, mb), GH = grid_h(H, mb);
+  const int OW = W * scale, OH = H * scale, s2 = 2 * scale, D = s2 * s2;
+  for (int64_t sf = f_lo; sf < f_hi && sf < (int64_t)S * F; ++sf) {
+    const uint8_t* img = frames + sf * (int64_t)H * W * 3;
+    const double* fr = hr_frames + (sf - f_lo) * (int64_t)OH * OW * 3;
+    uint8_t* o = out + (sf - f_lo) * (int64_t)OH * OW * 3;
+    for (int Y = 0; Y < OH; ++Y) {
+      int y0, y1, b;
+      src_num(Y, scale, H, &y0, &y1, &b);
+      for (int X = 0; X < OW; ++X) {
+        const int32_t own = mb_owner[sf * GH * GW + (int64_t)(Y / (mb * scale)) * GW + X / (mb * scale)];
+        for (int c = 0; c < 3; ++c) {
+          const int64_t e = ((int64_t)Y * OW + X) * 3 + c;
+          if (own >= 0) {
+            o[e] = (uint8_t)rhe_double(fr[e]);
+          } else {
+            int x0, x1, a;
+            src_num(X, scale, W, &x0, &x1, &a);
+            const int p00 = img[((int64_t)y0 * W + x0) * 3 + c], p01 = img[((int64_t)y0 * W + x1) * 3 + c];
+            const int p10 = img[((int64_t)y1 * W + x0) * 3 + c], p11 = img[((int64_t)y1 * W + x1) * 3 + c];
+            const int N = (s2 - b) * ((s2 - a) * p00 + a * p01) + b * ((s2 - a) * p10 + a * p11);
+            int q = N / D;
+            const int r = N - q * D;
+            if (2 * r > D || (2 * r == D && (q & 1))) ++q;
+            o[e] = (uint8_t)q;
+          }
+        }
+      }
+    }
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------------------------------------ */
 /* f3. Temporal MB-importance reuse, §3.2.2: the 1/Area operator Phi of one frame's   */
 /* Y-channel residual (Appx D.2 P:1625-1628: "1/Area captures the change of small    */
 /* objects"). Readings (D18): foreground = |residual| > thr; components are           */

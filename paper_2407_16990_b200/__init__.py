@@ -23,7 +23,7 @@ ORDER_DENSITY, ORDER_AREA, ORDER_HEIGHT = 0, 1, 2
 POLICY_GUILLOTINE, POLICY_MAXRECT, POLICY_SKYLINE, POLICY_SHELF = 0, 1, 2, 3
 DENSITY_SPAN, DENSITY_MEMBERS = 0, 1
 FORMAT_RGB8, FORMAT_NV12 = 0, 1
-DTYPE_BF16, DTYPE_FP32 = 0, 1
+DTYPE_BF16, DTYPE_FP32, DTYPE_U8 = 0, 1, 2   # U8: output frames only (D20)
 CALL_SELECT, CALL_PACK, CALL_ENHANCE, CALL_SCATTER, CALL_ENHANCE_SCATTER, CALL_TEMPORAL = 0, 1, 2, 3, 4, 5
 ST_REGION_OVERFLOW, ST_BOX_OVERFLOW, ST_FREELIST_OVERFLOW, ST_TOPK_INCOMPLETE = 1, 2, 4, 8
 TOPK_STATE_BYTES, TOPK_DIGITS = 24, 1 << 16
@@ -347,7 +347,8 @@ class Pipeline:
         self._hr_bins = None   # allocated on first use of the separate enhance/scatter calls
         self.out_dtype = (DTYPE_BF16 if bf16 else DTYPE_FP32) if out_dtype is None else out_dtype
         self.out = torch.empty((S, F, scale * H, scale * W, 3),
-                               dtype=torch.bfloat16 if self.out_dtype == DTYPE_BF16 else torch.float32, device=dev)
+                               dtype={DTYPE_BF16: torch.bfloat16, DTYPE_FP32: torch.float32,
+                                      DTYPE_U8: torch.uint8}[self.out_dtype], device=dev)
 
     @property
     def hr_bins(self):

@@ -116,6 +116,23 @@ __device__ __forceinline__ void frame_px(const uint8_t* frames, int format, int6
   }
 }
 
+// D20 u8 output: code = rhe(255 * clamp(v, 0, 1)), exact. With the magic constant 1.5 * 2^23 one
+// fma rounds the exact product to the nearest integer, ties to even, into the low mantissa bits:
+// u8_code(x, m) = bits(fma(x, m, 1.5 * 2^23)) & 0xff for 0 <= x * m <= 255 exactly representable, or
+// whose distance to a .5 tie exceeds fma's rounding error (the callers below state which).
+// An enhanced pixel: x = its model-dtype value clamped to [0, 1], m = 255 (bf16 x 255 is exact in
+// fp32; an fp32 model value is rounded once, by the fma). A bilinear pixel: x = the exact integer
+// sum N of D10's integer weights (over (2s)^2) and codes, m = 1 / (2s)^2: exact for s = 2, 4 (a
+// power of two), and for s = 3 no tie exists (every weight numerator is even, 255 v = M / 9) and
+// 1/36's rounding moves the product by < 2e-5, far from the nearest .5 (>= 1/18).
+constexpr float U8_MAGIC = 12582912.0f;
+__device__ __forceinline__ uint32_t u8_code(float x, float m) { return __float_as_uint(fmaf(x, m, U8_MAGIC)); }
+// four codes (low bytes) -> one little-endian word
+__device__ __forceinline__ uint32_t pack_u8x4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
+__device__ __forceinline__ uint32_t q_u8(float v) { return u8_code(__saturatef(v), 255.0f) & 0xffu; }
+
 __device__ __forceinline__ uint32_t score_ord(float s) {
   uint32_t b = __float_as_uint(s);
   if (s != s) return 0u;          // NaN lowest

@@ -65,7 +65,7 @@ struct Params {
   const int64_t* fdst;      // [bin][bin_h][bin_w] HR frame index of an owned pixel | rot << 62, else -1
   void* fout;               // HR frames
   const float* tbias;       // tail bias [3]
-  int fout_fp32, fOW;
+  int fout_mode, fOW;
   int ff_debug;             // timing experiments only (REGEN_FF_DEBUG): 1 = skip the combine, 2 = skip its stores
 };
 
@@ -603,7 +603,7 @@ __global__ void __launch_bounds__(ROLE == ROLE_FOLDF ? NTHREADS + 256 : NTHREADS
                 },
                 acc);
             if (p.ff_debug != 2)   // 2: compute but skip the frame stores (timing experiments only)
-              fold::store_frame<PS>(acc, b0, b1, b2, dst, 1, x, y, p.fOW, p.fout, p.fout_fp32);
+              fold::store_frame<PS>(acc, b0, b1, b2, dst, 1, x, y, p.fOW, p.fout, p.fout_mode);
             else {   // keep every accumulator live
               float cs = 0.f;
 #pragma unroll
@@ -1052,7 +1052,7 @@ regen_status fold_fused_launch(const SRNet* net, const void* in, const uint32_t*
   p.fdst = fa.dst;
   p.fout = fa.out;
   p.tbias = net->d_w32 + tail.b_off;
-  p.fout_fp32 = fa.out_dtype == REGEN_DTYPE_FP32 ? 1 : 0;
+  p.fout_mode = fa.out_dtype;
   p.fOW = fa.geom.frame_w * net->cfg.scale;
   {
     const char* e = getenv("REGEN_FF_DEBUG");

@@ -856,7 +856,8 @@ static regen_status enhance_scatter_parts(void* sr, const regen_geom* geom, cons
   REGEN_REQUIRE(d_frames && d_boxes && d_num_boxes && d_num_bins && d_mb_owner && d_out && d_status,
                 "null device pointer");
   REGEN_REQUIRE(max_boxes >= 1 && max_boxes < (1ll << 31), "bad max_boxes");
-  REGEN_REQUIRE(out_dtype == REGEN_DTYPE_BF16 || out_dtype == REGEN_DTYPE_FP32, "bad out dtype");
+  REGEN_REQUIRE(out_dtype == REGEN_DTYPE_BF16 || out_dtype == REGEN_DTYPE_FP32 || out_dtype == REGEN_DTYPE_U8,
+                "bad out dtype");
   const SRNet* net = (const SRNet*)sr;
   st = validate_pack(p, net);
   if (st != REGEN_OK) return st;
@@ -948,7 +949,8 @@ extern "C" regen_status regen_fold_combine_frames(void* sr, const regen_geom* ge
   st = validate_pack(p, net);
   if (st != REGEN_OK) return st;
   REGEN_REQUIRE(d_boxes && d_num_bins && d_mb_owner && d_out, "null device pointer");
-  REGEN_REQUIRE(out_dtype == REGEN_DTYPE_BF16 || out_dtype == REGEN_DTYPE_FP32, "bad out dtype");
+  REGEN_REQUIRE(out_dtype == REGEN_DTYPE_BF16 || out_dtype == REGEN_DTYPE_FP32 || out_dtype == REGEN_DTYPE_U8,
+                "bad out dtype");
   REGEN_UNSUPPORTED_IF(!fold_enabled(net, p->bin_w), "fold_combine_frames needs the UP-TAIL fold");
   EnhanceBufs e = enhance_bufs(net, *p, nullptr, false, n_mbs(*geom));
   REGEN_REQUIRE(d_ws && ws_bytes >= e.bytes, "workspace too small (%zu < %zu)", ws_bytes, e.bytes);

@@ -108,6 +108,32 @@ __device__ __forceinline__ void accumulate_batched(const LD& ld, float (&acc)[PS
   }
 }
 
+// NE u8 codes (low bytes of q) to o, which is A bytes past a 4-B boundary: a head of 1-3 bytes (u8
+// and/or u16), whole 32-bit words, a tail (u16 and/or u8) -- 3 or 4 stores for NE = 9 instead of 9.
+template <int NE, int A>
+__device__ __forceinline__ void store_codes_at(uint8_t* o, const uint32_t (&q)[NE]) {
+  constexpr int H0 = (4 - A) & 3;
+  constexpr int H = H0 < NE ? H0 : NE;
+  if constexpr (H & 1) o[0] = (uint8_t)q[0];
+  if constexpr (H >= 2) *reinterpret_cast<uint16_t*>(o + (H & 1)) = (uint16_t)__byte_perm(q[H & 1], q[(H & 1) + 1], 0x0040);
+  constexpr int NW = (NE - H) / 4;
+#pragma unroll
+  for (int w = 0; w < NW; ++w)
+    *reinterpret_cast<uint32_t*>(o + H + 4 * w) = pack_u8x4(q[H + 4 * w], q[H + 4 * w + 1], q[H + 4 * w + 2], q[H + 4 * w + 3]);
+  constexpr int T = H + 4 * NW, R = NE - T;
+  if constexpr (R >= 2) *reinterpret_cast<uint16_t*>(o + T) = (uint16_t)__byte_perm(q[T], q[T + 1], 0x0040);
+  if constexpr (R & 1) o[NE - 1] = (uint8_t)q[NE - 1];
+}
+template <int NE>
+__device__ __forceinline__ void store_codes(uint8_t* o, const uint32_t (&q)[NE]) {
+  switch ((uintptr_t)o & 3) {
+    case 0: store_codes_at<NE, 0>(o, q); break;
+    case 1: store_codes_at<NE, 1>(o, q); break;
+    case 2: store_codes_at<NE, 2>(o, q); break;
+    default: store_codes_at<NE, 3>(o, q); break;
+  }
+}
+
 // The PS x PS HR block of one LR bin pixel inside the HR frame (D7 un-rotation: bin-HR sub-pixel
 // (i, j) -> frame (j, i) unrotated, (i, PS-1-j) rotated; for res 2 (x4) the block is offset inside
 // the LR pixel's 4x4 square by the res-2 sub-position). Values rounded to bf16 first (bit-identical
@@ -116,7 +142,7 @@ __device__ __forceinline__ void accumulate_batched(const LD& ld, float (&acc)[PS
 // dst = HR frame index of the LR pixel's top-left HR pixel | rotated << 62.
 template <int PS>
 __device__ __forceinline__ void store_frame(const float (&acc)[PS][PS][3], float b0, float b1, float b2, int64_t dst,
-                                            int res, int x, int y, int OW, void* out, int out_fp32) {
+                                            int res, int x, int y, int OW, void* out, int out_mode) {
   const bool rot = (dst >> 62) & 1;
   int64_t base = dst & ((1ll << 62) - 1);
   if (res > 1) {
@@ -134,7 +160,18 @@ __device__ __forceinline__ void store_frame(const float (&acc)[PS][PS][3], float
       v[3 * c + 2] = (rot ? acc[c][PS - 1 - r][2] : acc[r][c][2]) + b2;
     }
     const size_t e0 = (size_t)(base + (int64_t)r * OW) * 3;   // element index of the run
-    if (out_fp32) {
+    if (out_mode == REGEN_DTYPE_U8) {   // D20: quantised from the bf16 value (= the HR-bin round trip)
+      constexpr int NE = 3 * PS;
+      uint32_t q[NE];
+      const __nv_bfloat162 zero = __floats2bfloat162_rn(0.f, 0.f), one = __floats2bfloat162_rn(1.f, 1.f);
+#pragma unroll
+      for (int e = 0; e < NE; e += 2) {   // bf16x2 round + clamp, then the exact x255 and rounding fma
+        const __nv_bfloat162 h = __hmin2(__hmax2(__floats2bfloat162_rn(v[e], e + 1 < NE ? v[e + 1] : 0.f), zero), one);
+        q[e] = u8_code(__low2float(h), 255.0f);
+        if (e + 1 < NE) q[e + 1] = u8_code(__high2float(h), 255.0f);
+      }
+      store_codes<NE>((uint8_t*)out + e0, q);
+    } else if (out_mode == REGEN_DTYPE_FP32) {
       float* o = (float*)out + e0;
 #pragma unroll
       for (int e = 0; e < 3 * PS; ++e) o[e] = __bfloat162float(__float2bfloat16_rn(v[e]));

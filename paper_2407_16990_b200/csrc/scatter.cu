@@ -1,7 +1,7 @@
 // a8: scatter-and-blend, eq. P:461-464 "SR(MB_s) + IN(unselected MBs)", "stitching them
 // back to bi-linear-interpolated non-regions". Every HR pixel is written exactly once: the bilinear
 // value (D10: half-pixel centres, edge clamp, fp32) or, inside the HR square of an owned selected MB,
-// the box's HR bin pixel (un-rotated, D7). Stores are 16-B vectors (bf16) / 32-B (fp32).
+// the box's HR bin pixel (un-rotated, D7). Stores are 16-B vectors; u8 frames (D20) quantise in integers.
 #include <algorithm>
 #include <stdlib.h>
 #include <string.h>
@@ -57,6 +57,8 @@ struct Phase {   // sub-pixel phase j: source offset d (-1 or 0) and fraction
   __host__ __device__ static constexpr float f(int j) {
     return 2 * j + 1 < S ? (float)(1.0 + ((j + 0.5) / S - 0.5)) : (float)((j + 0.5) / S - 0.5);
   }
+  // the fraction as an exact numerator over 2S (D20's integer form): f(j) = num(j) / (2S)
+  __host__ __device__ static constexpr int num(int j) { return 2 * j + 1 < S ? 2 * j + 1 + S : 2 * j + 1 - S; }
 };
 
 template <typename TO>
@@ -75,8 +77,10 @@ __global__ void __launch_bounds__(SC_THREADS, 8) scatter_rows_kernel(ScatterArgs
   const int64_t sf = blockIdx.y;
   const int y = blockIdx.x;
   const int W = a.W, W3 = W * 3;
-  const int npair = (W + 1) / 2;
-  constexpr int WPP = 3 * S * (int)sizeof(TO) / 2;                            // 32-bit words per column pair
+  constexpr bool U8 = sizeof(TO) == 1;
+  constexpr int CPT = U8 ? 4 : 2;                                             // LR columns per thread
+  const int npair = (W + CPT - 1) / CPT;
+  constexpr int WPP = 3 * S * CPT * (int)sizeof(TO) / 4;                      // 32-bit words per unit
   const int row_words = (npair * WPP + 3) / 4 * 4;                            // staging row (16-B multiple)
   const int W3p = (W3 + 15) / 16 * 16;
   float4* vr = reinterpret_cast<float4*>(sm);                                 // [W]
@@ -126,6 +130,20 @@ __global__ void __launch_bounds__(SC_THREADS, 8) scatter_rows_kernel(ScatterArgs
     {
       const uint8_t* r0 = lr + (yl0 - (y - 1)) * W3p;   // slot k holds row clamp(y-1+k)
       const uint8_t* r1 = lr + (yl1 - (y - 1)) * W3p;
+      if constexpr (U8) {   // D20: exact integer vertical sums 2S p0 + b (p1 - p0), ly = b / (2S), in fp32
+        const float b = ly == 0.f ? 0.f : (float)Phase<S>::num(i);   // ly == 0: the edge clamps (above)
+        for (int x = threadIdx.x; x < W; x += SC_THREADS) {
+          float4 v;
+          float p0 = (float)r0[3 * x], p1 = (float)r1[3 * x];
+          v.x = fmaf(b, p1 - p0, (float)(2 * S) * p0);
+          p0 = (float)r0[3 * x + 1]; p1 = (float)r1[3 * x + 1];
+          v.y = fmaf(b, p1 - p0, (float)(2 * S) * p0);
+          p0 = (float)r0[3 * x + 2]; p1 = (float)r1[3 * x + 2];
+          v.z = fmaf(b, p1 - p0, (float)(2 * S) * p0);
+          v.w = 0.f;
+          vr[x] = v;
+        }
+      } else
       for (int x = threadIdx.x; x < W; x += SC_THREADS) {
         float4 v;   // pre-scaled by 1/255 (the same arithmetic as bilinear_kernel: bit-identical pixels)
         float p0 = (float)r0[3 * x], p1 = (float)r1[3 * x];
@@ -141,6 +159,38 @@ __global__ void __launch_bounds__(SC_THREADS, 8) scatter_rows_kernel(ScatterArgs
     __syncthreads();   // vr ready; previous row's copy-out done
     // ---- 2. horizontal pass: a thread per pair of LR columns -> 2*S HR pixels (6*S values, whole
     // 32-bit words; consecutive threads -> consecutive words: no bank conflicts)
+    if constexpr (U8) {   // D20: a thread per 4 LR columns -> 4*S HR pixels = 3*S words
+      constexpr float invD = 1.0f / (float)(4 * S * S);
+      for (int t = threadIdx.x; t < npair; t += SC_THREADS) {
+        const int x0 = 4 * t;
+        float4 v[6];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) v[q] = vr[min(max(x0 - 1 + q, 0), W - 1)];
+        uint32_t o[12 * S];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int x = x0 + q;
+#pragma unroll
+          for (int j = 0; j < S; ++j) {
+            float4 A, B;
+            float n = (float)Phase<S>::num(j);
+            if (Phase<S>::d(j) < 0) {
+              A = v[q]; B = v[q + 1];
+              if (x == 0) { n = 0.f; A = v[q + 1]; }
+            } else {
+              A = v[q + 1]; B = v[q + 2];
+              if (x >= W - 1) n = 0.f;
+            }
+            const int e = 3 * (q * S + j);   // n = 2S A + num (B - A): exact integers in fp32
+            o[e] = u8_code(fmaf(n, B.x - A.x, (float)(2 * S) * A.x), invD);
+            o[e + 1] = u8_code(fmaf(n, B.y - A.y, (float)(2 * S) * A.y), invD);
+            o[e + 2] = u8_code(fmaf(n, B.z - A.z, (float)(2 * S) * A.z), invD);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < WPP; ++k) orow[t * WPP + k] = pack_u8x4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]);
+      }
+    } else
     for (int t = threadIdx.x; t < npair; t += SC_THREADS) {
       const int x0 = 2 * t;
       float4 v[4];
@@ -185,6 +235,9 @@ __global__ void __launch_bounds__(SC_THREADS, 8) scatter_rows_kernel(ScatterArgs
       }
       for (int c = n16 * 16 + threadIdx.x; c < row_bytes; c += SC_THREADS)
         if (own[c / MB_BYTES] < 0) drow[c] = srow[c];
+    } else if (U8) {
+      for (int c = threadIdx.x; c < row_bytes; c += SC_THREADS)
+        if (own[c / MB_BYTES] < 0) drow[c] = srow[c];
     } else {
       for (int c = threadIdx.x; c < row_bytes / 2; c += SC_THREADS)
         if (own[(2 * c) / MB_BYTES] < 0) reinterpret_cast<uint16_t*>(drow)[c] = reinterpret_cast<const uint16_t*>(srow)[c];
@@ -220,7 +273,11 @@ __global__ void __launch_bounds__(SC_THREADS, 8) scatter_rows_kernel(ScatterArgs
         const float4 f = *reinterpret_cast<const float4*>(src + (size_t)k * step);
         f0 = f.x; f1 = f.y; f2 = f.z;
       }
-      if (sizeof(TO) == 2) {
+      if (U8) {   // D20: the model-dtype value, quantised
+        ((uint8_t*)dst)[3 * k] = (uint8_t)q_u8(f0);
+        ((uint8_t*)dst)[3 * k + 1] = (uint8_t)q_u8(f1);
+        ((uint8_t*)dst)[3 * k + 2] = (uint8_t)q_u8(f2);
+      } else if (sizeof(TO) == 2) {
         ((__nv_bfloat16*)dst)[3 * k] = __float2bfloat16_rn(f0);
         ((__nv_bfloat16*)dst)[3 * k + 1] = __float2bfloat16_rn(f1);
         ((__nv_bfloat16*)dst)[3 * k + 2] = __float2bfloat16_rn(f2);
@@ -410,6 +467,113 @@ __global__ void __launch_bounds__(32 * BL_WARPS) bilinear_kernel(ScatterArgs a, 
   }
 }
 
+// The same pass for u8 frames (D20): integer weights over 2S per axis, so a lane's 8*S HR pixels
+// of a row are exact integer sums n = (2S - b)(2S - a) p00 + ... (exact in fp32), each rounded half to
+// even once by u8_code (common.cuh). A group is 24*S bytes; chunks of 16 B may straddle the two
+// groups of one MB, which share the owned flag.
+template <int S>
+__global__ void __launch_bounds__(32 * BL_WARPS) bilinear_u8_kernel(ScatterArgs a, int nwc) {
+  extern __shared__ __align__(16) uint8_t bsm[];
+  constexpr int GB = 24 * S, GW4 = GB / 4;
+  constexpr float invD = 1.0f / (float)(4 * S * S);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* stage = bsm + warp * 32 * GB;
+  const int W = a.W, W3 = 3 * W, GW = a.GW;
+  const int ngroups = W / 8;
+  const int64_t n_items = (int64_t)a.n_frames * a.OH * nwc;
+  for (int64_t it = (int64_t)blockIdx.x * BL_WARPS + warp; it < n_items; it += (int64_t)gridDim.x * BL_WARPS) {
+    const int wc = (int)(it % nwc);
+    const int64_t rowi = it / nwc;
+    const int Y = (int)(rowi % a.OH);
+    const int64_t f = rowi / a.OH;
+    const int g = wc * 32 + lane;
+    const int x0 = 8 * g;
+    const int my = (Y / S) / 16;
+    bool act = g < ngroups;
+    if (act) act = __ldg(a.owner + (f * a.GH + my) * GW + x0 / 16) < 0;
+    const uint32_t amask = __ballot_sync(0xffffffffu, act);
+    if (amask == 0u) continue;
+    if (act) {
+      const int y = Y / S, i = Y - y * S;
+      int yl0 = y + (2 * i + 1 < S ? -1 : 0);
+      int bi = 2 * i + 1 < S ? 2 * i + 1 + S : 2 * i + 1 - S;   // ly = bi / (2S)
+      if (yl0 < 0) { yl0 = 0; bi = 0; }
+      const int yl1 = min(yl0 + 1, a.H - 1);
+      if (yl1 == yl0) bi = 0;
+      const float b = (float)bi;
+      const uint8_t* r0 = a.frames + (f * a.H + yl0) * (int64_t)W3;
+      const uint8_t* r1 = a.frames + (f * a.H + yl1) * (int64_t)W3;
+      // LR columns x0-1 .. x0+8 (clamped): vertical sums 2S p0 + b (p1 - p0), exact integers in fp32
+      float vi[10][3];
+      if (x0 >= 8 && x0 + 9 <= W && ((((uintptr_t)r0) | ((uintptr_t)r1)) & 3) == 0) {
+        const uint32_t* w0 = reinterpret_cast<const uint32_t*>(r0 + 3 * x0 - 4);
+        const uint32_t* w1 = reinterpret_cast<const uint32_t*>(r1 + 3 * x0 - 4);
+        uint32_t u0[8], u1[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) u0[k] = __ldg(w0 + k);
+        if (bi != 0) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) u1[k] = __ldg(w1 + k);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) u1[k] = u0[k];
+        }
+        float* vf = &vi[0][0];
+        const unsigned long long m23 = f2pack(8388608.0f, 8388608.0f), s2 = f2pack(2.0f * S, 2.0f * S);
+        const unsigned long long b2 = f2pack(b, b);
+#pragma unroll
+        for (int e = 0; e < 30; e += 2) {
+          const int b0 = 1 + e, b1 = 2 + e;
+          const unsigned long long q0 = f2pack(__uint_as_float(__byte_perm(u0[b0 >> 2], 0x4B000000u, 0x7650u | (b0 & 3))),
+                                               __uint_as_float(__byte_perm(u0[b1 >> 2], 0x4B000000u, 0x7650u | (b1 & 3))));
+          const unsigned long long q1 = f2pack(__uint_as_float(__byte_perm(u1[b0 >> 2], 0x4B000000u, 0x7650u | (b0 & 3))),
+                                               __uint_as_float(__byte_perm(u1[b1 >> 2], 0x4B000000u, 0x7650u | (b1 & 3))));
+          const unsigned long long p0 = f2sub(q0, m23), p1 = f2sub(q1, m23);
+          const unsigned long long r = f2fma(b2, f2sub(p1, p0), f2mul(s2, p0));
+          vf[e] = f2lo(r);
+          vf[e + 1] = f2hi(r);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 10; ++c) {
+          const int cx = min(max(x0 - 1 + c, 0), W - 1);
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            const float p0 = (float)__ldg(r0 + 3 * cx + ch), p1 = (float)__ldg(r1 + 3 * cx + ch);
+            vi[c][ch] = fmaf(b, p1 - p0, (float)(2 * S) * p0);
+          }
+        }
+      }
+      // horizontal: n = 2S A + num (B - A) (exact), code = rhe(n / (2S)^2) (u8_code); edge clamps
+      // come out of the clamped column loads (A == B)
+      uint32_t o[GB];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+          const int ca = q + 1 + Phase<S>::d(j);
+          const float n = (float)Phase<S>::num(j);
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch)
+            o[3 * (q * S + j) + ch] =
+                u8_code(fmaf(n, vi[ca + 1][ch] - vi[ca][ch], (float)(2 * S) * vi[ca][ch]), invD);
+        }
+      uint32_t* st = reinterpret_cast<uint32_t*>(stage + lane * GB);
+#pragma unroll
+      for (int k = 0; k < GW4; ++k) st[k] = pack_u8x4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]);
+    }
+    __syncwarp();
+    uint8_t* drow = (uint8_t*)a.out + (rowi * a.OW + (int64_t)S * 8 * 32 * wc) * 3;
+#pragma unroll 3
+    for (int k = lane; k < 32 * GB / 16; k += 32) {
+      const int gl = (16 * k) / GB;   // a straddled chunk's two groups share their MB's flag
+      if ((amask >> gl) & 1u)
+        *reinterpret_cast<uint4*>(drow + 16 * k) = *reinterpret_cast<const uint4*>(stage + 16 * k);
+    }
+    __syncwarp();
+  }
+}
+
 }  // namespace regen
 
 using namespace regen;
@@ -443,13 +607,14 @@ regen_status scatter_launch(const regen_geom& g, const regen_pack_params& p, int
   REGEN_REQUIRE(g.mb == 16, "scatter expects 16-pixel MBs");
   REGEN_REQUIRE(scale == 2 || scale == 3 || scale == 4, "scatter scale must be 2, 3 or 4");
   REGEN_REQUIRE(n_frames(g) <= 65535, "scatter: at most 65535 frames per call");
-  const size_t es = out_dtype == REGEN_DTYPE_BF16 ? 2 : 4;
-  const size_t npair = ((size_t)g.frame_w + 1) / 2;
-  const size_t row_words = (npair * 3 * scale * es / 2 + 3) / 4 * 4;
+  const size_t es = out_dtype == REGEN_DTYPE_BF16 ? 2 : (out_dtype == REGEN_DTYPE_U8 ? 1 : 4);
+  const size_t cpt = out_dtype == REGEN_DTYPE_U8 ? 4 : 2;   // LR columns per thread of the row kernel
+  const size_t npair = ((size_t)g.frame_w + cpt - 1) / cpt;
+  const size_t row_words = (npair * 3 * scale * cpt * es / 4 + 3) / 4 * 4;
   const size_t smem = (size_t)g.frame_w * 16 + row_words * 4 + ((size_t)a.GW + 3) / 4 * 16 +
                       3 * (((size_t)g.frame_w * 3 + 15) / 16 * 16) + 16;
   REGEN_REQUIRE(smem <= 200 * 1024, "frame too wide for the scatter kernel (%zu B SMEM)", smem);
-  const size_t es_out = out_dtype == REGEN_DTYPE_BF16 ? 2 : 4;
+  const size_t es_out = es;
   // the warp-per-HR-row bilinear kernel for RGB8 frames; NV12 frames take the row kernel, which converts
   // each LR row once into SMEM for all S HR rows (measured: equal step time to RGB8, where the warp kernel
   // re-converting per HR row cost 5 %)
@@ -467,6 +632,7 @@ regen_status scatter_launch(const regen_geom& g, const regen_pack_params& p, int
     using bf = __nv_bfloat16;
 #define BL_GO(S_)                                                                      \
     if (out_dtype == REGEN_DTYPE_BF16) go2(bilinear_kernel<S_, bf>, BL<S_, bf>::BYTES); \
+    else if (out_dtype == REGEN_DTYPE_U8) go2(bilinear_u8_kernel<S_>, 24 * S_);         \
     else go2(bilinear_kernel<S_, float>, BL<S_, float>::BYTES);
     if (scale == 2) { BL_GO(2) } else if (scale == 3) { BL_GO(3) } else { BL_GO(4) }
 #undef BL_GO
@@ -479,16 +645,21 @@ regen_status scatter_launch(const regen_geom& g, const regen_pack_params& p, int
     kern<<<grid, SC_THREADS, smem, s>>>(a);
   };
   const bool bf_hr = hr_dtype == REGEN_DTYPE_BF16, bf_out = out_dtype == REGEN_DTYPE_BF16;
+  const bool u8_out = out_dtype == REGEN_DTYPE_U8;
   using bf = __nv_bfloat16;
+  using u8 = uint8_t;
 #define SC_DISPATCH(S_, M_)                                                          \
   if (M_ == SC_BILINEAR) {                                                           \
     if (bf_out) go(scatter_rows_kernel<S_, bf, bf, M_>);                             \
+    else if (u8_out) go(scatter_rows_kernel<S_, bf, u8, M_>);                        \
     else go(scatter_rows_kernel<S_, bf, float, M_>);                                 \
   } else if (bf_hr) {                                                                \
     if (bf_out) go(scatter_rows_kernel<S_, bf, bf, M_>);                             \
+    else if (u8_out) go(scatter_rows_kernel<S_, bf, u8, M_>);                        \
     else go(scatter_rows_kernel<S_, bf, float, M_>);                                 \
   } else {                                                                           \
     if (bf_out) go(scatter_rows_kernel<S_, float, bf, M_>);                          \
+    else if (u8_out) go(scatter_rows_kernel<S_, float, u8, M_>);                     \
     else go(scatter_rows_kernel<S_, float, float, M_>);                              \
   }
 #define SC_MODES(S_)                                                                 \
@@ -516,7 +687,8 @@ extern "C" regen_status regen_scatter_blend(const regen_geom* geom, const regen_
   REGEN_REQUIRE(p != nullptr, "pack params null");
   REGEN_REQUIRE(scale >= 2 && scale <= 4, "scale must be 2, 3 or 4");
   REGEN_REQUIRE(hr_dtype == REGEN_DTYPE_BF16 || hr_dtype == REGEN_DTYPE_FP32, "bad hr dtype");
-  REGEN_REQUIRE(out_dtype == REGEN_DTYPE_BF16 || out_dtype == REGEN_DTYPE_FP32, "bad out dtype");
+  REGEN_REQUIRE(out_dtype == REGEN_DTYPE_BF16 || out_dtype == REGEN_DTYPE_FP32 || out_dtype == REGEN_DTYPE_U8,
+                "bad out dtype");
   REGEN_REQUIRE(d_frames && d_boxes && d_mb_owner && d_hr_bins && d_out, "null device pointer");
   return scatter_launch(*geom, *p, scale, d_frames, d_boxes, d_mb_owner, d_hr_bins, hr_dtype, d_out, out_dtype, SC_ALL,
                         (cudaStream_t)stream);
@@ -529,7 +701,8 @@ extern "C" regen_status regen_scatter_bilinear(const regen_geom* geom, int32_t s
   regen_status st = validate_geom(geom);
   if (st != REGEN_OK) return st;
   REGEN_REQUIRE(scale >= 2 && scale <= 4, "scale must be 2, 3 or 4");
-  REGEN_REQUIRE(out_dtype == REGEN_DTYPE_BF16 || out_dtype == REGEN_DTYPE_FP32, "bad out dtype");
+  REGEN_REQUIRE(out_dtype == REGEN_DTYPE_BF16 || out_dtype == REGEN_DTYPE_FP32 || out_dtype == REGEN_DTYPE_U8,
+                "bad out dtype");
   REGEN_REQUIRE(d_frames && d_mb_owner && d_out, "null device pointer");
   regen_pack_params p;
   memset(&p, 0, sizeof(p));

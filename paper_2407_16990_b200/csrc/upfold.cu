@@ -40,7 +40,7 @@ struct FrameOut {
   const regen_box* boxes;
   const int32_t* owner;      // [S][F][GH][GW]
   void* out;
-  int out_fp32;
+  int out_mode;              // REGEN_DTYPE_*
   int F, W, H, GW, GH, mb, s;
 };
 
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(128, 8) combine_kernel(const __nv_bfloat16* P,
       }
     }
   } else {
-    store_frame<PS>(acc, b0, b1, b2, dst, res, x, y, fo.W * fo.s, fo.out, fo.out_fp32);
+    store_frame<PS>(acc, b0, b1, b2, dst, res, x, y, fo.W * fo.s, fo.out, fo.out_mode);
   }
   }
 }
@@ -193,7 +193,7 @@ regen_status fold_combine_launch(const SRNet* net, const void* P, void* hr_bins,
     fo.boxes = fa->boxes;
     fo.owner = fa->owner;
     fo.out = fa->out;
-    fo.out_fp32 = fa->out_dtype == REGEN_DTYPE_FP32;
+    fo.out_mode = fa->out_dtype;
     fo.F = fa->geom.F;
     fo.W = fa->geom.frame_w;
     fo.H = fa->geom.frame_h;
