@@ -8,11 +8,18 @@
 //   y0-1 .. y1 (34 rows) into TMEM ring A; epilogue quad A (warps 2-5) applies bias/ReLU/mask and
 //   writes each t row into an SMEM ring in the UMMA operand layout (generic-proxy stores + proxy fence);
 //   conv_b consumes those t rows from SMEM into TMEM ring B; epilogue quad B (warps 6-9) adds the
-//   residual (r, prefetched from HBM/L2) and stores r'.
+//   residual r and stores r'. The residual rows are bulk-copied into their own SMEM ring by warp 11
+//   (an L2 re-read of rows the producer loaded a few groups earlier), so no global-load latency sits
+//   on the epilogue's path; the occupancy words of a unit's rows are fetched once per unit.
 // Two issuing threads: warp 1 issues conv_a, warp 10 conv_b (each waits only on its own inputs).
 // Synchronisation is per group of G rows: r ring (in_full/in_empty), TMEM ring A and B
-// (acc*_full/acc*_empty), t ring (t_full by quad A, t_empty by tcgen05.commit). TMEM columns are
-// computed at run time from the per-CTA row sequence (no branches in the MMA stream).
+// (acc*_full/acc*_empty), t ring (t_full by quad A, t_empty by tcgen05.commit), residual ring
+// (res_full by the bulk copy, res_empty by quad B).
+// TMEM rings: R logical slots plus GU = 2 guard slots (see RShape); every unit starts at an
+// accumulator sequence that is a multiple of R (the group count per unit is padded with empty
+// "phantom" groups that only cycle the barriers), so a row's TMEM columns, and the split of its sum
+// between slot and guard, depend on its band-local index only: results do not depend on which CTA
+// computed a unit, and every TMEM column in the MMA stream is a compile-time constant.
 // HBM traffic per block: read r (+ its L2-hot re-read as the residual) and write r' once, instead
 // of r, t, t, r, r' for two separate convs.
 #include <stdlib.h>
@@ -26,11 +33,15 @@ namespace tc {
 
 namespace rb {
 
-constexpr int NTHREADS = 352;   // warp 0 producer, 1 conv_a MMAs, 2-9 epilogues, 10 conv_b MMAs
+// warp 0 r-row producer, 1 conv_a MMAs, 2 .. 2+8*EPG-1 epilogues (quad A then quad B, each EPG groups of
+// 4 warps taking alternate accumulator groups), then the conv_b MMA warp and the residual-row producer
+constexpr int EPG = 2;
+constexpr int NEPI = 8 * EPG;              // epilogue warps
+constexpr int W_MMAB = 2 + NEPI, W_RES = 3 + NEPI;
+constexpr int NTHREADS = 32 * (4 + NEPI);
 constexpr int BR = 32;        // output rows per unit
 constexpr int NA_OUT = BR + 2;   // t rows per unit
 constexpr int NA_IN = BR + 4;    // r rows per unit
-constexpr int NSLOT = 4;      // r-ring and t-ring groups (power of two)
 
 struct Params {
   const __nv_bfloat16* in;    // r
@@ -46,42 +57,54 @@ struct Params {
   int* counter;
   unsigned long long* prof;   // REGEN_TC_PROF=1: wait-time counters
   int reverse;                // hand out units last-to-first (L2 reuse along the chain)
-  int dbg;                    // REGEN_RB_DBG bits (timing experiments only): 1 no epilogue work, 2 no row loads, 4 no MMAs
+  int dbg;                    // REGEN_RB_DBG bits (timing experiments only): 1 no epilogue work, 2 no row loads, 4 no MMAs,
+                              // 8 no TMEM loads, 16 no TMEM re-arm stores, 32 no t-row / r' stores, 64 no proxy fence,
+                              // 128 no r' stores, 256 no t-row stores
 };
 
-template <int C, int R, int G>
+// R logical accumulator slots per ring plus GU guard slots (0 or 2) after them: with guards the 3-row
+// window that starts at slot s0 >= R-2 runs on into the guards instead of wrapping to slot 0, so every
+// row issues one N = 3C MMA per step (no 2-MMA split re-reading the A tile); a row at logical slot
+// s < GU then holds part of its sum in guard R+s, which its epilogue adds and re-arms with zero.
+template <int C, int R, int G, int GU>
 struct RShape {
   static constexpr int KC = C / 16, NS = 3 * KC, N = 3 * C;
+  static constexpr int RP = R + GU;                      // physical slots per ring
+  static constexpr int NSLOT = G * C <= 32 ? 8 : 4;      // r-ring and t-ring groups (power of two)
   static constexpr int NGA_IN = (NA_IN + G - 1) / G;
   static constexpr int NGA_OUT = (NA_OUT + G - 1) / G;   // = t groups = conv_b input groups
-
   static constexpr int NGB_OUT = BR / G;
   static constexpr int OGR = R / G;
-  static constexpr int COLB = R * C;                     // TMEM column of ring B
-  static_assert(2 * R * C <= 512 && R % G == 0 && OGR >= 3 && BR % G == 0 && OGR <= 8, "shape");
+  static constexpr int NRES = G == 1 ? 6 : 3;            // residual-ring groups
+  static constexpr int NGA_PAD = (NGA_OUT + OGR - 1) / OGR * OGR;   // + phantom groups
+  static constexpr int NGB_PAD = (NGB_OUT + OGR - 1) / OGR * OGR;
+  static constexpr int COLB = RP * C;                    // TMEM column of ring B
+  static_assert(2 * RP * C <= 512 && R % G == 0 && OGR >= 3 && BR % G == 0 && OGR <= 16, "shape");
+  static_assert(GU == 0 || GU == 2, "guards");
   // input group whose processing completes accumulator group k of a conv with NOUT real rows
   __host__ __device__ static constexpr int done_group(int k, int nout) {
     return ((G * k + G - 1 < nout ? G * k + G - 1 : nout - 1) + 2) / G;
   }
 };
 
-__device__ __forceinline__ uint32_t ring_slot(uint32_t seq, uint32_t Rm) { return (0u - seq) & Rm; }
+// TMEM slot of band-local output row j (every unit starts at a sequence that is a multiple of R)
+template <int R>
+__host__ __device__ constexpr uint32_t ring_slot(int j) { return (uint32_t)((R - j % R) % R); }
 
 // Issue the sliding-window MMAs of one input row: `i` = unit-local input row, `nout` = number of real
-// output rows, `seq0` = accumulator sequence of the unit's output row 0, `tmem` = TMEM column of the
-// ring, `a_row16` = the row's SMEM address (16-B units), `b16` = B image base (16-B units).
-template <int C, int R, int G>
-__device__ __forceinline__ void issue_row(int i, int nout, uint32_t seq0, uint32_t tmem, uint32_t a_row16,
-                                         uint32_t b16, uint32_t en) {
-  using S = RShape<C, R, G>;
-  constexpr uint32_t Rm = R - 1;
+// output rows, `tmem` = TMEM column of the ring, `a_row16` = the row's SMEM address (16-B units),
+// `b16` = B image base (16-B units). Every column is a compile-time constant after unrolling.
+template <int C, int R, int G, int GU>
+__device__ __forceinline__ void issue_row(int i, int nout, uint32_t tmem, uint32_t a_row16, uint32_t b16,
+                                         uint32_t en) {
+  using S = RShape<C, R, G, GU>;
   constexpr uint32_t BLBO = (uint32_t)S::N;
   const int gA = i < nout ? 0 : (i - 1 < nout ? 1 : 2);
   const int gB = i >= 2 ? 3 : (i >= 1 ? 2 : 1);
   if (gA >= gB) return;   // compile-time after unrolling
   const uint32_t ng = (uint32_t)(gB - gA);
-  const uint32_t s0 = ring_slot(seq0 + (uint32_t)(i - gA), Rm);
-  const uint32_t len1 = min(ng, (uint32_t)R - s0);
+  const uint32_t s0 = ring_slot<R>(i - gA);
+  const uint32_t len1 = GU ? ng : min(ng, (uint32_t)R - s0);   // guards: never split
   const uint32_t two = (len1 < ng && en) ? 1u : 0u;
   const uint32_t idesc1 = make_idesc((int)(len1 * C)), idesc2 = make_idesc((int)((ng - len1) * C));
   const uint32_t d1 = tmem + s0 * (uint32_t)C;
@@ -91,19 +114,52 @@ __device__ __forceinline__ void issue_row(int i, int nout, uint32_t seq0, uint32
     const uint32_t a_lo = (a_row16 + (uint32_t)(plane * 128) + (uint32_t)dx) + (128u << 16);   // LBO = plane
     const uint32_t b_lo = (b16 + (uint32_t)(st * S::N * 2) + (uint32_t)(gA * C)) + (BLBO << 16);
     mma_bf16(d1, a_lo, b_lo, idesc1, en);
-    mma_bf16(tmem, a_lo, b_lo + len1 * (uint32_t)C, idesc2, two);
+    if (!GU) mma_bf16(tmem, a_lo, b_lo + len1 * (uint32_t)C, idesc2, two);
   }
 }
 
-template <int C, int R, int G>
+// an accumulator row (C fp32 columns) into registers; a row with part of its sum in a guard slot
+// (warp-uniform `guarded`) adds the guard's columns
+template <int C, int GU>
+__device__ __forceinline__ void load_row(uint32_t taddr, uint32_t gaddr, bool guarded, uint32_t (&r)[C]) {
+  if constexpr (C % 32 == 0) {
+#pragma unroll
+    for (int c = 0; c < C; c += 32) tmem_ld32(taddr + (uint32_t)c, r + c);
+  } else {
+#pragma unroll
+    for (int c = 0; c < C; c += 16) tmem_ld16(taddr + (uint32_t)c, r + c);
+  }
+  tmem_ld_wait();
+  if (GU > 0 && guarded) {   // 16 guard columns at a time (register pressure)
+#pragma unroll
+    for (int c = 0; c < C; c += 16) {
+      uint32_t g[16];
+      tmem_ld16(gaddr + (uint32_t)c, g);
+      tmem_ld_wait();
+#pragma unroll
+      for (int e = 0; e < 16; ++e) r[c + e] = __float_as_uint(__uint_as_float(r[c + e]) + __uint_as_float(g[e]));
+    }
+  }
+}
+template <int C>
+__device__ __forceinline__ void rearm_zero(uint32_t gaddr) {
+  float z[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) z[e] = 0.f;
+#pragma unroll
+  for (int c = 0; c < C; c += 16) tmem_st16(gaddr + (uint32_t)c, z);
+}
+
+template <int C, int R, int G, int GU>
 __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_constant__ Params p) {
-  using S = RShape<C, R, G>;
+  using S = RShape<C, R, G, GU>;
+  constexpr int NSLOT = S::NSLOT, NRES = S::NRES;
   constexpr int ROW_BYTES = (C / 8) * 128 * 16;
   constexpr int GRP = G * ROW_BYTES;
-  constexpr uint32_t Rm = R - 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t in_full[NSLOT], in_empty[NSLOT], t_full[NSLOT], t_empty[NSLOT];
-  __shared__ __align__(8) uint64_t a_full[8], a_empty[8], b_fullacc[8], b_emptyacc[8];
+  __shared__ __align__(8) uint64_t a_full[16], a_empty[16], b_fullacc[16], b_emptyacc[16];
+  __shared__ __align__(8) uint64_t res_full[NRES], res_empty[NRES];
   __shared__ __align__(8) uint64_t w_full;
   __shared__ __align__(8) uint64_t unit_full[4], unit_empty[4];
   __shared__ int unit_ring[4];
@@ -114,6 +170,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
   uint8_t* rring = smem_raw + 1024;
   uint8_t* tring = rring + NSLOT * GRP;
   uint8_t* wimg = tring + NSLOT * GRP;
+  uint8_t* resring = wimg + 2 * p.b_bytes;
   const int nbins = min(*p.num_bins, p.max_bins);
   const int total_units = nbins * p.nbands;
 
@@ -126,8 +183,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
       mbar_init(&a_full[i], 1); mbar_init(&a_empty[i], 4);
       mbar_init(&b_fullacc[i], 1); mbar_init(&b_emptyacc[i], 4);
     }
+    for (int i = 0; i < NRES; ++i) { mbar_init(&res_full[i], 1); mbar_init(&res_empty[i], 4); }
     mbar_init(&w_full, 1);
-    for (int i = 0; i < 4; ++i) { mbar_init(&unit_full[i], 1); mbar_init(&unit_empty[i], 10); }
+    for (int i = 0; i < 4; ++i) { mbar_init(&unit_full[i], 1); mbar_init(&unit_empty[i], 3 + NEPI); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -145,23 +203,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
-  // arm both accumulator rings with their biases
-  if (warp >= 2 && warp < 10) {
-    const int quad = (warp - 2) >> 2, q4 = warp & 3;
-    for (int s = 0; s < R; ++s)
+  // arm both accumulator rings with their biases (guard slots with zero)
+  if (warp >= 2 && warp < 2 + NEPI && ((warp - 2) >> 2) % EPG == 0) {
+    const int quad = (warp - 2) >> 2 >= EPG ? 1 : 0, q4 = warp & 3;
+    float z[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) z[e] = 0.f;
+    for (int s = 0; s < S::RP; ++s)
 #pragma unroll
       for (int c0 = 0; c0 < C; c0 += 16)
-        tmem_st16(tmem + ((uint32_t)(32 * q4) << 16) + (uint32_t)(quad * S::COLB + s * C + c0), bias_sm[quad] + c0);
+        tmem_st16(tmem + ((uint32_t)(32 * q4) << 16) + (uint32_t)(quad * S::COLB + s * C + c0),
+                  s < R ? bias_sm[quad] + c0 : z);
     tmem_st_wait();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  long long w_ae = 0, w_if = 0, w_be = 0, w_tf = 0, w_ea = 0, w_te = 0, w_eb = 0;
+  uint32_t w_ae = 0, w_if = 0, w_be = 0, w_tf = 0, w_ea = 0, w_te = 0, w_eb = 0, w_rs = 0;
   const long long pstart = clock64();
 
   if (warp == 0) {
-    // =============================== producer ===============================
+    // =============================== producer: r rows ===============================
     if (lane == 0) {
       mbar_expect_tx(&w_full, 2 * p.b_bytes);
       bulk_g2s(wimg, p.wimg, 2 * p.b_bytes, &w_full);
@@ -193,14 +255,39 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
         }
       }
     }
-  } else if (warp == 1 || warp == 10) {
+  } else if (warp == W_RES) {
+    // =============================== producer: residual rows (quad B's r) ===============================
+    if (lane == 0) {
+      uint32_t rs = 0;
+      for (uint32_t us = 0;; ++us) {
+        mbar_wait(&unit_full[us & 3], (us >> 2) & 1);
+        const int u = *(volatile int*)&unit_ring[us & 3];
+        mbar_arrive(&unit_empty[us & 3]);
+        if (u < 0) break;
+        const int bin = u / p.nbands, y0 = (u - bin * p.nbands) * BR;
+        const int nrows = min(BR, p.Hr - y0);
+        for (int jb = 0; jb < S::NGB_OUT; ++jb, ++rs) {
+          const uint32_t slot = rs % NRES;
+          mbar_wait(&res_empty[slot], ((rs / NRES) & 1) ^ 1);
+          const int a = G * jb, n = min(G, nrows - a);
+          if (n > 0 && !(p.dbg & 1)) {
+            mbar_expect_tx(&res_full[slot], (uint32_t)n * ROW_BYTES);
+            bulk_g2s(resring + slot * GRP, p.in + ((size_t)bin * p.Hr + y0 + a) * (ROW_BYTES / 2),
+                     (uint32_t)n * ROW_BYTES, &res_full[slot]);
+          } else {
+            mbar_arrive(&res_full[slot]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1 || warp == W_MMAB) {
     // =============================== MMA issuers: conv_a (warp 1), conv_b (warp 10) ===============
     // Two issuing threads, so a conv_b wait for a t row never holds back conv_a's MMAs (tcgen05.commit
     // tracks the MMAs of the committing thread only).
     if (elect_one()) {
       const bool conv_a = warp == 1;
       uint32_t ig = 0, tg = 0;      // r-ring groups consumed, t-ring groups consumed
-      uint32_t qa = 0, qb = 0;      // accumulator group sequences (ring A, ring B)
+      uint32_t qa = 0, qb = 0;      // accumulator group sequences (ring A, ring B; multiples of OGR per unit)
       const uint32_t r16 = smem_u32(rring) >> 4, t16 = smem_u32(tring) >> 4;
       const uint32_t ba16 = smem_u32(wimg) >> 4, bb16 = (smem_u32(wimg) + p.b_bytes) >> 4;
       mbar_wait(&w_full, 0);
@@ -213,13 +300,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
         const int y1 = min(p.Hr, y0 + BR);
         const int rlo = max(y0 - 2, 0), rhi = min(y1 + 1, p.Hr - 1);
         if (conv_a) {
-          const uint32_t seqA = qa * G;
 #pragma unroll
           for (int k = 0; k < S::NGA_IN; ++k) {
             // ---- conv_a, input group k: r rows y0-2 + G*k ...
             const uint32_t slot = (ig + k) & (NSLOT - 1);
-            if (k < S::NGA_OUT) { const long long t0_ = clock64(); mbar_wait(&a_empty[(qa + k) % S::OGR], (((qa + k) / S::OGR) & 1) ^ 1); if (p.prof) w_ae += clock64() - t0_; }
-            { const long long t0_ = clock64(); mbar_wait(&in_full[slot], ((ig + k) / NSLOT) & 1); if (p.prof) w_if += clock64() - t0_; }
+            if (k < S::NGA_OUT) { const uint32_t t0_ = (uint32_t)clock(); mbar_wait(&a_empty[(qa + k) % S::OGR], (((qa + k) / S::OGR) & 1) ^ 1); if (p.prof) w_ae += (uint32_t)clock() - t0_; }
+            { const uint32_t t0_ = (uint32_t)clock(); mbar_wait(&in_full[slot], ((ig + k) / NSLOT) & 1); if (p.prof) w_if += (uint32_t)clock() - t0_; }
             tc_fence_after();
 #pragma unroll
             for (int ii = 0; ii < G; ++ii) {
@@ -227,7 +313,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
               if (i >= NA_IN) continue;
               const int r = y0 - 2 + i;
               const uint32_t en = (r >= rlo && r <= rhi && !(p.dbg & 4)) ? 1u : 0u;
-              issue_row<C, R, G>(i, NA_OUT, seqA, tmem, r16 + slot * (GRP / 16) + ii * (ROW_BYTES / 16), ba16, en);
+              issue_row<C, R, G, GU>(i, NA_OUT, tmem, r16 + slot * (GRP / 16) + ii * (ROW_BYTES / 16), ba16, en);
             }
             mma_commit(&in_empty[slot]);
 #pragma unroll
@@ -239,14 +325,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
                 if (S::done_group(ka, NA_OUT) > k) mma_commit(&a_full[(qa + ka) % S::OGR]);
             }
           }
+#pragma unroll
+          for (int ka = S::NGA_OUT; ka < S::NGA_PAD; ++ka) {   // phantom groups: cycle the barriers only
+            mbar_wait(&a_empty[(qa + ka) % S::OGR], (((qa + ka) / S::OGR) & 1) ^ 1);
+            mma_commit(&a_full[(qa + ka) % S::OGR]);
+          }
         } else {
-          const uint32_t seqB = qb * G;
 #pragma unroll
           for (int kb = 0; kb < S::NGA_OUT; ++kb) {
             // ---- conv_b, input group kb: t rows y0-1 + G*kb ... (SMEM t ring)
             const uint32_t tslot = (tg + kb) & (NSLOT - 1);
-            if (kb < S::NGB_OUT) { const long long t0_ = clock64(); mbar_wait(&b_emptyacc[(qb + kb) % S::OGR], (((qb + kb) / S::OGR) & 1) ^ 1); if (p.prof) w_be += clock64() - t0_; }
-            { const long long t0_ = clock64(); mbar_wait(&t_full[tslot], ((tg + kb) / NSLOT) & 1); if (p.prof) w_tf += clock64() - t0_; }
+            if (kb < S::NGB_OUT) { const uint32_t t0_ = (uint32_t)clock(); mbar_wait(&b_emptyacc[(qb + kb) % S::OGR], (((qb + kb) / S::OGR) & 1) ^ 1); if (p.prof) w_be += (uint32_t)clock() - t0_; }
+            { const uint32_t t0_ = (uint32_t)clock(); mbar_wait(&t_full[tslot], ((tg + kb) / NSLOT) & 1); if (p.prof) w_tf += (uint32_t)clock() - t0_; }
             tc_fence_after();
 #pragma unroll
             for (int ii = 0; ii < G; ++ii) {
@@ -254,8 +344,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
               if (i >= NA_OUT) continue;
               const int tr = y0 - 1 + i;
               const uint32_t en = (tr >= 0 && tr < p.Hr && !(p.dbg & 4)) ? 1u : 0u;
-              issue_row<C, R, G>(i, BR, seqB, tmem + S::COLB, t16 + tslot * (GRP / 16) + ii * (ROW_BYTES / 16), bb16,
-                                 en);
+              issue_row<C, R, G, GU>(i, BR, tmem + S::COLB, t16 + tslot * (GRP / 16) + ii * (ROW_BYTES / 16), bb16, en);
             }
             mma_commit(&t_empty[tslot]);
 #pragma unroll
@@ -267,24 +356,31 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
                 if (S::done_group(jb, BR) > kb) mma_commit(&b_fullacc[(qb + jb) % S::OGR]);
             }
           }
+#pragma unroll
+          for (int jb = S::NGB_OUT; jb < S::NGB_PAD; ++jb) {   // phantom groups
+            mbar_wait(&b_emptyacc[(qb + jb) % S::OGR], (((qb + jb) / S::OGR) & 1) ^ 1);
+            mma_commit(&b_fullacc[(qb + jb) % S::OGR]);
+          }
         }
         ig += S::NGA_IN;
         tg += S::NGA_OUT;
-        qa += S::NGA_OUT;
-        qb += S::NGB_OUT;
+        qa += S::NGA_PAD;
+        qb += S::NGB_PAD;
       }
     }
     __syncwarp();
   } else {
     // =============================== epilogues ===============================
-    const int quad = (warp - 2) >> 2;        // 0: t = relu(conv_a) -> SMEM; 1: r' = r + s*conv_b -> HBM
+    const int egrp = (warp - 2) >> 2;
+    const int quad = egrp >= EPG ? 1 : 0;    // 0: t = relu(conv_a) -> SMEM; 1: r' = r + s*conv_b -> HBM
+    const int par = egrp % EPG;              // this group takes accumulator groups par, par + EPG, ...
     const int q4 = warp & 3;
     const int m = 32 * q4 + lane;
     const uint32_t lane_off = (uint32_t)(32 * q4) << 16;
     const int words = p.bin_w / 32;
     const size_t bin_px = (size_t)p.Hr * 128;
     constexpr size_t PSTRIDE = 128 * 8;      // elements between planes of one row
-    uint32_t tg = 0, qa = 0, qb = 0;
+    uint32_t tg = 0, qa = 0, qb = 0, rs = 0;
     for (uint32_t us = 0;; ++us) {
       mbar_wait(&unit_full[us & 3], (us >> 2) & 1);
       const int u = *(volatile int*)&unit_ring[us & 3];
@@ -293,105 +389,142 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
       if (u < 0) break;
       const int bin = u / p.nbands, y0 = (u - bin * p.nbands) * BR;
       const int nrows = min(BR, p.Hr - y0);
+      const uint32_t* mrows = p.mbits + (size_t)bin * p.bin_h * words + q4;   // this warp's 32 pixels
       if (quad == 0) {
-        // ---- t rows y0-1 .. y0+32 into the SMEM t ring
-        const uint32_t seqA = qa * G;
-        for (int ka = 0; ka < S::NGA_OUT; ++ka) {
-          uint32_t occw[G];
-#pragma unroll
-          for (int jj = 0; jj < G; ++jj) {
-            const int tr = min(max(y0 - 1 + G * ka + jj, 0), p.Hr - 1);
-            occw[jj] = __ldg(p.mbits + ((size_t)bin * p.bin_h + tr) * words + m / 32);
+        // ---- t rows y0-1 .. y0+32 into the SMEM t ring; occupancy words of rows ja = lane, 32 + lane
+        const uint32_t occ0 = __ldg(mrows + (size_t)min(max(y0 - 1 + lane, 0), p.Hr - 1) * words);
+        const uint32_t occ1 = __ldg(mrows + (size_t)min(max(y0 + 31 + (lane & 1), 0), p.Hr - 1) * words);
+        for (int ka = par; ka < S::NGA_PAD; ka += EPG) {
+          const uint32_t gi = (qa + ka) % S::OGR, gph = ((qa + ka) / S::OGR) & 1;
+          if (ka >= S::NGA_OUT) {   // phantom group
+            mbar_wait(&a_full[gi], gph);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&a_empty[gi]);
+            continue;
           }
           const uint32_t tslot = (tg + ka) & (NSLOT - 1);
-          { const long long t0_ = clock64(); mbar_wait(&a_full[(qa + ka) % S::OGR], ((qa + ka) / S::OGR) & 1); if (p.prof) w_ea += clock64() - t0_; }
-          { const long long t0_ = clock64(); mbar_wait(&t_empty[tslot], (((tg + ka) / NSLOT) & 1) ^ 1); if (p.prof) w_te += clock64() - t0_; }
+          { const uint32_t t0_ = (uint32_t)clock(); mbar_wait(&a_full[gi], gph); if (p.prof) w_ea += (uint32_t)clock() - t0_; }
           tc_fence_after();
-          uint8_t* trow0 = tring + tslot * GRP;
+          // accumulators -> bias/ReLU/mask/bf16 in registers; slots re-armed and released before the
+          // t-row stores wait for their SMEM slot
+          uint4 q[G][C / 8];
 #pragma unroll
           for (int jj = 0; jj < G; ++jj) {
             const int ja = G * ka + jj;
-            const uint32_t taddr = tmem + lane_off + ring_slot(seqA + (uint32_t)ja, Rm) * (uint32_t)C;
-            if (ja < NA_OUT && !(p.dbg & 1)) {
-              const bool occ = (occw[jj] >> (m & 31)) & 1u;
+            const uint32_t sl = ring_slot<R>(ja);
+            const uint32_t taddr = tmem + lane_off + sl * (uint32_t)C;
+            const uint32_t gaddr = tmem + lane_off + (uint32_t)(R + sl) * (uint32_t)C;   // guard (sl < GU)
+            const uint32_t ow = __shfl_sync(0xffffffffu, ja < 32 ? occ0 : occ1, ja & 31);
+            if (ja < NA_OUT && !(p.dbg & 9)) {
               uint32_t r[C];
-#pragma unroll
-              for (int c = 0; c < C; c += 16) tmem_ld16(taddr + (uint32_t)c, r + c);
-              tmem_ld_wait();
+              load_row<C, GU>(taddr, gaddr, GU > 0 && sl < (uint32_t)GU, r);
+              const bool occ = (ow >> lane) & 1u;
 #pragma unroll
               for (int g = 0; g < C / 8; ++g) {
                 float v[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) v[e] = fmaxf(__uint_as_float(r[8 * g + e]), 0.f);
-                *reinterpret_cast<uint4*>(trow0 + jj * ROW_BYTES + g * 2048 + m * 16) = pack8(v, occ);
+                q[jj][g] = pack8(v, occ);
               }
-            }
+            } else {
 #pragma unroll
-            for (int c = 0; c < C; c += 16) tmem_st16(taddr + (uint32_t)c, bias_sm[0] + c);
+              for (int g = 0; g < C / 8; ++g) q[jj][g] = make_uint4(0, 0, 0, 0);
+            }
+            if (!(p.dbg & 16)) {
+#pragma unroll
+              for (int c = 0; c < C; c += 16) tmem_st16(taddr + (uint32_t)c, bias_sm[0] + c);
+              if (GU > 0 && sl < (uint32_t)GU) rearm_zero<C>(gaddr);
+            }
           }
           tmem_st_wait();
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // t rows -> tensor-core reads
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) {
-            mbar_arrive(&t_full[tslot]);
-            mbar_arrive(&a_empty[(qa + ka) % S::OGR]);
-          }
-        }
-      } else {
-        // ---- r' rows y0 .. y0+31 = r + res_scale * conv_b, masked, to HBM
-        const uint32_t seqB = qb * G;
-        for (int jb = 0; jb < S::NGB_OUT; ++jb) {
-          uint32_t occw[G];
-          uint4 sk[G][C / 8];
+          if (lane == 0) mbar_arrive(&a_empty[gi]);
+          { const uint32_t t0_ = (uint32_t)clock(); mbar_wait(&t_empty[tslot], (((tg + ka) / NSLOT) & 1) ^ 1); if (p.prof) w_te += (uint32_t)clock() - t0_; }
+          uint8_t* trow0 = tring + tslot * GRP;
 #pragma unroll
           for (int jj = 0; jj < G; ++jj) {
-            const int y = min(y0 + G * jb + jj, p.Hr - 1);
-            occw[jj] = __ldg(p.mbits + ((size_t)bin * p.bin_h + y) * words + m / 32);
-            const size_t act = (size_t)bin * bin_px * C + (size_t)y * (C / 8) * PSTRIDE + (size_t)m * 8;
+            const int ja = G * ka + jj;
+            if (ja < NA_OUT && !(p.dbg & 289)) {
 #pragma unroll
-            for (int g = 0; g < C / 8; ++g)
-              sk[jj][g] = (p.dbg & 1) ? make_uint4(0, 0, 0, 0) : *reinterpret_cast<const uint4*>(p.in + act + g * PSTRIDE);
+              for (int g = 0; g < C / 8; ++g) *reinterpret_cast<uint4*>(trow0 + jj * ROW_BYTES + g * 2048 + m * 16) = q[jj][g];
+            }
           }
-          { const long long t0_ = clock64(); mbar_wait(&b_fullacc[(qb + jb) % S::OGR], ((qb + jb) / S::OGR) & 1); if (p.prof) w_eb += clock64() - t0_; }
+          if (!(p.dbg & 64)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // t rows -> tensor-core reads
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&t_full[tslot]);
+        }
+      } else {
+        // ---- r' rows y0 .. y0+31 = r + res_scale * conv_b, masked, to HBM (r from the residual ring)
+        const uint32_t occ0 = __ldg(mrows + (size_t)min(y0 + lane, p.Hr - 1) * words);
+        for (int jb = par; jb < S::NGB_PAD; jb += EPG) {
+          const uint32_t gi = (qb + jb) % S::OGR, gph = ((qb + jb) / S::OGR) & 1;
+          if (jb >= S::NGB_OUT) {   // phantom group
+            mbar_wait(&b_fullacc[gi], gph);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&b_emptyacc[gi]);
+            continue;
+          }
+          const uint32_t rsq = rs + (uint32_t)jb, rslot = rsq % NRES;
+          { const uint32_t t0_ = (uint32_t)clock(); mbar_wait(&res_full[rslot], (rsq / NRES) & 1); if (p.prof) w_rs += (uint32_t)clock() - t0_; }
+          { const uint32_t t0_ = (uint32_t)clock(); mbar_wait(&b_fullacc[gi], gph); if (p.prof) w_eb += (uint32_t)clock() - t0_; }
           tc_fence_after();
+          // accumulators + residual -> bf16 in registers; slots re-armed and released before the stores
+          const uint8_t* res0 = resring + rslot * GRP + m * 16;
+          uint4 q[G][C / 8];
 #pragma unroll
           for (int jj = 0; jj < G; ++jj) {
             const int j = G * jb + jj;
-            const uint32_t taddr = tmem + lane_off + (uint32_t)S::COLB + ring_slot(seqB + (uint32_t)j, Rm) * (uint32_t)C;
-            if (j < nrows && !(p.dbg & 1)) {
-              const int y = y0 + j;
-              const bool occ = (occw[jj] >> (m & 31)) & 1u;
+            const uint32_t sl = ring_slot<R>(j);
+            const uint32_t taddr = tmem + lane_off + (uint32_t)S::COLB + sl * (uint32_t)C;
+            const uint32_t gaddr = tmem + lane_off + (uint32_t)S::COLB + (uint32_t)(R + sl) * (uint32_t)C;
+            const uint32_t ow = __shfl_sync(0xffffffffu, occ0, j & 31);
+            if (j < nrows && !(p.dbg & 9)) {
               uint32_t r[C];
-#pragma unroll
-              for (int c = 0; c < C; c += 16) tmem_ld16(taddr + (uint32_t)c, r + c);
-              tmem_ld_wait();
-              __nv_bfloat16* o = p.out + (size_t)bin * bin_px * C + (size_t)y * (C / 8) * PSTRIDE + (size_t)m * 8;
+              load_row<C, GU>(taddr, gaddr, GU > 0 && sl < (uint32_t)GU, r);
+              const bool occ = (ow >> lane) & 1u;
 #pragma unroll
               for (int g = 0; g < C / 8; ++g) {
+                const uint4 sk = *reinterpret_cast<const uint4*>(res0 + jj * ROW_BYTES + g * 2048);
                 float v[8];
-                const __nv_bfloat162* s2 = reinterpret_cast<const __nv_bfloat162*>(&sk[jj][g]);
+                const __nv_bfloat162* s2 = reinterpret_cast<const __nv_bfloat162*>(&sk);
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                   const float2 f = __bfloat1622float2(s2[e]);
                   v[2 * e] = fmaf(p.res_scale, __uint_as_float(r[8 * g + 2 * e]), f.x);
                   v[2 * e + 1] = fmaf(p.res_scale, __uint_as_float(r[8 * g + 2 * e + 1]), f.y);
                 }
-                *reinterpret_cast<uint4*>(o + g * PSTRIDE) = pack8(v, occ);
+                q[jj][g] = pack8(v, occ);
               }
             }
+            if (!(p.dbg & 16)) {
 #pragma unroll
-            for (int c = 0; c < C; c += 16) tmem_st16(taddr + (uint32_t)c, bias_sm[1] + c);
+              for (int c = 0; c < C; c += 16) tmem_st16(taddr + (uint32_t)c, bias_sm[1] + c);
+              if (GU > 0 && sl < (uint32_t)GU) rearm_zero<C>(gaddr);
+            }
           }
           tmem_st_wait();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&b_emptyacc[(qb + jb) % S::OGR]);
+          if (lane == 0) {
+            mbar_arrive(&b_emptyacc[gi]);
+            mbar_arrive(&res_empty[rslot]);
+          }
+#pragma unroll
+          for (int jj = 0; jj < G; ++jj) {
+            const int j = G * jb + jj;
+            if (j < nrows && !(p.dbg & 169)) {
+              __nv_bfloat16* o = p.out + (size_t)bin * bin_px * C + (size_t)(y0 + j) * (C / 8) * PSTRIDE + (size_t)m * 8;
+#pragma unroll
+              for (int g = 0; g < C / 8; ++g) *reinterpret_cast<uint4*>(o + g * PSTRIDE) = q[jj][g];
+            }
+          }
         }
       }
       tg += S::NGA_OUT;
-      qa += S::NGA_OUT;
-      qb += S::NGB_OUT;
+      qa += S::NGA_PAD;
+      qb += S::NGB_PAD;
+      rs += S::NGB_OUT;
     }
   }
   if (p.prof && lane == 0) {
@@ -400,9 +533,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
       atomicAdd(p.prof + 0, (unsigned long long)tot); atomicAdd(p.prof + 1, (unsigned long long)w_ae);
       atomicAdd(p.prof + 2, (unsigned long long)w_if);
     }
-    if (warp == 10) { atomicAdd(p.prof + 3, (unsigned long long)w_be); atomicAdd(p.prof + 4, (unsigned long long)w_tf); }
-    if (warp >= 2 && warp < 6) { atomicAdd(p.prof + 5, (unsigned long long)w_ea); atomicAdd(p.prof + 6, (unsigned long long)w_te); }
-    if (warp >= 6) atomicAdd(p.prof + 7, (unsigned long long)w_eb);
+    if (warp == W_MMAB) { atomicAdd(p.prof + 3, (unsigned long long)w_be); atomicAdd(p.prof + 4, (unsigned long long)w_tf); }
+    if (warp >= 2 && warp < 2 + 4 * EPG) { atomicAdd(p.prof + 5, (unsigned long long)w_ea); atomicAdd(p.prof + 6, (unsigned long long)w_te); }
+    if (warp >= 2 + 4 * EPG && warp < 2 + NEPI) { atomicAdd(p.prof + 7, (unsigned long long)w_eb); atomicAdd(p.prof + 8, (unsigned long long)w_rs); }
   }
   tc_fence_before();
   __syncthreads();
@@ -517,10 +650,25 @@ regen_status resblock_tc_launch(const SRNet* cnet, int block, const void* in, vo
   }
   void (*kern)(Params) = nullptr;
   int G = 0;
-  if (C == 32) { kern = resblock_tc_kernel<32, 8, 2>; G = 2; }
-  if (C == 16) { kern = resblock_tc_kernel<16, 16, 4>; G = 4; }
+  static const int guards = getenv("REGEN_RB_NOGUARD") ? 0 : 1;   // A/B aid: the wrapping ring
+  int nslot = 0, nres = 0;
+#define RB_PICK(C_, R_, G_, GU_)                                                       \
+  {                                                                                   \
+    kern = resblock_tc_kernel<C_, R_, G_, GU_>;                                       \
+    G = G_;                                                                           \
+    nslot = RShape<C_, R_, G_, GU_>::NSLOT;                                           \
+    nres = RShape<C_, R_, G_, GU_>::NRES;                                             \
+  }
+  if (C == 32) {
+    if (guards) RB_PICK(32, 6, 1, 2) else RB_PICK(32, 8, 1, 0)
+  }
+  if (C == 16) {
+    if (guards) RB_PICK(16, 12, 1, 2) else RB_PICK(16, 16, 1, 0)
+  }
+#undef RB_PICK
   REGEN_REQUIRE(kern != nullptr, "fused resblock: unsupported C=%d", C);
-  const size_t smem = 1024 + 2ull * NSLOT * G * (C / 8) * 128 * 16 + 2ull * p.b_bytes;
+  const size_t grp = (size_t)G * (C / 8) * 128 * 16;
+  const size_t smem = 1024 + 2ull * nslot * grp + 2ull * p.b_bytes + (size_t)nres * grp;
   REGEN_REQUIRE(smem <= 227 * 1024, "fused resblock SMEM %zu", smem);
   REGEN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int grid = std::min(max_bins * p.nbands, net->n_sm);
@@ -528,21 +676,21 @@ regen_status resblock_tc_launch(const SRNet* cnet, int block, const void* in, vo
   const char* pe = getenv("REGEN_TC_PROF");
   const bool prof = pe && pe[0] == '1';
   if (prof) {
-    if (!d_prof) cudaMalloc(&d_prof, 8 * sizeof(unsigned long long));
-    cudaMemsetAsync(d_prof, 0, 8 * sizeof(unsigned long long), s);
+    if (!d_prof) cudaMalloc(&d_prof, 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(d_prof, 0, 16 * sizeof(unsigned long long), s);
     p.prof = d_prof;
   }
   REGEN_TRACE("resblock", s);
   kern<<<grid, NTHREADS, smem, s>>>(p);
   REGEN_LAUNCH_CHECK();
   if (prof) {
-    unsigned long long h[8];
+    unsigned long long h[9];
     cudaMemcpyAsync(h, d_prof, sizeof(h), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     const double g = grid;
     fprintf(stderr, "[rb-prof] mma total %.0f | waits a_empty %.0f in_full %.0f b_empty %.0f t_full %.0f | epiA a_full %.0f "
-            "t_empty %.0f | epiB b_full %.0f (cycles/CTA)\n", h[0] / g, h[1] / g, h[2] / g, h[3] / g, h[4] / g,
-            h[5] / (4 * g), h[6] / (4 * g), h[7] / (4 * g));
+            "t_empty %.0f | epiB b_full %.0f res_full %.0f (cycles/CTA)\n", h[0] / g, h[1] / g, h[2] / g, h[3] / g,
+            h[4] / g, h[5] / (4 * EPG * g), h[6] / (4 * EPG * g), h[7] / (4 * EPG * g), h[8] / (4 * EPG * g));
   }
   return REGEN_OK;
 }

@@ -1,6 +1,8 @@
 import os
 import sys
 
+import gc
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -25,3 +27,15 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+@pytest.fixture(autouse=True)
+def _release_device_memory(request):
+    """GPU tests allocate multi-GB pipelines (full-size workspaces): return them to the device after each
+    test so later tests do not run out of memory behind the caching allocator."""
+    yield
+    if "gpu" in request.keywords:
+        import torch
+        gc.collect()
+        if torch.cuda.is_available():
+            torch.cuda.empty_cache()

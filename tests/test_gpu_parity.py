@@ -212,7 +212,8 @@ def _check_pixels(wl, seed=5, kind="blobs", box_sample=None, frame_sample=None):
             p.scatter_bilinear(fr_t, out=out_split)
             p.enhance_owned(fr_t, out=out_split)
         assert torch.equal(out_split, out), "regen_enhance_owned + regen_scatter_bilinear differ from the fused call"
-    if wl.sr.bf16 and wl.sr.n_resblocks > 0 and not os.environ.get("REGEN_NO_FOLD"):
+    if (wl.sr.bf16 and wl.sr.n_resblocks > 0 and not os.environ.get("REGEN_NO_FOLD")
+            and not os.environ.get("REGEN_FORCE_SIMT")):
         # the SR half split again (regen_enhance_partials + regen_fold_combine_frames): bit-identical
         out_split = torch.full_like(out, float("nan"))
         p.scatter_bilinear(fr_t, out=out_split)

@@ -90,7 +90,7 @@ def test_u8_frames_c2_geometry():
 
 def test_u8_frames_x2_c5_network():
     """x2 (p = 2 fold, C = 64 unfused convs), 720p frames, 10% of the MBs."""
-    wl = dataclasses.replace(synth.small(synth.CONFIGS["c5"], F=1), S=1, pct=10.0)
+    wl = dataclasses.replace(synth.small(synth.CONFIGS["c5"], F=1), S=1, pct=10.0, max_bins=128)   # ~10 bins used
     _check(wl, 32)
 
 
