@@ -171,8 +171,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
   uint8_t* tring = rring + NSLOT * GRP;
   uint8_t* wimg = tring + NSLOT * GRP;
   uint8_t* resring = wimg + 2 * p.b_bytes;
-  const int nbins = min(*p.num_bins, p.max_bins);
-  const int total_units = nbins * p.nbands;
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < NSLOT; ++i) {
@@ -219,6 +217,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  const int nbins = min(*p.num_bins, p.max_bins);
+  const int total_units = nbins * p.nbands;
   uint32_t w_ae = 0, w_if = 0, w_be = 0, w_tf = 0, w_ea = 0, w_te = 0, w_eb = 0, w_rs = 0;
   const long long pstart = clock64();
 
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
             const uint32_t taddr = tmem + lane_off + sl * (uint32_t)C;
             const uint32_t gaddr = tmem + lane_off + (uint32_t)(R + sl) * (uint32_t)C;   // guard (sl < GU)
             const uint32_t ow = __shfl_sync(0xffffffffu, ja < 32 ? occ0 : occ1, ja & 31);
-            if (ja < NA_OUT && !(p.dbg & 9)) {
+            if (ja < NA_OUT && ow != 0u && !(p.dbg & 9)) {   // a segment with no occupied pixel is all zero
               uint32_t r[C];
               load_row<C, GU>(taddr, gaddr, GU > 0 && sl < (uint32_t)GU, r);
               const bool occ = (ow >> lane) & 1u;
@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
             const uint32_t taddr = tmem + lane_off + (uint32_t)S::COLB + sl * (uint32_t)C;
             const uint32_t gaddr = tmem + lane_off + (uint32_t)S::COLB + (uint32_t)(R + sl) * (uint32_t)C;
             const uint32_t ow = __shfl_sync(0xffffffffu, occ0, j & 31);
-            if (j < nrows && !(p.dbg & 9)) {
+            if (j < nrows && ow != 0u && !(p.dbg & 9)) {
               uint32_t r[C];
               load_row<C, GU>(taddr, gaddr, GU > 0 && sl < (uint32_t)GU, r);
               const bool occ = (ow >> lane) & 1u;
@@ -496,6 +496,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) resblock_tc_kernel(const __grid_c
                 }
                 q[jj][g] = pack8(v, occ);
               }
+            } else {
+#pragma unroll
+              for (int g = 0; g < C / 8; ++g) q[jj][g] = make_uint4(0, 0, 0, 0);
             }
             if (!(p.dbg & 16)) {
 #pragma unroll
