@@ -349,6 +349,41 @@ __global__ void bin_fill_kernel(const regen_box* boxes, const int64_t* num_boxes
   }
 }
 
+// the same three steps in one CTA (counts and fill cursors in SMEM): one launch instead of a memset and
+// three on the SR stream; a bin's list order is arbitrary (its boxes do not overlap, so the stitch
+// paints the same band either way)
+__global__ void __launch_bounds__(1024) bin_lists_kernel(const regen_box* boxes, const int64_t* num_boxes,
+                                                         int64_t max_boxes, const int32_t* num_bins, int max_bins,
+                                                         int32_t* off, int32_t* list) {
+  extern __shared__ int32_t bl_cnt[];   // [max_bins + 1]
+  __shared__ int scratch[33];
+  const int n = min(*num_bins, max_bins);
+  const int64_t nbx = min(*num_boxes, max_boxes);
+  for (int i = threadIdx.x; i <= n; i += blockDim.x) bl_cnt[i] = 0;
+  __syncthreads();
+  for (int64_t b = threadIdx.x; b < nbx; b += blockDim.x) {
+    const int bin = boxes[b].bin;
+    if (bin >= 0 && bin < n) atomicAdd(bl_cnt + bin, 1);
+  }
+  __syncthreads();
+  int carry = 0;
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const int c = i < n ? bl_cnt[i] : 0;
+    int tot;
+    const int ex = block_exclusive_scan(c, scratch, &tot);
+    __syncthreads();   // every thread has read its count and the total before the cursors overwrite them
+    if (i < n) { off[i] = carry + ex; bl_cnt[i] = carry + ex; }
+    carry += tot;
+  }
+  if (threadIdx.x == 0) off[n] = carry;
+  __syncthreads();
+  for (int64_t b = threadIdx.x; b < nbx; b += blockDim.x) {
+    const int bin = boxes[b].bin;
+    if (bin >= 0 && bin < n) list[atomicAdd(bl_cnt + bin, 1)] = (int32_t)b;
+  }
+}
+
 template <typename T, int LAYOUT>
 __global__ void __launch_bounds__(256) stitch_band_kernel(const uint8_t* frames, const regen_box* boxes,
                                                           const int32_t* off, const int32_t* list,
@@ -638,9 +673,14 @@ regen_status stitch_into(const regen_geom& g, const regen_pack_params& p, int dt
     int32_t* cnt = lists;                       // [max_bins + 1] counts, then fill cursors
     int32_t* off = lists + p.max_bins + 1;      // [max_bins + 1]
     int32_t* list = off + p.max_bins + 1;       // [max_boxes]
-    const unsigned gb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((max_boxes + 255) / 256, 148 * 4));
-    REGEN_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)p.max_bins + 1), s));
-    {
+    const size_t lsm = sizeof(int32_t) * ((size_t)p.max_bins + 1);
+    if (lsm <= 160 * 1024) {
+      REGEN_TRACE("stitch_lists", s);
+      if (lsm > 48 * 1024) REGEN_CUDA(cudaFuncSetAttribute(bin_lists_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+      bin_lists_kernel<<<1, 1024, lsm, s>>>(d_boxes, d_num_boxes, max_boxes, d_num_bins, p.max_bins, off, list);
+    } else {
+      const unsigned gb = (unsigned)std::max<int64_t>(1, std::min<int64_t>((max_boxes + 255) / 256, 148 * 4));
+      REGEN_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)p.max_bins + 1), s));
       REGEN_TRACE("stitch_lists", s);
       bin_count_kernel<<<gb, 256, 0, s>>>(d_boxes, d_num_boxes, max_boxes, cnt);
       bin_scan_kernel<<<1, 1024, 0, s>>>(d_num_bins, p.max_bins, cnt, off);

@@ -19,4 +19,10 @@ timeout 1500 ncu --set full --clock-control none --import-source on \
 for r in ${TAG}_prof_rb ${TAG}_prof; do
   ncu -i $O/$r.ncu-rep --page raw --csv > $O/$r.raw.csv 2>/dev/null
 done
+# per-kernel source pages (SASS + stall samples) of the multi-kernel capture, then drop its report
+# (gpurun copies back at most 64 MiB)
+for k in stitch_band bilinear_kernel conv_tc_kernel; do
+  ncu -i $O/${TAG}_prof.ncu-rep --page source --csv --print-source sass -k regex:$k > $O/${TAG}_src_$k.csv 2>/dev/null
+done
+rm -f $O/${TAG}_prof.ncu-rep
 ls -la $O | grep $TAG
