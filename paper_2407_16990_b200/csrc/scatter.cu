@@ -323,6 +323,23 @@ __device__ __forceinline__ unsigned long long f2fma(unsigned long long a, unsign
   return r;
 }
 
+// The 8 words holding LR columns x0-1 .. x0+8 of a row at bytes 1 + 3c (c = 0..9), x0 a multiple of 8;
+// the edge clamps (column -1 -> 0 at x0 = 0, column W -> W-1 at x0 = W-8) are built by word moves, so
+// the first and last group of a row take the same instructions as the others (no divergent clamped path
+// in their warps). `row` = the LR row's first byte, 4-B aligned; W >= 16.
+__device__ __forceinline__ void row_window(const uint8_t* row, int x0, int W, uint32_t (&u)[8]) {
+  const bool left = x0 == 0, right = x0 + 9 > W;
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(left ? row : row + 3 * x0 - 4);
+  uint32_t t[8];
+#pragma unroll
+  for (int k = 0; k < 7; ++k) t[k] = __ldg(w + k);
+  t[7] = right ? 0u : __ldg(w + 7);   // past the row at the right edge: not loaded
+  u[0] = left ? t[0] << 8 : t[0];     // window byte b = row byte b - 4 at the left edge, col -1 = col 0
+#pragma unroll
+  for (int k = 1; k < 7; ++k) u[k] = left ? t[k - 1] : t[k];
+  u[7] = left ? t[6] : (right ? t[6] >> 8 : t[7]);   // right edge: col x0+8 = col x0+7 (bytes 25..27)
+}
+
 template <int S, typename TO>
 struct BL {
   static constexpr int VALS = 8 * S * 3;                        // values per group
@@ -339,12 +356,16 @@ __global__ void __launch_bounds__(32 * BL_WARPS) bilinear_kernel(ScatterArgs a, 
   uint8_t* stage = bsm + warp * 32 * G::BYTES;
   const int W = a.W, W3 = 3 * W, GW = a.GW;
   const int ngroups = W / 8;
-  const int64_t n_items = (int64_t)a.n_frames * a.OH * nwc;
-  for (int64_t it = (int64_t)blockIdx.x * BL_WARPS + warp; it < n_items; it += (int64_t)gridDim.x * BL_WARPS) {
-    const int wc = (int)(it % nwc);
-    const int64_t rowi = it / nwc;             // frame * OH + Y
-    const int Y = (int)(rowi % a.OH);
-    const int64_t f = rowi / a.OH;
+  // 32-bit item arithmetic (the host launches this kernel only for < 2^31 items): two 32-bit divisions
+  // per item instead of two calls of the 64-bit division routine
+  const uint32_t n_items = (uint32_t)((int64_t)a.n_frames * a.OH * nwc);
+  for (uint32_t it = blockIdx.x * BL_WARPS + warp; it < n_items; it += gridDim.x * BL_WARPS) {
+    const uint32_t rowi32 = it / (uint32_t)nwc;
+    const int wc = (int)(it - rowi32 * (uint32_t)nwc);
+    const uint32_t f32 = rowi32 / (uint32_t)a.OH;
+    const int64_t rowi = rowi32;             // frame * OH + Y
+    const int Y = (int)(rowi32 - f32 * (uint32_t)a.OH);
+    const int64_t f = f32;
     const int g = wc * 32 + lane;
     const int x0 = 8 * g;
     const int my = (Y / S) / 16;
@@ -368,13 +389,10 @@ __global__ void __launch_bounds__(32 * BL_WARPS) bilinear_kernel(ScatterArgs a, 
       // LR columns x0-1 .. x0+8 after the vertical lerp, pre-scaled by 1/255, and the differences
       // of neighbouring columns: each HR value is then one FMA (or a copy at fraction 0)
       float vr[10][3];
-      if (a.format == REGEN_FORMAT_RGB8 && x0 >= 8 && x0 + 9 <= W && ((((uintptr_t)r0) | ((uintptr_t)r1)) & 3) == 0) {
-        const uint32_t* w0 = reinterpret_cast<const uint32_t*>(r0 + 3 * x0 - 4);
-        const uint32_t* w1 = reinterpret_cast<const uint32_t*>(r1 + 3 * x0 - 4);
+      if (a.format == REGEN_FORMAT_RGB8 && W >= 16 && ((((uintptr_t)r0) | ((uintptr_t)r1)) & 3) == 0) {
         uint32_t u0[8], u1[8];
         if (ly == 0.f) {   // the HR row sits on LR row yl0 (phase fraction 0, or an edge clamp): one row
-#pragma unroll
-          for (int k = 0; k < 8; ++k) u0[k] = __ldg(w0 + k);
+          row_window(r0, x0, W, u0);
 #pragma unroll
           for (int c = 0; c < 10; ++c)
 #pragma unroll
@@ -384,8 +402,8 @@ __global__ void __launch_bounds__(32 * BL_WARPS) bilinear_kernel(ScatterArgs a, 
               vr[c][ch] = __fmul_rn(p0, 1.0f / 255.0f);   // == fmaf(0, p1 - p0, p0) / 255 exactly
             }
         } else {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) { u0[k] = __ldg(w0 + k); u1[k] = __ldg(w1 + k); }
+          row_window(r0, x0, W, u0);
+          row_window(r1, x0, W, u1);
           // the 30 values as 15 pairs, each step one packed fp32x2 instruction (FADD2/FFMA2/FMUL2:
           // per-element IEEE round-to-nearest, bit-identical to the scalar chain of the row kernel)
           float* vf = &vr[0][0];
@@ -480,12 +498,16 @@ __global__ void __launch_bounds__(32 * BL_WARPS) bilinear_u8_kernel(ScatterArgs 
   uint8_t* stage = bsm + warp * 32 * GB;
   const int W = a.W, W3 = 3 * W, GW = a.GW;
   const int ngroups = W / 8;
-  const int64_t n_items = (int64_t)a.n_frames * a.OH * nwc;
-  for (int64_t it = (int64_t)blockIdx.x * BL_WARPS + warp; it < n_items; it += (int64_t)gridDim.x * BL_WARPS) {
-    const int wc = (int)(it % nwc);
-    const int64_t rowi = it / nwc;
-    const int Y = (int)(rowi % a.OH);
-    const int64_t f = rowi / a.OH;
+  // 32-bit item arithmetic (the host launches this kernel only for < 2^31 items): two 32-bit divisions
+  // per item instead of two calls of the 64-bit division routine
+  const uint32_t n_items = (uint32_t)((int64_t)a.n_frames * a.OH * nwc);
+  for (uint32_t it = blockIdx.x * BL_WARPS + warp; it < n_items; it += gridDim.x * BL_WARPS) {
+    const uint32_t rowi32 = it / (uint32_t)nwc;
+    const int wc = (int)(it - rowi32 * (uint32_t)nwc);
+    const uint32_t f32 = rowi32 / (uint32_t)a.OH;
+    const int64_t rowi = rowi32;
+    const int Y = (int)(rowi32 - f32 * (uint32_t)a.OH);
+    const int64_t f = f32;
     const int g = wc * 32 + lane;
     const int x0 = 8 * g;
     const int my = (Y / S) / 16;
@@ -505,15 +527,11 @@ __global__ void __launch_bounds__(32 * BL_WARPS) bilinear_u8_kernel(ScatterArgs 
       const uint8_t* r1 = a.frames + (f * a.H + yl1) * (int64_t)W3;
       // LR columns x0-1 .. x0+8 (clamped): vertical sums 2S p0 + b (p1 - p0), exact integers in fp32
       float vi[10][3];
-      if (x0 >= 8 && x0 + 9 <= W && ((((uintptr_t)r0) | ((uintptr_t)r1)) & 3) == 0) {
-        const uint32_t* w0 = reinterpret_cast<const uint32_t*>(r0 + 3 * x0 - 4);
-        const uint32_t* w1 = reinterpret_cast<const uint32_t*>(r1 + 3 * x0 - 4);
+      if (W >= 16 && ((((uintptr_t)r0) | ((uintptr_t)r1)) & 3) == 0) {
         uint32_t u0[8], u1[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) u0[k] = __ldg(w0 + k);
+        row_window(r0, x0, W, u0);
         if (bi != 0) {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) u1[k] = __ldg(w1 + k);
+          row_window(r1, x0, W, u1);
         } else {
 #pragma unroll
           for (int k = 0; k < 8; ++k) u1[k] = u0[k];
@@ -618,10 +636,11 @@ regen_status scatter_launch(const regen_geom& g, const regen_pack_params& p, int
   // the warp-per-HR-row bilinear kernel for RGB8 frames; NV12 frames take the row kernel, which converts
   // each LR row once into SMEM for all S HR rows (measured: equal step time to RGB8, where the warp kernel
   // re-converting per HR row cost 5 %)
+  const int64_t bl_items = (int64_t)a.n_frames * a.OH * ((g.frame_w / 8 + 31) / 32);
   if (mode == SC_BILINEAR && g.format == REGEN_FORMAT_RGB8 && g.frame_w % 8 == 0 &&
-      ((size_t)a.OW * 3 * es_out) % 16 == 0 && getenv("REGEN_OLD_BILINEAR") == nullptr) {
+      ((size_t)a.OW * 3 * es_out) % 16 == 0 && bl_items < (1ll << 31) && getenv("REGEN_OLD_BILINEAR") == nullptr) {
     const int ngroups = g.frame_w / 8, nwc = (ngroups + 31) / 32;
-    const int64_t items = a.n_frames * a.OH * nwc;
+    const int64_t items = bl_items;
     const unsigned grid2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>((items + BL_WARPS - 1) / BL_WARPS, 148 * 16));
     auto go2 = [&](auto kern, int bytes) {
       const size_t sm2 = (size_t)BL_WARPS * 32 * bytes;
