@@ -474,12 +474,14 @@ __global__ void __launch_bounds__(32 * BL_WARPS) bilinear_kernel(ScatterArgs a, 
     }
     __syncwarp();
     // coalesced copy-out of the warp's run (chunks of groups in owned MBs / past the row are skipped)
-    uint8_t* drow = (uint8_t*)a.out + (rowi * a.OW + (int64_t)S * 8 * 32 * wc) * 3 * (int64_t)sizeof(TO);
-#pragma unroll 3
-    for (int k = lane; k < 32 * G::CHUNKS; k += 32) {
-      const int gl = k / G::CHUNKS;
+    // (fully unrolled: chunk t of a lane sits at a constant offset from the lane's first one)
+    uint8_t* drow = (uint8_t*)a.out + (rowi * a.OW + (int64_t)S * 8 * 32 * wc) * 3 * (int64_t)sizeof(TO) + 16 * lane;
+    const uint8_t* srow = stage + 16 * lane;
+#pragma unroll
+    for (int t = 0; t < G::CHUNKS; ++t) {
+      const int gl = (lane + 32 * t) / G::CHUNKS;
       if ((amask >> gl) & 1u)
-        *reinterpret_cast<uint4*>(drow + 16 * k) = *reinterpret_cast<const uint4*>(stage + 16 * k);
+        *reinterpret_cast<uint4*>(drow + 512 * t) = *reinterpret_cast<const uint4*>(srow + 512 * t);
     }
     __syncwarp();
   }
@@ -582,10 +584,12 @@ __global__ void __launch_bounds__(32 * BL_WARPS) bilinear_u8_kernel(ScatterArgs 
     }
     __syncwarp();
     uint8_t* drow = (uint8_t*)a.out + (rowi * a.OW + (int64_t)S * 8 * 32 * wc) * 3;
-#pragma unroll 3
-    for (int k = lane; k < 32 * GB / 16; k += 32) {
+    constexpr int NCH = 32 * GB / 16;
+#pragma unroll
+    for (int t = 0; t < (NCH + 31) / 32; ++t) {
+      const int k = lane + 32 * t;
       const int gl = (16 * k) / GB;   // a straddled chunk's two groups share their MB's flag
-      if ((amask >> gl) & 1u)
+      if (k < NCH && ((amask >> gl) & 1u))
         *reinterpret_cast<uint4*>(drow + 16 * k) = *reinterpret_cast<const uint4*>(stage + 16 * k);
     }
     __syncwarp();
