@@ -384,33 +384,59 @@ __global__ void __launch_bounds__(1024) bin_lists_kernel(const regen_box* boxes,
   }
 }
 
+// A box of the bin being stitched, as the affine map bin pixel (x, y) -> source pixel (sx, sy):
+// unrotated sx = ax + x, sy = ay + y; rotated (D7) sx = ax + y, sy = ay - x.
+struct StitchBox {
+  int32_t id, ax, ay, rot;
+  int32_t fr;   // stream * F + frame
+};
+constexpr int SB_CACHE = 128;   // boxes of one bin kept in SMEM (more: read from the box records)
+
+__device__ __forceinline__ StitchBox stitch_box(const regen_box& bx, int id, int F) {
+  StitchBox b;
+  b.id = id;
+  b.rot = bx.rotated;
+  b.ax = bx.rotated ? bx.x0 - bx.by : bx.x0 - bx.bx;
+  b.ay = bx.rotated ? bx.y0 + bx.h - 1 + bx.bx : bx.y0 - bx.by;
+  b.fr = bx.stream * F + bx.frame;
+  return b;
+}
+
 template <typename T, int LAYOUT>
 __global__ void __launch_bounds__(256) stitch_band_kernel(const uint8_t* frames, const regen_box* boxes,
                                                           const int32_t* off, const int32_t* list,
                                                           const int32_t* num_bins, int max_bins, int bin_w, int bin_h,
                                                           int F, int W, int H, int32_t* map, T* out, uint32_t* mbits,
                                                           OwnArgs oa) {
+  // band_ids: -1 empty, 0 .. SB_CACHE-1 the bin-local index of a cached box, SB_CACHE + id otherwise
   extern __shared__ int32_t band_ids[];   // [STITCH_BAND][bin_w]
   __shared__ float u8f[256];              // fp32(u8 / 255), correctly rounded (D9): one table load per value
+  __shared__ StitchBox sbox[SB_CACHE];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) u8f[i] = __fdiv_rn((float)i, 255.0f);
   const int nbands = (bin_h + STITCH_BAND - 1) / STITCH_BAND;
   const int items = min(*num_bins, max_bins) * nbands;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   const int npx = STITCH_BAND * bin_w;
   const int words = bin_w / 32;
+  const int64_t OW = (int64_t)oa.W * oa.s, OH = (int64_t)oa.H * oa.s;
+  const int64_t gsz = (int64_t)oa.GH * oa.GW;
+  const bool mb16 = oa.mb == 16;
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
     const int bin = item / nbands, y0 = (item - bin * nbands) * STITCH_BAND;
     const int rows = min(STITCH_BAND, bin_h - y0);
     for (int i = threadIdx.x; i < npx; i += blockDim.x) band_ids[i] = -1;
     __syncthreads();
-    // paint: a warp per box of this bin, its footprint rows inside the band
-    for (int j = off[bin] + warp; j < off[bin + 1]; j += nwarps) {
-      const int id = list[j];
+    // paint: a warp per box of this bin, its footprint rows inside the band; lane 0 caches the box
+    const int j0 = off[bin];
+    for (int j = j0 + warp; j < off[bin + 1]; j += nwarps) {
+      const int id = list[j], loc = j - j0;
       const regen_box& bx = boxes[id];
+      if (lane == 0 && loc < SB_CACHE) sbox[loc] = stitch_box(bx, id, F);
+      const int tag = loc < SB_CACHE ? loc : SB_CACHE + id;
       const int fw = bx.rotated ? bx.h : bx.w, fh = bx.rotated ? bx.w : bx.h;
       const int ra = max(bx.by, y0), rb = min(bx.by + fh, y0 + rows);
       for (int r = ra; r < rb; ++r)
-        for (int p = lane; p < fw; p += 32) band_ids[(r - y0) * bin_w + bx.bx + p] = id;
+        for (int p = lane; p < fw; p += 32) band_ids[(r - y0) * bin_w + bx.bx + p] = tag;
     }
     __syncthreads();
     // bin_w dividing the block: a thread keeps its column and steps rows (no division per pixel)
@@ -419,34 +445,32 @@ __global__ void __launch_bounds__(256) stitch_band_kernel(const uint8_t* frames,
     for (int i = threadIdx.x, yy = ys, x = xs; i < rows * bin_w; i += blockDim.x) {
       if (ystep == 0) { yy = i / bin_w; x = i - yy * bin_w; }
       const int y = y0 + yy;
-      const int32_t id = band_ids[i];
+      const int32_t tag = band_ids[i];
       const size_t px = ((size_t)bin * bin_h + y) * bin_w + x;
       if (mbits != nullptr) {   // bin_w % 32 == 0: a warp covers 32 consecutive pixels of one row
-        const uint32_t bits = __ballot_sync(0xffffffffu, id >= 0);
+        const uint32_t bits = __ballot_sync(0xffffffffu, tag >= 0);
         if (lane == 0) mbits[((size_t)bin * bin_h + y) * words + x / 32] = bits;
       }
-      map[px] = id;
       float v[3] = {0.f, 0.f, 0.f};
       int64_t d = -1;
-      if (id >= 0) {
-        const regen_box& bx = boxes[id];
-        const int p = x - bx.bx, q = y - bx.by;
-        const int sx = bx.rotated ? bx.x0 + q : bx.x0 + p;
-        const int sy = bx.rotated ? bx.y0 + bx.h - 1 - p : bx.y0 + q;
+      int32_t id = -1;
+      if (tag >= 0) {
+        const StitchBox b = tag < SB_CACHE ? sbox[tag] : stitch_box(boxes[tag - SB_CACHE], tag - SB_CACHE, F);
+        id = b.id;
+        const int sx = b.rot ? b.ax + y : b.ax + x;
+        const int sy = b.rot ? b.ay - x : b.ay + y;
         int cr, cg, cb;   // RGB8, or NV12 converted here (D19): the BT.601 conversion fused into the gather
-        frame_px(frames, oa.format, (int64_t)bx.stream * F + bx.frame, W, H, sx, sy, cr, cg, cb);
+        frame_px(frames, oa.format, b.fr, W, H, sx, sy, cr, cg, cb);
         v[0] = u8f[cr];
         v[1] = u8f[cg];
         v[2] = u8f[cb];
         if (oa.owner) {
-          const int32_t* ow = oa.owner + ((size_t)bx.stream * oa.F + bx.frame) * oa.GH * oa.GW;
-          if (ow[(sy / oa.mb) * oa.GW + sx / oa.mb] == id) {
-            const int64_t OW = (int64_t)oa.W * oa.s, OH = (int64_t)oa.H * oa.s;
-            d = ((((int64_t)bx.stream * oa.F + bx.frame) * OH + (int64_t)oa.s * sy) * OW + (int64_t)oa.s * sx) |
-                ((int64_t)bx.rotated << 62);
-          }
+          const int mx = mb16 ? sx >> 4 : sx / oa.mb, my = mb16 ? sy >> 4 : sy / oa.mb;
+          if (oa.owner[(int64_t)b.fr * gsz + my * oa.GW + mx] == id)
+            d = (((int64_t)b.fr * OH + (int64_t)oa.s * sy) * OW + (int64_t)oa.s * sx) | ((int64_t)b.rot << 62);
         }
       }
+      map[px] = id;
       if (oa.owner) oa.dst[px] = d;
       if (LAYOUT == 0) {
         T* o = out + px * 8;
