@@ -14,6 +14,7 @@ run() {   # name, args...
 run c2
 REGEN_PIPES=2 run c2_pipes2 --no-cpu-baseline
 run c2_nv12 --input nv12 --no-cpu-baseline
+run c2_u8out --out u8 --no-cpu-baseline
 run c1 --config c1 --no-cpu-baseline
 run c3 --config c3 --steps 5 --warmup 3 --no-cpu-baseline
 run c4g --config c4g --steps 5 --warmup 3 --no-cpu-baseline
@@ -23,6 +24,7 @@ for r in 5 10 15 20 25 35 50; do
 done
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > $O/${TAG}_bench_reference.json 2> $O/${TAG}_bench_reference.err
 echo "reference rc=$? $(head -c 200 $O/${TAG}_bench_reference.json)"
-timeout 1500 python tools/sbubd_study.py --shuffles 1000 > $O/${TAG}_sbubd.log 2>&1; echo "sbubd rc=$?"
-cp profiles/r02_sbubd_study.* $O/ 2>/dev/null
+if [ "${SBUBD:-0}" = "1" ]; then   # the packing study (packer unchanged since profiles/r02_sbubd_study.*)
+  timeout 1500 python tools/sbubd_study.py --shuffles 1000 > $O/${TAG}_sbubd.log 2>&1; echo "sbubd rc=$?"
+fi
 bash tools/gpu_profile.sh $TAG
