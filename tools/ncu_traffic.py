@@ -3,7 +3,7 @@
 names the launch tracer uses (regen_trace_*), written to profiles/ncu_traffic.json for bench.py's
 roofline `traffic` field.
 
-  python tools/ncu_traffic.py gpurun_out/prof.ncu-rep [--out profiles/ncu_traffic.json]
+  python tools/ncu_traffic.py gpurun_out/prof.ncu-rep|prof.raw.csv ... [--out profiles/ncu_traffic.json]
 """
 from __future__ import annotations
 
@@ -49,8 +49,11 @@ def main():
     a = ap.parse_args()
     acc: dict[str, list] = {}
     for rep in a.report:
-        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], check=True, capture_output=True,
-                             text=True).stdout
+        if rep.endswith(".csv"):   # an exported raw page (ncu -i <rep> --page raw --csv)
+            raw = open(rep).read()
+        else:
+            raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], check=True, capture_output=True,
+                                 text=True).stdout
         rows = list(csv.reader(io.StringIO(raw)))
         h, units = rows[0], rows[1]
         ki, ri, wi, ti = (h.index(x) for x in ("Kernel Name", "dram__bytes_read.sum", "dram__bytes_write.sum",
