@@ -346,6 +346,18 @@ def test_upsampler_tail_fold_matches_oracle_and_literal_path(s, C, monkeypatch):
     assert worst_fold <= TOL[True] and worst_lit <= TOL[True]
 
 
+def test_stitch_bin_with_more_boxes_than_the_smem_cache():
+    """A 1024 x 128 bin of one-MB boxes holds more than the stitch's 128-entry SMEM box cache: the boxes
+    past it are read from their records; every pixel still matches the oracle (fp32 tiny model)."""
+    wl = dataclasses.replace(synth.small(synth.CONFIGS["c1"], F=6), bin_w=1024, bin_h=128, pct=40.0,
+                             partition_mb=1, max_bins=8)
+    imp = synth.importance_maps(wl.S, wl.F, wl.GH, wl.GW, 31, "noisy")
+    o = _oracle_index(wl, imp)
+    per_bin = np.bincount(o["placement"][:, 0][o["placement"][:, 0] >= 0])
+    assert per_bin.max() > 128, per_bin
+    assert _check_pixels(wl, seed=31, kind="noisy") <= TOL[False]
+
+
 def test_no_selection_gives_the_pure_bilinear_frames():
     """k = 0: no region, no box, no bin; every HR pixel is the D10 bilinear value (the enhance call runs
     over zero bins)."""
