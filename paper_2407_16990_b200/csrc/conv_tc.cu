@@ -67,6 +67,7 @@ struct Params {
   const float* tbias;       // tail bias [3]
   int fout_mode, fOW;
   int ff_debug;             // timing experiments only (REGEN_FF_DEBUG): 1 = skip the combine, 2 = skip its stores
+  int npr;                  // ROLE_FOLDF: partial-sum rows in the SMEM ring (FF_NPR .. FF_NPR_MAX)
 };
 
 // ------------------------------------------------------------------------------- compile-time shape
@@ -139,8 +140,9 @@ __host__ __device__ constexpr int up_column(int n) {
 }
 
 // ------------------------------------------------------------------------------- kernel
-constexpr int FF_NPR = 4;   // ROLE_FOLDF: partial-sum rows held in SMEM for the fused combine (4 x 20.8 KB,
+constexpr int FF_NPR = 4;   // ROLE_FOLDF: partial-sum rows held in SMEM for the fused combine (at least 4 x 20.8 KB,
                             // leaving room for an 8-row input ring: the row loads are latency-bound)
+constexpr int FF_NPR_MAX = 6;
 constexpr int FF_W = 130;   // ring row width: 128 pixels + a zero column each side (the combine's x
                             // padding, so its 16-B loads need no bounds checks)
 
@@ -154,7 +156,7 @@ __global__ void __launch_bounds__(ROLE == ROLE_FOLDF ? NTHREADS + 256 : NTHREADS
   __shared__ __align__(8) uint64_t b_full[2], b_empty[2];
   __shared__ uint32_t tmem_base_sh;
   __shared__ __align__(16) float bias_sm[768];   // bias per accumulator column (all chunks)
-  __shared__ __align__(8) uint64_t prow_full[FF_NPR], prow_empty[FF_NPR];   // ROLE_FOLDF partial-sum rows
+  __shared__ __align__(8) uint64_t prow_full[FF_NPR_MAX], prow_empty[FF_NPR_MAX];   // ROLE_FOLDF partial-sum rows
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cin8 = S::HEAD ? 1 : C / 8;
@@ -186,7 +188,7 @@ __global__ void __launch_bounds__(ROLE == ROLE_FOLDF ? NTHREADS + 256 : NTHREADS
     // stores) and read by the three combines of rows r-1, r, r+1 (3 x 128 lane arrivals; band-edge
     // rows get the missing ones from the edge combines)
     if (S::FF)
-      for (int i = 0; i < FF_NPR; ++i) { mbar_init(&prow_full[i], 128); mbar_init(&prow_empty[i], 3 * 128); }
+      for (int i = 0; i < p.npr; ++i) { mbar_init(&prow_full[i], 128); mbar_init(&prow_empty[i], 3 * 128); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -207,7 +209,7 @@ __global__ void __launch_bounds__(ROLE == ROLE_FOLDF ? NTHREADS + 256 : NTHREADS
     bias_sm[n] = b;
   }
   if (S::FF) {   // the ring rows' zero columns (x = -1 and x = 128), never overwritten
-    for (int i = threadIdx.x; i < FF_NPR * (CP / 8) * 2; i += S::NT) {
+    for (int i = threadIdx.x; i < p.npr * (CP / 8) * 2; i += S::NT) {
       const int row = i / ((CP / 8) * 2), r2 = i - row * (CP / 8) * 2, pl = r2 >> 1, side = r2 & 1;
       *reinterpret_cast<uint4*>(pring + row * PROW_BYTES + (uint32_t)(pl * FF_W + side * (FF_W - 1)) * 16) =
           make_uint4(0, 0, 0, 0);
@@ -446,10 +448,10 @@ __global__ void __launch_bounds__(ROLE == ROLE_FOLDF ? NTHREADS + 256 : NTHREADS
             // partial-sum row j -> SMEM ring (bf16, masked: exactly the values ROLE_FOLD writes to
             // HBM); rows outside the bin are zero rows (the combine's zero padding)
             const uint32_t q = pbase + (uint32_t)j;
-            const uint32_t sl = q % FF_NPR;
+            const uint32_t sl = q % (uint32_t)p.npr;
             {
               const long long t0 = clock64();
-              mbar_wait(&prow_empty[sl], ((q / FF_NPR) & 1) ^ 1);
+              mbar_wait(&prow_empty[sl], ((q / (uint32_t)p.npr) & 1) ^ 1);
               if (p.prof) pwR += clock64() - t0;
             }
             uint8_t* rowp = pring + sl * PROW_BYTES + (uint32_t)(m + 1) * 16;
@@ -590,9 +592,9 @@ __global__ void __launch_bounds__(ROLE == ROLE_FOLDF ? NTHREADS + 256 : NTHREADS
           for (int d = 0; d < 3; ++d) {
             const uint32_t q = pbase + (uint32_t)(c - 1 + d);
             const long long t0 = clock64();
-            mbar_wait(&prow_full[q % FF_NPR], (q / FF_NPR) & 1);
+            mbar_wait(&prow_full[q % (uint32_t)p.npr], (q / (uint32_t)p.npr) & 1);
             if (p.prof) pwR += clock64() - t0;
-            rb[d] = pring + (q % FF_NPR) * PROW_BYTES + (uint32_t)(x + 1) * 16;
+            rb[d] = pring + (q % (uint32_t)p.npr) * PROW_BYTES + (uint32_t)(x + 1) * 16;
           }
           if (y < p.Hr && dst >= 0 && p.ff_debug != 1) {
             float acc[PS][PS][3];
@@ -623,7 +625,7 @@ __global__ void __launch_bounds__(ROLE == ROLE_FOLDF ? NTHREADS + 256 : NTHREADS
               if (c == 1 && d == 1) n = 2;
               if (c == S::BSTR && d == 1) n = 2;
               if (c == S::BSTR && d == 2) n = 3;
-              mbar_arrive_cnt(&prow_empty[(pbase + (uint32_t)(c - 1 + d)) % FF_NPR], n);
+              mbar_arrive_cnt(&prow_empty[(pbase + (uint32_t)(c - 1 + d)) % (uint32_t)p.npr], n);
             }
           }
         }
@@ -1059,7 +1061,14 @@ regen_status fold_fused_launch(const SRNet* net, const void* in, const uint32_t*
     p.ff_debug = e ? atoi(e) : 0;
   }
   const uint32_t grp_bytes = (uint32_t)(cv.cin / 8) * p.Wr * 16;   // G = 1
-  const size_t pring = (size_t)FF_NPR * (pl->cp / 8) * FF_W * 16;
+  // ring depths: the deepest partial-sum ring (the epilogue and the combines decoupled) that leaves
+  // room for >= 4 input rows in flight, else the shallowest
+  const size_t prow = (size_t)(pl->cp / 8) * FF_W * 16;
+  p.npr = FF_NPR;
+  for (int n = FF_NPR_MAX; n > FF_NPR; --n)
+    if (1024 + 4ull * grp_bytes + pl->b_bytes + n * prow <= 224 * 1024) { p.npr = n; break; }
+  if (const char* e = getenv("REGEN_FF_NPR")) p.npr = std::max(FF_NPR, std::min(FF_NPR_MAX, atoi(e)));   // A/B aid
+  const size_t pring = (size_t)p.npr * prow;
   int gslog = 3;
   while (gslog > 1 && 1024 + ((size_t)1 << gslog) * grp_bytes + pl->b_bytes + pring > 224 * 1024) --gslog;
   p.ngs = 1 << gslog;
