@@ -1,6 +1,6 @@
 """Full-size parity (BASELINE.json configs at their stated frame sizes, ratios and networks: C2 and C3
 whole; C4 and C5 as one selection group each — 8 of C4's 64 streams at 15 %, 2 of C5's 16 streams at
-its default ratio — the bench runs every group) in the launch configuration bench.py
+5 % — the bench runs every group) in the launch configuration bench.py
 times: two pipelines on two streams, the steps captured into one CUDA graph and replayed
 (paper_2407_16990_b200.schedule.PipelinedRunner). The index path (selection, regions, boxes, order,
 placements, owners) is compared bit-exactly with the oracle over the whole workload; the HR frames
