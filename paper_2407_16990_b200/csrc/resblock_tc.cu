@@ -4,14 +4,16 @@
 // Both convs use the sliding-window mapping of conv_tc.cu (kernel rows folded into N = 3*C, one MMA
 // per (dx, K-chunk pair) per input row, output-row accumulators in a TMEM ring at decreasing
 // columns). A work unit is a band of BR = 32 output rows of one bin:
-//   conv_a reads r rows y0-2 .. y1+1 (36 rows, bulk-copied in groups of G) and produces t rows
-//   y0-1 .. y1 (34 rows) into TMEM ring A; epilogue quad A (warps 2-5) applies bias/ReLU/mask and
-//   writes each t row into an SMEM ring in the UMMA operand layout (generic-proxy stores + proxy fence);
-//   conv_b consumes those t rows from SMEM into TMEM ring B; epilogue quad B (warps 6-9) adds the
-//   residual r and stores r'. The residual rows are bulk-copied into their own SMEM ring by warp 11
-//   (an L2 re-read of rows the producer loaded a few groups earlier), so no global-load latency sits
-//   on the epilogue's path; the occupancy words of a unit's rows are fetched once per unit.
-// Two issuing threads: warp 1 issues conv_a, warp 10 conv_b (each waits only on its own inputs).
+//   conv_a reads r rows y0-2 .. y1+1 (36 rows, bulk-copied in groups of G = 1 row) and produces t rows
+//   y0-1 .. y1 (34 rows) into TMEM ring A; the quad-A epilogue warps (warps 2-9: two groups of four
+//   taking alternate rows) apply bias/ReLU/mask and write each t row into an SMEM ring in the UMMA
+//   operand layout (generic-proxy stores + proxy fence); conv_b consumes those t rows from SMEM into
+//   TMEM ring B; the quad-B warps (10-17) add the residual r and store r'. The residual rows are
+//   bulk-copied into their own SMEM ring by warp 19 (an L2 re-read of rows the producer loaded a few
+//   rows earlier), so no global-load latency sits on the epilogue's path; the occupancy words of a
+//   unit's rows are fetched once per unit. Each epilogue releases its accumulator slot (TMEM loads,
+//   re-arm) before it waits for its t-ring / store slot.
+// Two issuing threads: warp 1 issues conv_a, warp 18 conv_b (each waits only on its own inputs).
 // Synchronisation is per group of G rows: r ring (in_full/in_empty), TMEM ring A and B
 // (acc*_full/acc*_empty), t ring (t_full by quad A, t_empty by tcgen05.commit), residual ring
 // (res_full by the bulk copy, res_empty by quad B).
