@@ -197,3 +197,14 @@ def test_global_topk_protocol_is_exact_over_ranks(world, k_frac):
     ref = oracle.select(imp, W, H, oracle.MODE_TOPK, k_total)
     np.testing.assert_array_equal(sel, ref)
     assert sel.sum() == min(k_total, imp.size)
+
+
+def test_bench_dominant_kernel_skips_one_cta_kernels():
+    """bench.py's roofline kernel: the largest summed device time among the kernels that spread over the
+    GPU; a one-CTA kernel (the packer of a C4 group, 12 ms on one SM) does not displace the residual
+    block, and is chosen only when nothing else ran."""
+    import bench
+    kern = {"pack": [8, 93.5], "resblock": [64, 40.7], "scatter_bilinear": [8, 16.4], "select": [8, 4.1]}
+    assert bench.dominant_kernel(kern) == "resblock"
+    assert bench.dominant_kernel({"pack": [1, 2.0], "select": [1, 1.0]}) == "pack"
+    assert bench.dominant_kernel({"conv_fold_frames": [1, 0.2], "resblock": [8, 0.72]}) == "resblock"
