@@ -349,7 +349,7 @@ struct BL {
 };
 
 template <int S, typename TO>
-__global__ void __launch_bounds__(32 * BL_WARPS) bilinear_kernel(ScatterArgs a, int nwc) {
+__global__ void __launch_bounds__(32 * BL_WARPS, 8) bilinear_kernel(ScatterArgs a, int nwc) {
   extern __shared__ __align__(16) uint8_t bsm[];
   using G = BL<S, TO>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
