@@ -403,7 +403,7 @@ __device__ __forceinline__ StitchBox stitch_box(const regen_box& bx, int id, int
 }
 
 template <typename T, int LAYOUT>
-__global__ void __launch_bounds__(256) stitch_band_kernel(const uint8_t* frames, const regen_box* boxes,
+__global__ void __launch_bounds__(256, 8) stitch_band_kernel(const uint8_t* frames, const regen_box* boxes,
                                                           const int32_t* off, const int32_t* list,
                                                           const int32_t* num_bins, int max_bins, int bin_w, int bin_h,
                                                           int F, int W, int H, int32_t* map, T* out, uint32_t* mbits,
