@@ -522,9 +522,14 @@ def main() -> None:
             else:
                 roof = {"kernel": dom, "bound": None, "achieved": None, "peak": None, "unit": None, "frac": None,
                         "traffic": load_traffic(dom), "launch_ms_mean": dom_ms}
+            occ_bin = job_box_px / max(job_bins * wl.bin_w * wl.bin_h, 1)
+            if roof.get("frac") is not None and occ_bin > 0:
+                # the kernel computes every pixel of the bins it covers: the same time over the FLOPs of
+                # the bin pixels (frac / box-over-bin fill) is the tensor-core work rate it executes
+                roof["frac_bin_px"] = roof["frac"] / occ_bin
             roof.update({"flops_per_step": flops_step, "box_px_per_step": job_box_px,
                          "occupy_ratio_sel_over_box": job_sel_px / max(job_box_px, 1),
-                         "occupy_ratio_box_over_bin": job_box_px / max(job_bins * wl.bin_w * wl.bin_h, 1),
+                         "occupy_ratio_box_over_bin": occ_bin,
                          "sr_network_tflops": box_px * fp / (stage[2] / 1000.0) / 1e12 if stage[2] else None})
         # HBM-bound kernels against the measured copy bandwidth: algorithmic bytes per launch / mean
         # launch time (concurrent replay: includes co-scheduling with the SR stream)
