@@ -465,8 +465,18 @@ __global__ void __launch_bounds__(ROLE == ROLE_FOLDF ? NTHREADS + 256 : NTHREADS
                 const int c0 = h ? H1 : 0, c1 = h ? CP : H1;
                 uint32_t r[H1];
 #pragma unroll
-                for (int c = 0; c < H1; c += 16)
-                  if (c0 + c < c1) tmem_ld16(taddr + (uint32_t)(c0 + c), r + c);
+                for (int c = 0; c < H1; c += 16) {
+                  if (c0 + c >= c1) continue;
+                  if (PS == 3 && c0 + c == 64) {   // 75 partial channels of 80: columns 64..74 only
+                    tmem_ld8(taddr + 64u, r + c);
+                    tmem_ld2(taddr + 72u, r + c + 8);
+                    tmem_ld1(taddr + 74u, r + c + 10);
+#pragma unroll
+                    for (int e = 11; e < 16; ++e) r[c + e] = 0u;   // padding channels, never read
+                  } else {
+                    tmem_ld16(taddr + (uint32_t)(c0 + c), r + c);
+                  }
+                }
                 tmem_ld_wait();
 #pragma unroll
                 for (int g = 0; g < H1 / 8; ++g) {
@@ -541,7 +551,15 @@ __global__ void __launch_bounds__(ROLE == ROLE_FOLDF ? NTHREADS + 256 : NTHREADS
 #pragma unroll
             for (int e = 0; e < 16; ++e) z[e] = 0.f;
 #pragma unroll
-            for (int c = 0; c < CP; c += 16) tmem_st16(taddr + (uint32_t)c, S::BIAS_IN_ACC ? bias_sm + c : z);
+            for (int c = 0; c < CP; c += 16) {
+              if (S::FF && PS == 3 && c == 64) {   // the 5 padding columns accumulate zeros: never re-armed
+                tmem_st8(taddr + 64u, bias_sm + 64);
+                tmem_st2(taddr + 72u, bias_sm + 72);
+                tmem_st1(taddr + 74u, bias_sm + 74);
+              } else {
+                tmem_st16(taddr + (uint32_t)c, S::BIAS_IN_ACC ? bias_sm + c : z);
+              }
+            }
           }
           if (p.prof) pwS += clock64() - tst;
         }
